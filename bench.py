@@ -1,0 +1,406 @@
+"""Benchmark: pseudo-transient LOD step throughput (interior grid-point updates/s, fp64).
+
+Workload (BASELINE.json metric is quoted at 1/2/4/8 B200 on the sharded config): config 4,
+a 10,000-atom synthetic protein on a 513^3 grid (h = 0.3 A, eps 2/80, 0.15 M), LODIE2,
+dt = 0.5.  One bench "step" = one LODIE2 time step over the whole grid (flow + source +
+three implicit line sweeps).  Fields are 1.1 GB each (>> 126 MB L2), so no L2 flush is
+needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c3] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU): every rank marches its own copy (replicas, weak
+scaling); the slab-sharded single-grid solve is the next multi-GPU step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_LOD = 48  # algorithmic bytes per interior update per LOD step
+BYTES_SWEEP = 16  # one fp64 read + one fp64 write per interior node per sweep launch
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.05)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.05)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except (ValueError, IndexError):
+                continue
+            for name, val in zip(names, f[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_problem(cfg_key):
+    import paper_1410_2788_b200 as pb
+    from paper_1410_2788_b200.configs import CONFIGS, cubic_box, kappa_bar, synthetic_atoms
+    from paper_1410_2788_b200.problem import assemble_on_grid
+
+    c = CONFIGS[cfg_key]
+    atoms = synthetic_atoms(c.n_atoms, c.ball_radius, c.seed)
+    lo, hi = cubic_box(atoms, c.n, c.h)
+    grid = pb.make_grid(lo, hi, c.h)
+    system = pb.MolecularSystem([pb.Atom(a[:3], a[3], a[4]) for a in atoms], label=c.name)
+    t0 = time.perf_counter()
+    p = assemble_on_grid(system, grid, kappa_bar(c.ionic_strength), c.eps_m, c.eps_s)
+    import torch
+
+    torch.cuda.synchronize()
+    return c, p, time.perf_counter() - t0
+
+
+def march_desc(p, c, nsteps):
+    from paper_1410_2788_b200 import _native as nat
+    from paper_1410_2788_b200.schemes import device_problem
+
+    dp = device_problem(p)
+    w0, w1 = dp.work_pair()
+    d = nat.PbgMarchDesc()
+    d.grid = dp.gs
+    d.pal = dp.pal
+    d.variant = nat.VARIANT_IDS[c.variant]
+    d.dt, d.alpha, d.divergence_threshold = c.dt, p.alpha, 1e12
+    d.nsteps, d.check_divergence = nsteps, 1
+    d.codes, d.rho = dp.codes.data_ptr(), dp.rho.data_ptr()
+    d.initial = w0.data_ptr()  # protein default: zero interior, Dirichlet faces
+    d.work[0], d.work[1] = w0.data_ptr(), w1.data_ptr()
+    return d, dp, (w0, w1)
+
+
+def run_march(d, nsteps):
+    from paper_1410_2788_b200 import _native as nat
+
+    d.nsteps = nsteps
+    taken, dstep, slot = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    ms = ctypes.c_float()
+    nat.check(nat.lib().pbg_march(ctypes.byref(d), ctypes.byref(taken), ctypes.byref(dstep),
+                                  ctypes.byref(slot), ctypes.byref(ms), nat.stream_ptr()))
+    if taken.value != nsteps or dstep.value:
+        raise RuntimeError(f"march diverged at step {dstep.value}")
+    return ms.value
+
+
+def faces_packed(arr):
+    return np.concatenate([arr[0].ravel(), arr[-1].ravel(), arr[:, 0].ravel(),
+                           arr[:, -1].ravel(), arr[:, :, 0].ravel(), arr[:, :, -1].ravel()])
+
+
+def e2e_measure(p, c, dp, nsteps):
+    """Same metric through the C ABI with HOST buffers (pbg_march_host): uploads codes,
+    sparse source and packed faces from pinned memory, marches, downloads the final field."""
+    import torch
+
+    from paper_1410_2788_b200 import _native as nat
+
+    g = p.grid
+    codes_h = torch.empty(dp.codes.numel(), dtype=torch.uint8, pin_memory=True)
+    codes_h.copy_(dp.codes)
+    rho = p.rho._dev
+    n0, n1, n2 = g.shape
+    pitch = dp.gs.pitch
+    rd = rho.view(n0, n1, pitch)[:, :, nat.PBG_OFFSET:nat.PBG_OFFSET + n2]
+    flat = torch.nonzero(rd.reshape(-1)).reshape(-1)
+    idx_h = flat.cpu().numpy().astype(np.int64)
+    val_h = rd.reshape(-1)[flat].cpu().numpy()
+    bnd = dp.bnd.view(n0, n1, pitch)[:, :, nat.PBG_OFFSET:nat.PBG_OFFSET + n2]
+    fc = torch.cat([bnd[0].reshape(-1), bnd[-1].reshape(-1), bnd[:, 0].reshape(-1),
+                    bnd[:, -1].reshape(-1), bnd[:, :, 0].reshape(-1), bnd[:, :, -1].reshape(-1)])
+    faces_h = torch.empty(fc.numel(), dtype=torch.float64, pin_memory=True)
+    faces_h.copy_(fc)
+    out_h = torch.empty((n0, n1, n2), dtype=torch.float64, pin_memory=True)
+    desc = nat.PbgMarchDesc()
+    desc.grid = dp.gs
+    desc.pal = dp.pal
+    desc.variant = nat.VARIANT_IDS[c.variant]
+    desc.dt, desc.alpha, desc.divergence_threshold = c.dt, p.alpha, 1e12
+    desc.nsteps, desc.check_divergence = nsteps, 1
+    taken, dstep = ctypes.c_int32(), ctypes.c_int32()
+    ms = ctypes.c_float()
+
+    def call():
+        nat.check(nat.lib().pbg_march_host(
+            ctypes.byref(desc), codes_h.data_ptr(), len(idx_h), idx_h.ctypes.data,
+            val_h.ctypes.data, faces_h.data_ptr(), None, out_h.data_ptr(), ctypes.byref(taken),
+            ctypes.byref(dstep), ctypes.byref(ms), nat.stream_ptr()))
+
+    call()  # warm the allocator pool
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    call()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    h2d = codes_h.numel() + idx_h.nbytes + val_h.nbytes + faces_h.numel() * 8
+    d2h = out_h.numel() * 8
+    return wall, h2d, d2h, float(np.isfinite(out_h[n0 // 2].numpy()).all())
+
+
+def oracle_slab(p, dp, nplanes):
+    """CPU oracle problem for planes i < nplanes of the device problem (test/baseline
+    infrastructure): same codes, source and faces; plane nplanes-1 acts as a Dirichlet face."""
+    import torch
+
+    from oracle import pbs_oracle as O
+    from paper_1410_2788_b200 import _native as nat
+
+    g = p.grid
+    n0, n1, n2 = g.shape
+    pitch = dp.gs.pitch
+    sl = slice(nat.PBG_OFFSET, nat.PBG_OFFSET + n2)
+    codes = dp.codes.view(n0, n1, pitch)[:nplanes, :, sl].cpu().numpy()
+    rho = dp.rho.view(n0, n1, pitch)[:nplanes, :, sl].cpu().numpy().copy()
+    bv = dp.bnd.view(n0, n1, pitch)[:nplanes, :, sl].cpu().numpy().copy()
+    rho[-1] = 0.0
+    eps = dp.pal.as_tuple()[0]
+    k2p = dp.pal.as_tuple()[1]
+    pick = lambda bit, pal: np.where((codes & bit) != 0, pal[1], pal[0])
+    eh = (pick(2, eps[0])[1:], pick(4, eps[1])[:, 1:], pick(8, eps[2])[:, :, 1:])
+    k2 = pick(1, k2p)
+    region = O.ORegion(pick(1, (eps[0][0], eps[0][1])), eh, k2)
+    og = O.OGrid(g.lo, g.h, (nplanes, n1, n2))
+    init = np.zeros(og.shape)
+    O.apply_faces(init, bv)
+    del torch
+    return O.OProblem(og, region, rho, np.zeros(og.shape), bv, p.alpha, init)
+
+
+def cpu_oracle_rate(p, dp, c, nplanes=65, steps=1):
+    from oracle import pbs_oracle as O
+
+    op = oracle_slab(p, dp, nplanes)
+    st = O.OStepper(op, c.variant, c.dt)
+    u = op.initial.copy()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        u = st.step(u)
+    wall = time.perf_counter() - t0
+    nint = (nplanes - 2) * (p.grid.ny - 2) * (p.grid.nz - 2)
+    return nint * steps / wall, nint, wall
+
+
+def profiled_kernels(d, nsteps):
+    from paper_1410_2788_b200 import _native as nat
+
+    lib = nat.lib()
+    lib.pbg_set_profiling(1)
+    run_march(d, nsteps)
+    ms = (ctypes.c_double * 3)()
+    n = (ctypes.c_int64 * 3)()
+    lib.pbg_get_profile(ms, n)
+    lib.pbg_set_profiling(0)
+    return [ms[a] / max(1, n[a]) for a in range(3)], [int(n[a]) for a in range(3)]
+
+
+def ncu_traffic(config_name, axis):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get(config_name, {}).get(str(axis))
+    except Exception:
+        return None
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+
+    if args.impl == "reference":
+        return reference_arm(args, world, rank)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    c, p, t_asm = build_problem(args.config)
+    nint = (c.n - 2) ** 3
+    d, dp, keep = march_desc(p, c, args.steps)
+    run_march(d, max(3, args.warmup))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms = run_march(d, args.steps)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = nint * args.steps * world / (ms_max / 1e3)
+
+    per_ms, launches = profiled_kernels(d, min(args.steps, 20))
+    dom = int(np.argmax(per_ms))
+    peak, peak_kind = peaks()
+    achieved = BYTES_SWEEP * nint / (per_ms[dom] / 1e3) / 1e9
+    step_gbs = BYTES_LOD * nint / (ms_max / args.steps / 1e3) / 1e9
+
+    e2e = None
+    if not args.no_e2e:
+        wall, h2d, d2h, ok = e2e_measure(p, c, dp, args.steps)
+        e2e = {"value": nint * args.steps / wall, "unit": "grid-point updates/s",
+               "h2d_bytes_per_step": int(h2d / args.steps),
+               "d2h_bytes_per_step": int(d2h / args.steps),
+               "note": f"pbg_march_host: {args.steps}-step march from pinned host buffers "
+                       "(codes, sparse source, packed faces) incl. allocation, H2D, D2H"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, nn, wall = cpu_oracle_rate(p, dp, c)
+        cpu = {"value": rate, "unit": "grid-point updates/s", "cores": 1, "kind": "port",
+               "sample": f"1 {c.variant} step of {c.name} restricted to planes i<65 "
+                         f"({nn} interior nodes, {wall:.1f} s), numpy oracle port of "
+                         "pbsplit Stepper"}
+    clocks = clk.summary()
+    if rank == 0:
+        line = {
+            "metric": "LOD grid-point updates/s (fp64)",
+            "value": value,
+            "unit": "grid-point updates/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(3, args.warmup),
+            "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded generator, configs.py)",
+            "config": {"workload": c.name, "grid": [c.n] * 3, "atoms": c.n_atoms, "h": c.h,
+                       "variant": c.variant, "dt": c.dt, "interior_nodes": nint,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "fields 1.1 GB >> L2, no flush", "assembly_s": round(t_asm, 3)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(c.name, dom),
+                         "kernel": ["sweep_axis0 (strided)", "sweep_axis1 (strided)",
+                                    "sweep_axis2 (contiguous)"][dom],
+                         "kernel_ms": per_ms, "peak_kind": peak_kind,
+                         "step_GBps_48B": step_gbs, "step_frac": step_gbs / peak},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 3 * args.steps + 1,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def reference_arm(args, world, rank):
+    """CPU reference arm: the numpy oracle port of pbsplit's Stepper (the reference itself
+    is Python and cannot travel to the box), on a bounded sample of the same workload."""
+    if rank != 0:
+        return
+    import torch
+
+    torch.cuda.set_device(0)
+    c, p, _ = build_problem(args.config)  # device assembly only to produce identical inputs
+    from paper_1410_2788_b200.schemes import device_problem
+    from oracle import pbs_oracle as O
+
+    dp = device_problem(p)
+    nplanes = 65
+    op = oracle_slab(p, dp, nplanes)
+    st = O.OStepper(op, c.variant, c.dt)
+    u = op.initial.copy()
+    steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        u = st.step(u)
+    wall = time.perf_counter() - t0
+    nint = (nplanes - 2) * (c.n - 2) ** 2
+    v = nint * steps / wall
+    line = {"metric": "LOD grid-point updates/s (fp64)", "value": v,
+            "unit": "grid-point updates/s", "n_gpus": world, "steps": steps, "warmup": 0,
+            "ms_per_step": wall / steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
+            "config": {"workload": c.name, "grid": [c.n] * 3, "variant": c.variant,
+                       "dt": c.dt, "sample_planes": nplanes},
+            "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "grid-point updates/s", "cores": 1,
+                             "kind": "port",
+                             "sample": f"{steps} {c.variant} step(s) of {c.name} restricted "
+                                       f"to planes i<{nplanes} ({nint} interior nodes)"},
+            "e2e": {"value": v, "unit": "grid-point updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

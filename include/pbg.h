@@ -164,6 +164,12 @@ typedef struct pbg_march_desc {
 PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken, int32_t* diverged_step,
                       int32_t* result_slot, float* device_ms, void* stream);
 
+/* Per-sweep-kernel timing (CUDA events around every launch inside pbg_march, on the
+ * launching stream).  pbg_set_profiling(1) enables and resets the accumulators;
+ * pbg_get_profile returns the summed milliseconds and launch counts per sweep axis. */
+PBG_API int pbg_set_profiling(int32_t on);
+PBG_API int pbg_get_profile(double axis_ms[3], int64_t launches[3]);
+
 /* Same march from HOST buffers: uploads the inputs, marches, downloads the final field.
  *   codes_pitched_host  uint8 codes in the pitched layout (pbg_layout nelem bytes)
  *   rho_nnz/idx/val     the deposited source as (flat C-order node index, value) pairs

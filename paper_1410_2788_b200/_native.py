@@ -96,6 +96,8 @@ _SIGS = {
     "pbg_axpby": ([_P(PbgGrid), c_double, c_void_p, c_double, c_void_p, c_void_p, c_void_p],
                   ctypes.c_int),
     "pbg_maxabs": ([_P(PbgGrid), c_void_p, _P(c_double), c_void_p], ctypes.c_int),
+    "pbg_set_profiling": ([c_int32], ctypes.c_int),
+    "pbg_get_profile": ([_P(c_double), _P(c_int64)], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -466,7 +466,7 @@ PBG_API int pbg_energy_atoms(const pbg_grid* g, const double* atoms, int32_t nat
   Layout L = make_layout(g);
   double* out = nullptr;
   PBG_CUDA(cudaMallocAsync(&out, sizeof(double), st));
-  k_energy_atoms<<<1, 1024, 0, st>>>(L, g->lo[0], g->lo[1], g->lo[2], g->h, atoms, natoms,
+  k_energy_atoms<<<1, kRedThreads, 0, st>>>(L, g->lo[0], g->lo[1], g->lo[2], g->h, atoms, natoms,
                                      phi_m_a, phi_m_b, ca, cb, phi_0_a, phi_0_b, cc, cd,
                                      out);
   PBG_LAUNCH_CHECK("k_energy_atoms");

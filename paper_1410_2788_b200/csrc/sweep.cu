@@ -658,9 +658,30 @@ __global__ void k_faces_bad(const Layout L, const double* x, double thr, int* fl
   }
 }
 
+static bool g_profile = false;
+static double g_prof_ms[3] = {0, 0, 0};
+static long long g_prof_n[3] = {0, 0, 0};
+
 }  // namespace pbg
 
 using namespace pbg;
+
+extern "C" PBG_API int pbg_set_profiling(int32_t on) {
+  g_profile = on != 0;
+  for (int a = 0; a < 3; ++a) {
+    g_prof_ms[a] = 0.0;
+    g_prof_n[a] = 0;
+  }
+  return PBG_OK;
+}
+
+extern "C" PBG_API int pbg_get_profile(double axis_ms[3], int64_t launches[3]) {
+  for (int a = 0; a < 3; ++a) {
+    if (axis_ms) axis_ms[a] = g_prof_ms[a];
+    if (launches) launches[a] = g_prof_n[a];
+  }
+  return PBG_OK;
+}
 
 extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
                                  int32_t* diverged_step, int32_t* result_slot,
@@ -764,6 +785,7 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
   cudaEvent_t e0, e1;
   PBG_CUDA(cudaEventCreate(&e0));
   PBG_CUDA(cudaEventCreate(&e1));
+  std::vector<cudaEvent_t> kev;  // per-launch events when profiling is on
   PBG_CUDA(cudaEventRecord(e0, st));
   for (int s = 1; s <= d->nsteps; ++s) {
     const double* X = st_idx < 0 ? d->initial : d->work[st_idx];
@@ -782,7 +804,19 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
         a.acc = A;
         a.dst = A;
       }
+      if (g_profile) {
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        cudaEventRecord(ev, st);
+        kev.push_back(ev);
+      }
       rc = launch_sweep(a, axis, st);
+      if (g_profile) {
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        cudaEventRecord(ev, st);
+        kev.push_back(ev);
+      }
       if (rc) {
         cudaFreeAsync(dflag, st);
         return rc;
@@ -799,6 +833,14 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  for (size_t q = 0; q + 1 < kev.size(); q += 2) {
+    float kms = 0.f;
+    cudaEventElapsedTime(&kms, kev[q], kev[q + 1]);
+    const int axis = (int)((q / 2) % 3);
+    g_prof_ms[axis] += kms;
+    g_prof_n[axis] += 1;
+  }
+  for (auto ev : kev) cudaEventDestroy(ev);
   int taken = d->nsteps;
   if (d->check_divergence && dstep != INT_MAX) {
     taken = dstep;
