@@ -343,7 +343,8 @@ PBG_API int pbg_layout(int32_t n0, int32_t n1, int32_t n2, int64_t* pitch, int64
   if (n0 < 3 || n1 < 3 || n2 < 3) return fail(PBG_E_INVALID, "every axis needs >= 3 nodes");
   const int64_t p = ((int64_t)n2 + kOff + 31) / 32 * 32;
   if (pitch) *pitch = p;
-  if (nelem) *nelem = (int64_t)n0 * n1 * p;
+  // +64 elements of slack: tile loads may read a few padding columns past the last row
+  if (nelem) *nelem = (int64_t)n0 * n1 * p + 64;
   return PBG_OK;
 }
 
@@ -569,7 +570,7 @@ extern "C" PBG_API int pbg_march_host(const pbg_march_desc* t, const uint8_t* co
     pool_set = true;
   }
   Layout L = make_layout(&t->grid);
-  const size_t nelem = (size_t)L.n0 * L.n1 * L.pitch;
+  const size_t nelem = (size_t)L.n0 * L.n1 * L.pitch + 64;  // pbg_layout's nelem
   const size_t nf = (size_t)face_count(L);
   uint8_t* codes = nullptr;
   double *rho = nullptr, *w0 = nullptr, *w1 = nullptr, *init = nullptr, *faces = nullptr;

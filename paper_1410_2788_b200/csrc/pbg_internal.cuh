@@ -69,4 +69,22 @@ __device__ __forceinline__ double sinh_flow(double w, double decay, double pm) {
   return pm != 1.0 ? __dmul_rn(pm, out) : out;
 }
 
+// Same map as sinh_flow, evaluated as log(((1+d)E + (1-d)) / ((1-d)E + (1+d))), E = exp(w):
+// one exp, one division and one log instead of tanh + atanh (~2x fewer instructions).  For
+// |w| > 38, tanh(w/2) rounds to +-1 in fp64 and the reference returns +-2*atanh(d) (`sat`,
+// precomputed on the host).  Agrees with sinh_flow to ~1e-16 absolute.
+__device__ __forceinline__ double sinh_flow_fast(double w, double d, double sat, double pm) {
+  double out;
+  if (d >= 1.0) {
+    out = w;
+  } else if (fabs(w) > 38.0) {
+    out = copysign(sat, w);
+  } else {
+    const double E = exp(w);
+    const double opd = 1.0 + d, omd = 1.0 - d;
+    out = log(fma(opd, E, omd) / fma(omd, E, opd));
+  }
+  return pm != 1.0 ? pm * out : out;
+}
+
 }  // namespace pbg

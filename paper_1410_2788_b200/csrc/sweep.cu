@@ -6,27 +6,30 @@
 // Every implicit sweep solves (1 - f*d2_a) x = rhs on all interior lines of axis a, where
 // the tridiagonal rows are  sub = -f*e_minus, diag = 1 + f*(e_plus + e_minus),
 // sup = -f*e_plus  (tridiag.py:165, 179-181), with the static Dirichlet fold-ins on the
-// first/last row (tridiag.py:193-202).  Instead of the reference's single serial Thomas per
-// line with stored LU factors (3 x 8 B/node of coefficient traffic per sweep), each line is
-// split into P segments of S rows handled by P threads:
+// first/last row (tridiag.py:193-202).  The reference runs one serial Thomas per line with
+// stored LU factors (3 x 8 B/node of coefficient traffic per sweep).  Here each line is split
+// into 32 segments of S rows (S = ceil(m/32)), one thread per segment:
 //
-//   * rows j < S-1 of a segment are "inner"; row S-1 is a separator t_k.  Inner unknowns are
-//     x_j = y_j + alpha_j * t_{k-1} + beta_j * t_k (three Thomas solves of the segment block
-//     sharing one elimination, coefficients recomputed from the 1-byte node codes);
-//   * the separators obey a diagonally dominant tridiagonal "reduced" system, solved by
-//     parallel cyclic reduction (warp shuffles for the contiguous axis, shared memory for the
-//     strided axes);
-//   * inner values are then reconstructed in registers.
+//   * rows j < S-1 of a segment are "inner", row S-1 is a separator t_k; inner unknowns are
+//     x_j = y_j + alpha_j * t_{k-1} + beta_j * t_k  (one elimination, three right-hand sides);
+//   * the 32 separators of a line satisfy a diagonally dominant tridiagonal "reduced" system,
+//     solved by parallel cyclic reduction (5 steps: warp shuffles on the contiguous axis,
+//     shared memory on the strided axes);
+//   * alpha/beta and the LU factors of a segment depend only on the coefficient codes, so a
+//     segment whose S nodes all carry the same dielectric ("uniform", >90% of segments in the
+//     protein configs) reads them from a per-axis table built once per launch: 5 fp64 ops per
+//     node and no reciprocal.  Other segments ("general") eliminate on the fly with their
+//     per-row state in shared memory and L1-resident local arrays.
 //
-// The result equals the reference's Thomas solution up to fp64 reassociation (the system is
-// strictly diagonally dominant; see DESIGN.md for the measured 1e-15-level agreement).
+// Data movement: every block stages its lines through shared memory with asynchronous copies
+// (LDGSTS, the whole tile in flight at once): strided axes stage a tile of 8 adjacent k
+// columns x the whole line (each row segment 64 contiguous bytes), the contiguous axis one row
+// per warp.  The prologue is applied in the staging pass, the line is solved from shared
+// memory, and the epilogue runs in the coalesced store pass.  Geometry (S, 32 segments, 8
+// columns) is compile time, offsets are 32-bit; the transcendental prologue / epilogue live in
+// rolled loops so the unrolled solver stays small.
 //
-// Strided axes (0 and 1): block = LB adjacent k columns x P segments.  Each warp row reads
-// LB consecutive doubles of one grid row (coalesced 64-256 B), no transposition.
-// Contiguous axis (2): one warp per line; the row is staged in shared memory with a padded
-// (bank-conflict-free) segment layout, lane = segment, PCR via shuffles.
-//
-// Prologue / epilogue fusions (all per node, in registers):
+// Prologue / epilogue fusions:
 //   PRO_FLOW  w = pm*flow(u)         LODIE1/LODCN1 first sweep, MAOS branches
 //   PRO_SRC   w = u + dta*rho        LODIE2/LODCN2 first sweep
 //   CN        rhs += (cn_f/h^2)*delta2(w) along the sweep axis
@@ -56,6 +59,9 @@ enum {
   EPI_MAOS2 = 8
 };
 
+constexpr int kSeg = 32;   // segments per line
+constexpr int kCols = 8;   // k columns per strided tile (64-byte row segments)
+
 struct AxisCoef {
   double diag[4];  // [em*2 + ep]  1 + f*(e_plus + e_minus)
   double sub[2];   // [em]         -f*e_minus
@@ -64,6 +70,14 @@ struct AxisCoef {
   double fhi[2];   // [ep]         f*e_plus    (high fold)
   double eps[2];   // palette (CN stencil)
 };
+
+// Uniform-segment tables: tab[((type*2 + v)*5 + q)*kTabRows + j], type 0 = interior segment,
+// 1 = first segment of a line (row 0 has no sub-diagonal), 2 = last segment whose separator is
+// the padding row m (its last inner row is row m-1, no super-diagonal); q = inv, g = a*inv,
+// cp, alpha, beta.
+constexpr int kTabRows = 32;
+constexpr int kTabDoubles = 3 * 2 * 5 * kTabRows;
+enum { TQ_INV = 0, TQ_G = 1, TQ_CP = 2, TQ_AL = 3, TQ_BE = 4 };
 
 struct SweepArgs {
   Layout L;
@@ -74,6 +88,7 @@ struct SweepArgs {
   const double* rho;
   double* dst;
   const double* acc;
+  const double* tab;
   AxisCoef co;
   int cn;
   double cnc;  // cn_f / h^2
@@ -82,6 +97,7 @@ struct SweepArgs {
   int has_extra;
   double extra;
   double decay0, decay1;  // flow decay for solute-bit 0 / 1
+  double sat0, sat1;      // 2*atanh(decay)
   double pm;
   int epi;
   double epi_coef;
@@ -91,17 +107,36 @@ struct SweepArgs {
   int check;
 };
 
-__device__ __forceinline__ double pro_val(const SweepArgs& a, double v, uint32_t c,
-                                          long long off) {
-  if (a.pro == PRO_FLOW) return sinh_flow(v, (c & 1u) ? a.decay1 : a.decay0, a.pm);
-  if (a.pro == PRO_SRC && (c & 16u)) return __dadd_rn(v, __dmul_rn(a.pro_coef, a.rho[off]));
-  return v;
+// Asynchronous global->shared copies (LDGSTS): issued back to back, no register round trip.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// Which second tile the epilogue needs: 0 none, 1 the raw field (AOS0), 2 the accumulator.
+__host__ __device__ __forceinline__ int epi_needs(int epi) {
+  return epi == EPI_AOS0 ? 1
+                         : ((epi == EPI_AOS1 || epi == EPI_AOS2 || epi == EPI_MAOS1 ||
+                             epi == EPI_MAOS2)
+                                ? 2
+                                : 0);
 }
 
-// Face value seen by the CN stencil: after a flow stage the reference re-applies the
-// boundary (schemes.py:280-283), otherwise the running field's own faces are read.
-__device__ __forceinline__ double face_val(const SweepArgs& a, long long off) {
-  return a.pro == PRO_FLOW ? a.bnd[off] : a.src[off];
+__device__ __forceinline__ double flow_at(const SweepArgs& a, double w, uint32_t c, double pm) {
+  return (c & 1u) ? sinh_flow_fast(w, a.decay1, a.sat1, pm)
+                  : sinh_flow_fast(w, a.decay0, a.sat0, pm);
+}
+
+__device__ __forceinline__ double pro_val(const SweepArgs& a, double v, uint32_t c,
+                                          const double* rho_at) {
+  if (a.pro == PRO_FLOW) return flow_at(a, v, c, a.pm);
+  if (a.pro == PRO_SRC && (c & 16u)) return __dadd_rn(v, __dmul_rn(a.pro_coef, *rho_at));
+  return v;
 }
 
 __device__ __forceinline__ void row_coefs(const AxisCoef& co, int i, int m, uint32_t em,
@@ -117,39 +152,45 @@ __device__ __forceinline__ void row_coefs(const AxisCoef& co, int i, int m, uint
   bv = em ? (ep ? co.diag[3] : co.diag[2]) : (ep ? co.diag[1] : co.diag[0]);
 }
 
-// rhs of row i from the stage field w (wm, wc, wp = w at rows i-1, i, i+1).
-__device__ __forceinline__ double row_rhs(const SweepArgs& a, int i, uint32_t c, uint32_t em,
-                                          uint32_t ep, double wm, double wc, double wp,
-                                          long long off, double blo, double bhi) {
+// rhs of row i from the stage field (wm, wc, wp = w at rows i-1, i, i+1); schemes.py:290-297
+// and the fold-ins of tridiag.py:216-217.
+template <bool CN>
+__device__ __forceinline__ double row_rhs(const SweepArgs& a, bool row0, bool rowlast,
+                                          uint32_t c, uint32_t em, uint32_t ep, double wm,
+                                          double wc, double wp, const double* rho_at,
+                                          double blo, double bhi) {
   double r = wc;
-  if (a.cn) {
+  if (CN) {
     const double epv = ep ? a.co.eps[1] : a.co.eps[0];
     const double emv = em ? a.co.eps[1] : a.co.eps[0];
     const double d2 =
         __dadd_rn(__dmul_rn(epv, __dsub_rn(wp, wc)), __dmul_rn(emv, __dsub_rn(wm, wc)));
     r = __dadd_rn(r, __dmul_rn(a.cnc, d2));
   }
-  if (a.has_extra && (c & 16u)) r = __dadd_rn(r, __dmul_rn(a.extra, a.rho[off]));
-  if (i == 0) r = __dadd_rn(r, __dmul_rn(em ? a.co.flo[1] : a.co.flo[0], blo));
-  if (i == a.m - 1) r = __dadd_rn(r, __dmul_rn(ep ? a.co.fhi[1] : a.co.fhi[0], bhi));
+  if ((c & 16u) && a.has_extra) r = __dadd_rn(r, __dmul_rn(a.extra, *rho_at));
+  if (row0) r = __dadd_rn(r, __dmul_rn(em ? a.co.flo[1] : a.co.flo[0], blo));
+  if (rowlast) r = __dadd_rn(r, __dmul_rn(ep ? a.co.fhi[1] : a.co.fhi[0], bhi));
   return r;
 }
 
-// Epilogue for the final value x at a node (AOS0's flow(u) term is added by the caller).
-__device__ __forceinline__ double epi_val(const SweepArgs& a, double x, uint32_t c,
-                                          long long off) {
+// Epilogue for the final value x at a node (schemes.py:309-311, 322, 329); y is the
+// prefetched raw field (AOS0) or accumulator (AOS1/2, MAOS1/2) at the node.
+__device__ __forceinline__ double epi_val(const SweepArgs& a, double x, double y, uint32_t c,
+                                          const double* rho_at) {
   switch (a.epi) {
     case EPI_SRC:
-      return (c & 16u) ? __dadd_rn(x, __dmul_rn(a.epi_coef, a.rho[off])) : x;
+      return (c & 16u) ? __dadd_rn(x, __dmul_rn(a.epi_coef, *rho_at)) : x;
     case EPI_FLOW:
-      return sinh_flow(x, (c & 1u) ? a.decay1 : a.decay0, 1.0);
+      return flow_at(a, x, c, 1.0);
+    case EPI_AOS0:
+      return __dadd_rn(flow_at(a, y, c, a.pm), x);
     case EPI_AOS1:
     case EPI_MAOS1:
-      return __dadd_rn(a.acc[off], x);
+      return __dadd_rn(y, x);
     case EPI_AOS2:
-      return __dmul_rn(0.25, __dadd_rn(a.acc[off], x));
+      return __dmul_rn(0.25, __dadd_rn(y, x));
     case EPI_MAOS2:
-      return __ddiv_rn(__dadd_rn(a.acc[off], x), 3.0);
+      return __ddiv_rn(__dadd_rn(y, x), 3.0);
     default:
       return x;
   }
@@ -159,189 +200,272 @@ __device__ __forceinline__ bool is_bad(double v, double thr) {
   return !isfinite(v) || fabs(v) > thr;
 }
 
-// Segment elimination.  On entry r[j] = rhs of row i0+j, cd[j] = code of node of row i0+j
-// (cd[S] = code of the following node).  On exit, for inner rows j < S-1:
-//   r[j] = y_j, da[j] = alpha_j, cb[j] = beta_j;  separator coefficients in as/bs/cs.
-template <int S>
-__device__ __forceinline__ void seg_solve(double (&r)[S], double (&cb)[S], double (&da)[S],
-                                          const uint32_t (&cd)[S + 1], int i0, int m, int sh,
-                                          const AxisCoef& co, double& as, double& bs,
-                                          double& cs) {
-  double cpp = 0.0, dyp = 0.0, dap = 1.0, lastinv = 0.0, lastc = 0.0;
+// Per-thread segment state after the local elimination.
+struct SegOut {
+  double yF, aF, bF, yL, aL, bL;  // first / last inner row: y, alpha, beta
+  double as, bs, cs, rs;          // separator row coefficients and rhs
+};
+
+// Local elimination of one segment.
+//   r[j]   rhs of row i0+j (registers; on exit y_j for a uniform segment)
+//   amask  bit j = eps bit (sweep axis) of the node of row i0+j, j = 0..S (S = next node)
+//   T      shared-memory copy of the uniform tables for this axis
+//   w0/ws  shared-memory slots of rows j = 0..S-2 (general path keeps y_j there)
+//   c0/cst shared-memory codes of the same nodes (general path)
+//   al/be  L1-resident local arrays for the general path
+// Returns the table type (0 interior, 1 first, 2 last) for a uniform segment, -1 otherwise.
+template <int S, int WS, int CST>
+__device__ __forceinline__ int seg_eliminate(const SweepArgs& a, double (&r)[S],
+                                              unsigned long long amask, int i0, int first,
+                                              int sh, const double* T, double* w0,
+                                              const uint8_t* c0, double (&al)[S],
+                                              double (&be)[S], SegOut& o) {
+  const int m = a.m;
+  const unsigned long long allm = (1ull << S) - 1ull;
+  const unsigned long long seg_bits = amask & allm;
+  int ttype = -1;
+  if (seg_bits == 0ull || seg_bits == allm) {
+    if (i0 + S <= m) ttype = first ? 1 : 0;
+    else if (i0 + S - 1 == m && !first) ttype = 2;
+  }
+  o.rs = r[S - 1];
+  {
+    const uint32_t em = (uint32_t)(amask >> (S - 1)) & 1u, ep = (uint32_t)(amask >> S) & 1u;
+    row_coefs(a.co, i0 + S - 1, m, em, ep, o.as, o.bs, o.cs);
+  }
+  if (ttype >= 0) {
+    const double* Tv = T + (ttype * 2 + (seg_bits ? 1 : 0)) * 5 * kTabRows;
+    double dyp = 0.0;
 #pragma unroll
+    for (int j = 0; j < S - 1; ++j) {
+      const double dy = fma(-Tv[TQ_G * kTabRows + j], dyp, r[j] * Tv[TQ_INV * kTabRows + j]);
+      r[j] = dy;
+      dyp = dy;
+    }
+    double y = r[S - 2];
+#pragma unroll
+    for (int j = S - 3; j >= 0; --j) {
+      y = fma(-Tv[TQ_CP * kTabRows + j], y, r[j]);
+      r[j] = y;
+    }
+    o.yF = r[0];
+    o.yL = r[S - 2];
+    o.aF = Tv[TQ_AL * kTabRows];
+    o.bF = Tv[TQ_BE * kTabRows];
+    o.aL = Tv[TQ_AL * kTabRows + S - 2];
+    o.bL = Tv[TQ_BE * kTabRows + S - 2];
+    return ttype;
+  }
+  // General segment: rhs to shared memory, then rolled elimination.
+#pragma unroll
+  for (int j = 0; j < S - 1; ++j) w0[j * WS] = r[j];
+  double cpp = 0.0, dyp = 0.0, dap = 1.0, lastinv = 0.0, lastc = 0.0;
+#pragma unroll 1
   for (int j = 0; j < S - 1; ++j) {
-    const uint32_t em = (cd[j] >> sh) & 1u, ep = (cd[j + 1] >> sh) & 1u;
+    const uint32_t em = (c0[j * CST] >> sh) & 1u, ep = (c0[(j + 1) * CST] >> sh) & 1u;
     double av, bv, cv;
-    row_coefs(co, i0 + j, m, em, ep, av, bv, cv);
+    row_coefs(a.co, i0 + j, m, em, ep, av, bv, cv);
     const double inv = __drcp_rn(fma(-av, cpp, bv));
     const double cpj = cv * inv;
-    const double dy = fma(-av, dyp, r[j]) * inv;
+    const double dy = fma(-av, dyp, w0[j * WS]) * inv;
     const double dA = -(av * dap) * inv;
-    r[j] = dy;
-    da[j] = dA;
-    cb[j] = cpj;
+    w0[j * WS] = dy;
+    al[j] = dA;
+    be[j] = cpj;
     cpp = cpj;
     dyp = dy;
     dap = dA;
     lastinv = inv;
     lastc = cv;
   }
-  double be = -lastc * lastinv;
-  double y = r[S - 2], al = da[S - 2];
-  cb[S - 2] = be;
-#pragma unroll
+  double bb = -lastc * lastinv;
+  double y = w0[(S - 2) * WS], aa = al[S - 2];
+  be[S - 2] = bb;
+  o.yL = y;
+  o.aL = aa;
+  o.bL = bb;
+#pragma unroll 1
   for (int j = S - 3; j >= 0; --j) {
-    const double c = cb[j];
-    y = fma(-c, y, r[j]);
-    al = fma(-c, al, da[j]);
-    be = -c * be;
-    r[j] = y;
-    da[j] = al;
-    cb[j] = be;
+    const double c = be[j];
+    y = fma(-c, y, w0[j * WS]);
+    aa = fma(-c, aa, al[j]);
+    bb = -c * bb;
+    w0[j * WS] = y;
+    al[j] = aa;
+    be[j] = bb;
   }
-  const uint32_t em = (cd[S - 1] >> sh) & 1u, ep = (cd[S] >> sh) & 1u;
-  row_coefs(co, i0 + S - 1, m, em, ep, as, bs, cs);
+  o.yF = w0[0];
+  o.aF = al[0];
+  o.bF = be[0];
+  return -1;
+}
+
+// x_j = y_j + alpha_j*tm + beta_j*t for the inner rows, written to w0[j*WS].
+template <int S, int WS>
+__device__ __forceinline__ void seg_finish(int ttype, const double (&r)[S],
+                                           unsigned long long amask, double tm, double t,
+                                           const double* T, double* w0,
+                                           const double (&al)[S], const double (&be)[S]) {
+  if (ttype >= 0) {
+    const double* Tv = T + (ttype * 2 + (amask & 1ull ? 1 : 0)) * 5 * kTabRows;
+#pragma unroll
+    for (int j = 0; j < S - 1; ++j)
+      w0[j * WS] = fma(Tv[TQ_BE * kTabRows + j], t, fma(Tv[TQ_AL * kTabRows + j], tm, r[j]));
+  } else {
+#pragma unroll 1
+    for (int j = 0; j < S - 1; ++j) w0[j * WS] = fma(be[j], t, fma(al[j], tm, w0[j * WS]));
+  }
+}
+
+// Reduced-system coefficients of separator k (needs the next segment's first-row values).
+__device__ __forceinline__ void reduced_row(const SegOut& o, double yFn, double aFn,
+                                            double bFn, double& A, double& B, double& C,
+                                            double& R) {
+  A = o.as * o.aL;
+  B = o.bs + o.as * o.bL + o.cs * aFn;
+  C = o.cs * bFn;
+  R = o.rs - o.as * o.yL - o.cs * yFn;
 }
 
 // ---------------------------------------------------------------------------------------
-// Strided axes (0, 1).  blockDim = (LB, P); block (x = k group, y = outer interior index).
+// Strided axes (0, 1).  blockDim = (8 columns, 32 segments); block (x = k group, y = outer).
+// Shared memory: tables | W[NR][8] stage/solution | Y[NR][8] (AOS/MAOS) | 4x256 scratch |
+// codes C[NR][8].
 template <int S>
-__global__ void __launch_bounds__(512) k_sweep_strided(const SweepArgs a, const int axis) {
+__host__ __device__ constexpr int strided_rows() {
+  return kSeg * S + 2;
+}
+
+template <int S, bool CN>
+__global__ void __launch_bounds__(256) k_sweep_strided(const SweepArgs a, const int axis) {
   extern __shared__ double sm[];
   if (a.div_step && *((volatile int*)a.div_step) < a.step) return;
-  const int LB = blockDim.x, P = blockDim.y;
+  constexpr int LB = kCols, NT = kCols * kSeg, NR = strided_rows<S>();
   const int lane = threadIdx.x, seg = threadIdx.y;
-  const int tid = seg * LB + lane, NT = LB * P;
+  const int tid = seg * LB + lane;
   const Layout& L = a.L;
-  const int m = a.m;
-  const int kcol = 1 + blockIdx.x * LB + lane;
+  const int m = a.m, nl = m + 2;
+  const int k0 = 1 + blockIdx.x * LB;
   const int outer = 1 + blockIdx.y;
-  const bool active = kcol <= L.n2 - 2;
-  long long base, stride;
+  const int ncols = min(LB, L.n2 - 1 - k0);  // active columns in this tile
+  long long base;
+  int stride;
   if (axis == 0) {
-    base = L.at(0, outer, kcol);
-    stride = L.s0;
+    base = L.at(0, outer, k0);
+    stride = (int)L.s0;
   } else {
-    base = L.at(outer, 0, kcol);
-    stride = L.pitch;
+    base = L.at(outer, 0, k0);
+    stride = (int)L.pitch;
   }
+  const int needY = epi_needs(a.epi);
+  double* T = sm;
+  double* W = T + kTabDoubles;
+  double* Yt = W + NR * LB;
+  double* X = Yt + (needY ? NR * LB : 0);
+  uint8_t* C = reinterpret_cast<uint8_t*>(X + 4 * NT);
   const int sh = 1 + axis;
-  const int i0 = seg * S;
+  const double* gsrc = a.src + base;
+  const double* gface = (a.pro == PRO_FLOW ? a.bnd : a.src) + base;
+  const double* gy = (needY == 1 ? a.src : a.acc) + base;
+  const double* grho = a.rho + base;
 
-  double r[S], cb[S], da[S];
-  uint32_t cd[S + 1];
+  // Phase 1: asynchronous staging of the field (+ epilogue operand), codes and tables.
+  for (int c = tid; c < nl * (LB / 2); c += NT) {
+    const int p = c >> 2, q = (c & 3) * 2;
+    const int off = p * stride + q;
+    cp_async16(W + p * LB + q, ((p == 0 || p == nl - 1) ? gface : gsrc) + off);
+    if (needY) cp_async16(Yt + p * LB + q, gy + off);
+  }
+  for (int p = tid; p < nl; p += NT) cp_async8(C + p * LB, a.codes + base + p * stride);
+  for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
+  cp_async_wait_all();
+  __syncthreads();
+  if (a.pro != PRO_NONE) {  // prologue in place on the interior rows
+    for (int c = LB + tid; c < (nl - 1) * LB; c += NT) {
+      const int p = c >> 3, l = c & 7;
+      W[c] = pro_val(a, W[c], C[c], grho + p * stride + l);
+    }
+    __syncthreads();
+  }
+
+  // Phase 2: rhs of the own rows (registers), local elimination.
+  const bool active = lane < ncols;
+  const int i0 = seg * S;
+  double r[S];
+  unsigned long long amask = 0;
 #pragma unroll
   for (int j = 0; j <= S; ++j) {
-    const int i = i0 + j;
-    cd[j] = (active && i <= m) ? (uint32_t)a.codes[base + (long long)(i + 1) * stride] : 0u;
+    const int p = i0 + j + 1;
+    if (p < nl) amask |= (unsigned long long)((C[p * LB + lane] >> sh) & 1u) << j;
   }
-#pragma unroll
-  for (int j = 0; j < S; ++j) {
-    const int i = i0 + j;
-    r[j] = (active && i < m) ? a.src[base + (long long)(i + 1) * stride] : 0.0;
-  }
+  const int jlast = m - 1 - i0;
   double blo = 0.0, bhi = 0.0;
-  if (active && i0 == 0) blo = a.bnd[base];
-  if (active && i0 <= m - 1 && m - 1 < i0 + S) bhi = a.bnd[base + (long long)(m + 1) * stride];
-
-  // stage field w (prologue) for own rows; rows == m hold the far face (CN neighbour)
+  if (active && i0 == 0) blo = a.bnd[base + lane];
+  if (active && i0 <= m - 1 && m - 1 < i0 + S) bhi = a.bnd[base + (long long)(m + 1) * stride + lane];
 #pragma unroll
   for (int j = 0; j < S; ++j) {
-    const int i = i0 + j;
-    const long long off = base + (long long)(i + 1) * stride;
-    if (!active || i > m) {
-      r[j] = 0.0;
-    } else if (i == m) {
-      r[j] = a.cn ? face_val(a, off) : 0.0;
+    const int i = i0 + j, p = i + 1;
+    if (i < m) {
+      const double* wp = W + p * LB + lane;
+      r[j] = row_rhs<CN>(a, j == 0 && i0 == 0, j == jlast, C[p * LB + lane], (uint32_t)(amask >> j) & 1u,
+                         (uint32_t)(amask >> (j + 1)) & 1u, CN ? wp[-LB] : 0.0, wp[0],
+                         CN ? wp[LB] : 0.0, grho + p * stride + lane, blo, bhi);
     } else {
-      r[j] = pro_val(a, r[j], cd[j], off);
+      r[j] = 0.0;
     }
   }
-  double wprev = 0.0, wnext = 0.0;
-  if (a.cn && active) {
-    if (i0 == 0) {
-      wprev = face_val(a, base);
-    } else if (i0 - 1 < m) {
-      const long long off = base + (long long)i0 * stride;
-      wprev = pro_val(a, a.src[off], a.codes[off], off);
-    }
-    const int inx = i0 + S;
-    const long long off = base + (long long)(inx + 1) * stride;
-    if (inx < m) {
-      wnext = pro_val(a, a.src[off], a.codes[off], off);
-    } else if (inx == m) {
-      wnext = face_val(a, off);
-    }
-  }
-  // rhs (in place, keeping the previous stage value for the stencil)
-  {
-    double wm = wprev;
-#pragma unroll
-    for (int j = 0; j < S; ++j) {
-      const int i = i0 + j;
-      const double wc = r[j];
-      const double wp = (j + 1 < S) ? r[j + 1] : wnext;
-      if (active && i < m) {
-        const uint32_t sh2 = (uint32_t)sh;
-        const uint32_t em = (cd[j] >> sh2) & 1u, ep = (cd[j + 1] >> sh2) & 1u;
-        r[j] = row_rhs(a, i, cd[j], em, ep, wm, wc, wp, base + (long long)(i + 1) * stride,
-                       blo, bhi);
-      } else {
-        r[j] = 0.0;
-      }
-      wm = wc;
-    }
-  }
+  __syncthreads();  // all stencil reads of W done; rows are private from here on
 
-  double as, bs, cs;
-  seg_solve<S>(r, cb, da, cd, i0, m, sh, a.co, as, bs, cs);
-  const double rs = r[S - 1];
+  double al[S], be[S];
+  SegOut o;
+  double* w0 = W + (i0 + 1) * LB + lane;
+  const int ttype = seg_eliminate<S, LB, LB>(a, r, amask, i0, seg == 0, sh, T, w0,
+                                            C + (i0 + 1) * LB + lane, al, be, o);
 
-  double* sA = sm;
-  double* sB = sm + NT;
-  double* sC = sm + 2 * NT;
-  double* sR = sm + 3 * NT;
-  sA[tid] = r[0];
-  sB[tid] = da[0];
-  sC[tid] = cb[0];
+  // Phase 3: reduced system over the 32 separators of each line (PCR in shared memory).
+  double* sA = X;
+  double* sB = X + NT;
+  double* sC = X + 2 * NT;
+  double* sR = X + 3 * NT;
+  sA[tid] = o.yF;
+  sB[tid] = o.aF;
+  sC[tid] = o.bF;
   __syncthreads();
   double yFn = 0.0, aFn = 0.0, bFn = 0.0;
-  if (seg + 1 < P) {
+  if (seg + 1 < kSeg) {
     yFn = sA[tid + LB];
     aFn = sB[tid + LB];
     bFn = sC[tid + LB];
   }
   __syncthreads();
-  const double yL = r[S - 2], aL = da[S - 2], bL = cb[S - 2];
-  double A = as * aL;
-  double B = bs + as * bL + cs * aFn;
-  double C = cs * bFn;
-  double R = rs - as * yL - cs * yFn;
-  for (int d = 1; d < P; d <<= 1) {
+  double A, B, Cc, R;
+  reduced_row(o, yFn, aFn, bFn, A, B, Cc, R);
+#pragma unroll
+  for (int d = 1; d < kSeg; d <<= 1) {
     sA[tid] = A;
     sB[tid] = __drcp_rn(B);
-    sC[tid] = C;
+    sC[tid] = Cc;
     sR[tid] = R;
     __syncthreads();
     double Am = 0.0, iBm = 1.0, Cm = 0.0, Rm = 0.0, Ap = 0.0, iBp = 1.0, Cp = 0.0, Rp = 0.0;
     if (seg >= d) {
-      const int o = tid - d * LB;
-      Am = sA[o];
-      iBm = sB[o];
-      Cm = sC[o];
-      Rm = sR[o];
+      const int q = tid - d * LB;
+      Am = sA[q];
+      iBm = sB[q];
+      Cm = sC[q];
+      Rm = sR[q];
     }
-    if (seg + d < P) {
-      const int o = tid + d * LB;
-      Ap = sA[o];
-      iBp = sB[o];
-      Cp = sC[o];
-      Rp = sR[o];
+    if (seg + d < kSeg) {
+      const int q = tid + d * LB;
+      Ap = sA[q];
+      iBp = sB[q];
+      Cp = sC[q];
+      Rp = sR[q];
     }
     __syncthreads();
-    const double k1 = -A * iBm, k2 = -C * iBp;
+    const double k1 = -A * iBm, k2 = -Cc * iBp;
     A = k1 * Am;
-    C = k2 * Cp;
+    Cc = k2 * Cp;
     B = B + k1 * Cm + k2 * Ap;
     R = R + k1 * Rm + k2 * Rp;
   }
@@ -350,29 +474,38 @@ __global__ void __launch_bounds__(512) k_sweep_strided(const SweepArgs a, const 
   __syncthreads();
   const double tm = (seg > 0) ? sA[tid - LB] : 0.0;
 
+  // Phase 4: reconstruct the inner rows, separator = t.
+  seg_finish<S, LB>(ttype, r, amask, tm, t, T, w0, al, be);
+  if (i0 + S - 1 < m) W[(i0 + S) * LB + lane] = t;
+  __syncthreads();
+
+  // Phase 5: epilogue + coalesced store of the interior rows.
   bool bad = false;
-#pragma unroll
-  for (int j = 0; j < S; ++j) {
-    const int i = i0 + j;
-    if (!active || i >= m) continue;
-    const long long off = base + (long long)(i + 1) * stride;
-    double x = (j < S - 1) ? fma(cb[j], t, fma(da[j], tm, r[j])) : t;
-    if (a.epi == EPI_AOS0) {
-      x = __dadd_rn(sinh_flow(a.src[off], (cd[j] & 1u) ? a.decay1 : a.decay0, a.pm), x);
-    } else {
-      x = epi_val(a, x, cd[j], off);
+  double* gdst = a.dst + base;
+  if (a.epi == EPI_STORE && !a.check) {
+    for (int c = LB + tid; c < (m + 1) * LB; c += NT) {
+      const int p = c >> 3, l = c & 7;
+      if (l < ncols) gdst[p * stride + l] = W[c];
     }
-    a.dst[off] = x;
-    bad |= is_bad(x, a.thr);
+  } else {
+    for (int c = LB + tid; c < (m + 1) * LB; c += NT) {
+      const int p = c >> 3, l = c & 7;
+      if (l >= ncols) continue;
+      const int off = p * stride + l;
+      const double x = epi_val(a, W[c], needY ? Yt[c] : 0.0, C[c], grho + off);
+      gdst[off] = x;
+      bad |= is_bad(x, a.thr);
+    }
   }
   if (a.check) {
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x + threadIdx.y * blockDim.x) % 32 == 0)
-      atomicMin(a.div_step, a.step);
+    if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicMin(a.div_step, a.step);
   }
 }
 
 // ---------------------------------------------------------------------------------------
-// Contiguous axis (2): one warp per (i, j) line, lane = segment of S rows.
+// Contiguous axis (2): one warp per (i, j) line, lane = segment of S rows.  The row lives in
+// shared memory with one pad slot per S nodes (S even) so lanes read their rows without bank
+// conflicts.
 template <int S>
 __host__ __device__ constexpr int cpos(int p) {
   return (S % 2 == 0) ? p + p / S : p;
@@ -383,92 +516,101 @@ __host__ __device__ constexpr int contig_buf_doubles() {
   return ((cpos<S>(32 * S + 2) + 2) + 1) & ~1;
 }
 
-template <int S>
+constexpr int kContigWarps = 8;
+
+template <int S, bool CN>
 __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const int nlines) {
   extern __shared__ double sm[];
   if (a.div_step && *((volatile int*)a.div_step) < a.step) return;
   constexpr int BUF = contig_buf_doubles<S>();
-  constexpr int CBUF = 32 * S + 8;
-  const int W = blockDim.x >> 5;
+  constexpr int CBUF = 32 * S + 64;
+  constexpr int W = kContigWarps;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int needY = epi_needs(a.epi);
+  const int YB = needY ? 32 * S + 2 : 0;
+  double* T = sm;
+  double* buf = T + kTabDoubles + warp * (BUF + YB);
+  double* ybuf = buf + BUF;
+  uint8_t* craw = reinterpret_cast<uint8_t*>(T + kTabDoubles + W * (BUF + YB)) + warp * CBUF;
+  const uint8_t* cbuf = craw + kOff;  // cbuf[e] = code of node e
+
+  for (int c = threadIdx.x; c < kTabDoubles / 2; c += 32 * W) cp_async16(T + 2 * c, a.tab + 2 * c);
   const int line = blockIdx.x * W + warp;
-  if (line >= nlines) return;
+  const bool live = line < nlines;
   const Layout& L = a.L;
   const int m = a.m, n2 = L.n2;
   const int ii = 1 + line / (L.n1 - 2), jj = 1 + line % (L.n1 - 2);
   const long long rb = L.at(ii, jj, 0);
-  double* buf = sm + warp * BUF;
-  uint8_t* cbuf = reinterpret_cast<uint8_t*>(sm + W * BUF) + warp * CBUF;
+  const double* gsrc = a.src + rb;
+  const double* grho = a.rho + rb;
 
-  for (int e = lane; e < n2; e += 32) {
-    buf[cpos<S>(e)] = a.src[rb + e];
-    cbuf[e] = a.codes[rb + e];
+  // Phase 1: asynchronous staging.
+  if (live) {
+    const double* gface = (a.pro == PRO_FLOW ? a.bnd : a.src) + rb;
+    const double* gy = (needY == 1 ? a.src : a.acc) + rb;
+    for (int e = lane; e < n2; e += 32) {
+      cp_async8(buf + cpos<S>(e), ((e == 0 || e == n2 - 1) ? gface : gsrc) + e);
+      if (needY) cp_async8(ybuf + e, gy + e);
+    }
+    const int nch = (n2 + kOff + 15) / 16;
+    for (int q = lane; q < nch; q += 32) cp_async16(craw + 16 * q, a.codes + (rb - kOff) + 16 * q);
   }
-  __syncwarp();
+  cp_async_wait_all();
+  __syncthreads();  // tables are shared by the block
+  if (!live) return;
+  if (a.pro != PRO_NONE) {
+    for (int e = lane + 1; e < n2 - 1; e += 32)
+      buf[cpos<S>(e)] = pro_val(a, buf[cpos<S>(e)], cbuf[e], grho + e);
+    __syncwarp();
+  }
 
   const int i0 = lane * S;
-  double r[S], cb[S], da[S];
-  uint32_t cd[S + 1];
+  double r[S];
+  unsigned long long amask = 0;
 #pragma unroll
   for (int j = 0; j <= S; ++j) {
     const int p = i0 + j + 1;
-    cd[j] = (p <= n2 - 1) ? (uint32_t)cbuf[p] : 0u;
+    if (p < n2) amask |= (unsigned long long)((cbuf[p] >> 3) & 1u) << j;
   }
+  const int jlast = m - 1 - i0;
+  double blo = 0.0, bhi = 0.0;
+  if (i0 == 0) blo = a.bnd[rb];
+  if (i0 <= m - 1 && m - 1 < i0 + S) bhi = a.bnd[rb + m + 1];
 #pragma unroll
   for (int j = 0; j < S; ++j) {
     const int i = i0 + j, p = i + 1;
     if (i < m) {
-      r[j] = pro_val(a, buf[cpos<S>(p)], cd[j], rb + p);
-    } else if (i == m) {
-      r[j] = a.cn ? face_val(a, rb + p) : 0.0;
+      r[j] = row_rhs<CN>(a, j == 0 && i0 == 0, j == jlast, cbuf[p], (uint32_t)(amask >> j) & 1u,
+                         (uint32_t)(amask >> (j + 1)) & 1u, CN ? buf[cpos<S>(p - 1)] : 0.0,
+                         buf[cpos<S>(p)], CN ? buf[cpos<S>(p + 1)] : 0.0, grho + p, blo, bhi);
     } else {
       r[j] = 0.0;
     }
   }
-  double wprev = __shfl_up_sync(0xffffffffu, r[S - 1], 1);
-  double wnext = __shfl_down_sync(0xffffffffu, r[0], 1);
-  if (lane == 0) wprev = a.cn ? face_val(a, rb) : 0.0;
-  if (lane == 31) wnext = (a.cn && 32 * S == m) ? face_val(a, rb + m + 1) : 0.0;
-  double blo = 0.0, bhi = 0.0;
-  if (i0 == 0) blo = a.bnd[rb];
-  if (i0 <= m - 1 && m - 1 < i0 + S) bhi = a.bnd[rb + m + 1];
-  {
-    double wm = wprev;
-#pragma unroll
-    for (int j = 0; j < S; ++j) {
-      const int i = i0 + j;
-      const double wc = r[j];
-      const double wp = (j + 1 < S) ? r[j + 1] : wnext;
-      if (i < m) {
-        const uint32_t em = (cd[j] >> 3) & 1u, ep = (cd[j + 1] >> 3) & 1u;
-        r[j] = row_rhs(a, i, cd[j], em, ep, wm, wc, wp, rb + i + 1, blo, bhi);
-      } else {
-        r[j] = 0.0;
-      }
-      wm = wc;
-    }
-  }
-  double as, bs, cs;
-  seg_solve<S>(r, cb, da, cd, i0, m, 3, a.co, as, bs, cs);
-  const double rs = r[S - 1];
-  double yFn = __shfl_down_sync(0xffffffffu, r[0], 1);
-  double aFn = __shfl_down_sync(0xffffffffu, da[0], 1);
-  double bFn = __shfl_down_sync(0xffffffffu, cb[0], 1);
+  __syncwarp();
+
+  double al[S], be[S];
+  SegOut o;
+  double* w0 = buf + cpos<S>(i0 + 1);
+  const int ttype = seg_eliminate<S, 1, 1>(a, r, amask, i0, lane == 0, 3, T, w0, cbuf + i0 + 1,
+                                          al, be, o);
+
+  double yFn = __shfl_down_sync(0xffffffffu, o.yF, 1);
+  double aFn = __shfl_down_sync(0xffffffffu, o.aF, 1);
+  double bFn = __shfl_down_sync(0xffffffffu, o.bF, 1);
   if (lane == 31) yFn = aFn = bFn = 0.0;
-  double A = as * da[S - 2];
-  double B = bs + as * cb[S - 2] + cs * aFn;
-  double C = cs * bFn;
-  double R = rs - as * r[S - 2] - cs * yFn;
+  double A, B, Cc, R;
+  reduced_row(o, yFn, aFn, bFn, A, B, Cc, R);
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const double iB = __drcp_rn(B);
     double Am = __shfl_up_sync(0xffffffffu, A, d);
     double iBm = __shfl_up_sync(0xffffffffu, iB, d);
-    double Cm = __shfl_up_sync(0xffffffffu, C, d);
+    double Cm = __shfl_up_sync(0xffffffffu, Cc, d);
     double Rm = __shfl_up_sync(0xffffffffu, R, d);
     double Ap = __shfl_down_sync(0xffffffffu, A, d);
     double iBp = __shfl_down_sync(0xffffffffu, iB, d);
-    double Cp = __shfl_down_sync(0xffffffffu, C, d);
+    double Cp = __shfl_down_sync(0xffffffffu, Cc, d);
     double Rp = __shfl_down_sync(0xffffffffu, R, d);
     if (lane < d) {
       Am = 0.0;
@@ -482,9 +624,9 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
       Cp = 0.0;
       Rp = 0.0;
     }
-    const double k1 = -A * iBm, k2 = -C * iBp;
+    const double k1 = -A * iBm, k2 = -Cc * iBp;
     A = k1 * Am;
-    C = k2 * Cp;
+    Cc = k2 * Cp;
     B = B + k1 * Cm + k2 * Ap;
     R = R + k1 * Rm + k2 * Rp;
   }
@@ -492,22 +634,20 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
   double tm = __shfl_up_sync(0xffffffffu, t, 1);
   if (lane == 0) tm = 0.0;
 
-#pragma unroll
-  for (int j = 0; j < S; ++j) {
-    const int i = i0 + j, p = i + 1;
-    if (i >= m) continue;
-    double x = (j < S - 1) ? fma(cb[j], t, fma(da[j], tm, r[j])) : t;
-    if (a.epi == EPI_AOS0)
-      x = __dadd_rn(sinh_flow(buf[cpos<S>(p)], (cd[j] & 1u) ? a.decay1 : a.decay0, a.pm), x);
-    buf[cpos<S>(p)] = x;
-  }
+  seg_finish<S, 1>(ttype, r, amask, tm, t, T, w0, al, be);
+  if (i0 + S - 1 < m) buf[cpos<S>(i0 + S)] = t;
   __syncwarp();
+
   bool bad = false;
-  for (int p = lane + 1; p <= m; p += 32) {
-    double x = buf[cpos<S>(p)];
-    if (a.epi != EPI_AOS0) x = epi_val(a, x, cbuf[p], rb + p);
-    a.dst[rb + p] = x;
-    bad |= is_bad(x, a.thr);
+  double* gdst = a.dst + rb;
+  if (a.epi == EPI_STORE && !a.check) {
+    for (int p = lane + 1; p <= m; p += 32) gdst[p] = buf[cpos<S>(p)];
+  } else {
+    for (int p = lane + 1; p <= m; p += 32) {
+      const double x = epi_val(a, buf[cpos<S>(p)], needY ? ybuf[p] : 0.0, cbuf[p], grho + p);
+      gdst[p] = x;
+      bad |= is_bad(x, a.thr);
+    }
   }
   if (a.check) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(a.div_step, a.step);
@@ -517,59 +657,84 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
 // ---------------------------------------------------------------------------------------
 // Host-side launch helpers.
 
-static int strided_S(int m) { return m <= 128 ? 4 : (m <= 512 ? 8 : 16); }
+static int seg_S(int m) {
+  const int opts[] = {2, 3, 4, 6, 8, 12, 16, 24, 32};
+  for (int s : opts)
+    if (kSeg * s >= m) return s;
+  return 0;
+}
+
+template <int S, bool CN>
+static void launch_strided_SC(const SweepArgs& a, int axis, cudaStream_t st) {
+  const int nouter = (axis == 0 ? a.L.n1 : a.L.n0) - 2;
+  dim3 grid((a.L.n2 - 2 + kCols - 1) / kCols, nouter);
+  dim3 block(kCols, kSeg);
+  const size_t NR = strided_rows<S>();
+  const size_t tiles = epi_needs(a.epi) ? 2 : 1;
+  const size_t smem =
+      sizeof(double) * (kTabDoubles + tiles * NR * kCols + 4 * kCols * kSeg) + NR * kCols;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_sweep_strided<S, CN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  k_sweep_strided<S, CN><<<grid, block, smem, st>>>(a, axis);
+}
 
 template <int S>
 static void launch_strided_S(const SweepArgs& a, int axis, cudaStream_t st) {
-  const int m = a.m;
-  const int P = (m + S - 1) / S;
-  const int LB = P <= 16 ? 32 : (P <= 32 ? 16 : 8);
-  const int nouter = (axis == 0 ? a.L.n1 : a.L.n0) - 2;
-  dim3 grid((a.L.n2 - 2 + LB - 1) / LB, nouter);
-  dim3 block(LB, P);
-  const size_t smem = sizeof(double) * 4 * LB * P;
-  k_sweep_strided<S><<<grid, block, smem, st>>>(a, axis);
+  if (a.cn) launch_strided_SC<S, true>(a, axis, st);
+  else launch_strided_SC<S, false>(a, axis, st);
 }
 
-static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
-  const int m = a.m;
-  if (m > 1024) return fail(PBG_E_UNSUPPORTED, "line too long for strided sweep (m > 1024)");
-  switch (strided_S(m)) {
-    case 4: launch_strided_S<4>(a, axis, st); break;
-    case 8: launch_strided_S<8>(a, axis, st); break;
-    default: launch_strided_S<16>(a, axis, st); break;
-  }
-  PBG_LAUNCH_CHECK("k_sweep_strided");
-  return PBG_OK;
+template <int S, bool CN>
+static void launch_contig_SC(const SweepArgs& a, cudaStream_t st) {
+  const int W = kContigWarps;
+  const int nlines = (a.L.n0 - 2) * (a.L.n1 - 2);
+  const size_t yb = epi_needs(a.epi) ? 32 * S + 2 : 0;
+  const size_t smem = sizeof(double) * kTabDoubles +
+                      (size_t)W * ((contig_buf_doubles<S>() + yb) * sizeof(double) + (32 * S + 64));
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_sweep_contig<S, CN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  k_sweep_contig<S, CN><<<(nlines + W - 1) / W, 32 * W, smem, st>>>(a, nlines);
 }
 
 template <int S>
 static void launch_contig_S(const SweepArgs& a, cudaStream_t st) {
-  const int W = 8;
-  const int nlines = (a.L.n0 - 2) * (a.L.n1 - 2);
-  const size_t smem = (size_t)W * (contig_buf_doubles<S>() * sizeof(double) + (32 * S + 8));
-  k_sweep_contig<S><<<(nlines + W - 1) / W, 32 * W, smem, st>>>(a, nlines);
+  if (a.cn) launch_contig_SC<S, true>(a, st);
+  else launch_contig_SC<S, false>(a, st);
+}
+
+#define PBG_DISPATCH_S(S_, CALL)                                                        \
+  switch (S_) {                                                                         \
+    case 2: CALL(2); break;                                                             \
+    case 3: CALL(3); break;                                                             \
+    case 4: CALL(4); break;                                                             \
+    case 6: CALL(6); break;                                                             \
+    case 8: CALL(8); break;                                                             \
+    case 12: CALL(12); break;                                                           \
+    case 16: CALL(16); break;                                                           \
+    case 24: CALL(24); break;                                                           \
+    case 32: CALL(32); break;                                                           \
+    default: return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 1024)"); \
+  }
+
+static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
+#define PBG_STRIDED(S) launch_strided_S<S>(a, axis, st)
+  PBG_DISPATCH_S(seg_S(a.m), PBG_STRIDED)
+#undef PBG_STRIDED
+  PBG_LAUNCH_CHECK("k_sweep_strided");
+  return PBG_OK;
 }
 
 static int launch_contig(const SweepArgs& a, cudaStream_t st) {
-  const int m = a.m;
-  if (m <= 64) launch_contig_S<2>(a, st);
-  else if (m <= 96) launch_contig_S<3>(a, st);
-  else if (m <= 128) launch_contig_S<4>(a, st);
-  else if (m <= 192) launch_contig_S<6>(a, st);
-  else if (m <= 256) launch_contig_S<8>(a, st);
-  else if (m <= 384) launch_contig_S<12>(a, st);
-  else if (m <= 512) launch_contig_S<16>(a, st);
-  else if (m <= 768) launch_contig_S<24>(a, st);
-  else if (m <= 1024) launch_contig_S<32>(a, st);
-  else return fail(PBG_E_UNSUPPORTED, "line too long for contiguous sweep (m > 1024)");
+#define PBG_CONTIG(S) launch_contig_S<S>(a, st)
+  PBG_DISPATCH_S(seg_S(a.m), PBG_CONTIG)
+#undef PBG_CONTIG
   PBG_LAUNCH_CHECK("k_sweep_contig");
   return PBG_OK;
 }
 
-static int launch_sweep(const SweepArgs& a, int axis, cudaStream_t st) {
-  return axis == 2 ? launch_contig(a, st) : launch_strided(a, axis, st);
-}
+static int sweep_S(int /*axis*/, int m) { return seg_S(m); }
 
 // Tridiagonal row tables for one axis: f = factor / h^2 (tridiag.py:165, 179-181, 199-202).
 static AxisCoef make_axis_coef(const double eps[2], double factor, double h) {
@@ -587,18 +752,81 @@ static AxisCoef make_axis_coef(const double eps[2], double factor, double h) {
   return c;
 }
 
+// Uniform-segment tables (same recurrences as the general device path).
+static void make_tables(const AxisCoef& co, int S, double* out) {
+  for (int i = 0; i < kTabDoubles; ++i) out[i] = 0.0;
+  for (int type = 0; type < 3; ++type) {
+    for (int v = 0; v < 2; ++v) {
+      double* T = out + (type * 2 + v) * 5 * kTabRows;
+      const double b = co.diag[v * 2 + v];
+      double cpp = 0.0, dap = 1.0, lastinv = 0.0, c = 0.0;
+      double da[kTabRows], cp[kTabRows];
+      for (int j = 0; j < S - 1; ++j) {
+        const double aj = (type == 1 && j == 0) ? 0.0 : co.sub[v];
+        c = (type == 2 && j == S - 2) ? 0.0 : co.sup[v];
+        const double inv = 1.0 / (b - aj * cpp);
+        cp[j] = c * inv;
+        da[j] = -(aj * dap) * inv;
+        T[TQ_INV * kTabRows + j] = inv;
+        T[TQ_G * kTabRows + j] = aj * inv;
+        T[TQ_CP * kTabRows + j] = cp[j];
+        cpp = cp[j];
+        dap = da[j];
+        lastinv = inv;
+      }
+      double bb = -c * lastinv, aa = da[S - 2];
+      T[TQ_AL * kTabRows + S - 2] = aa;
+      T[TQ_BE * kTabRows + S - 2] = bb;
+      for (int j = S - 3; j >= 0; --j) {
+        aa = da[j] - cp[j] * aa;
+        bb = -cp[j] * bb;
+        T[TQ_AL * kTabRows + j] = aa;
+        T[TQ_BE * kTabRows + j] = bb;
+      }
+    }
+  }
+}
+
+static void set_decays(SweepArgs& a, double d0, double d1) {
+  a.decay0 = d0;
+  a.decay1 = d1;
+  a.sat0 = d0 < 1.0 ? 2.0 * std::atanh(d0) : 0.0;
+  a.sat1 = d1 < 1.0 ? 2.0 * std::atanh(d1) : 0.0;
+}
+
 static SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, double factor) {
   SweepArgs a;
   memset(&a, 0, sizeof(a));
   a.L = make_layout(g);
   a.m = g->n[axis] - 2;
   a.co = make_axis_coef(pal->eps[axis], factor, g->h);
-  a.decay0 = a.decay1 = 1.0;
+  set_decays(a, 1.0, 1.0);
   a.pm = 1.0;
   a.pro = PRO_NONE;
   a.epi = EPI_STORE;
   a.thr = INFINITY;
   return a;
+}
+
+// Device copy of the axes' tables for one launch sequence (stream ordered).
+static int upload_tables(const SweepArgs ax[], int naxes, const int axes[], double** dtab,
+                         cudaStream_t st) {
+  std::vector<double> host((size_t)naxes * kTabDoubles);
+  for (int q = 0; q < naxes; ++q) {
+    const int S = sweep_S(axes[q], ax[q].m);
+    if (S < 2) return fail(PBG_E_UNSUPPORTED, "line too long (m > 1024)");
+    make_tables(ax[q].co, S, host.data() + (size_t)q * kTabDoubles);
+  }
+  PBG_CUDA(cudaMallocAsync(dtab, host.size() * sizeof(double), st));
+  PBG_CUDA(cudaMemcpyAsync(*dtab, host.data(), host.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, st));
+  // the host vector dies here; make the copy complete before returning
+  PBG_CUDA(cudaStreamSynchronize(st));
+  return PBG_OK;
+}
+
+static int launch_sweep(const SweepArgs& a, int axis, cudaStream_t st) {
+  return axis == 2 ? launch_contig(a, st) : launch_strided(a, axis, st);
 }
 
 // Variant table (schemes.py:209-262).
@@ -725,8 +953,7 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
       case 0:  // LODIE1 / LODCN1: flow -> sweeps -> + dta*rho
         if (axis == 0) {
           a.pro = PRO_FLOW;
-          a.decay0 = dec_lod[0];
-          a.decay1 = dec_lod[1];
+          set_decays(a, dec_lod[0], dec_lod[1]);
         }
         if (axis == 2) {
           a.epi = EPI_SRC;
@@ -740,15 +967,13 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
         }
         if (axis == 2) {
           a.epi = EPI_FLOW;
-          a.decay0 = dec_lod[0];
-          a.decay1 = dec_lod[1];
+          set_decays(a, dec_lod[0], dec_lod[1]);
         }
         break;
       case 2:  // AOS: 0.25*(((pm*flow(u) + b0) + b1) + b2), branches from u
         a.epi = axis == 0 ? EPI_AOS0 : (axis == 1 ? EPI_AOS1 : EPI_AOS2);
         if (axis == 0) {
-          a.decay0 = dec_aos[0];
-          a.decay1 = dec_aos[1];
+          set_decays(a, dec_aos[0], dec_aos[1]);
           a.pm = aos_pm;
         }
         a.has_extra = plan.src[axis] != 0.0;
@@ -756,8 +981,7 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
         break;
       case 3:  // MAOS: ((b0 + b1) + b2)/3, branches from flow(u)
         a.pro = PRO_FLOW;
-        a.decay0 = dec_lod[0];
-        a.decay1 = dec_lod[1];
+        set_decays(a, dec_lod[0], dec_lod[1]);
         a.epi = axis == 0 ? EPI_MAOS0 : (axis == 1 ? EPI_MAOS1 : EPI_MAOS2);
         a.has_extra = 1;
         a.extra = plan.src[axis] * dta;
@@ -767,6 +991,13 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
     ax[axis] = a;
   }
 
+  double* dtab = nullptr;
+  {
+    const int axes[3] = {0, 1, 2};
+    rc = upload_tables(ax, 3, axes, &dtab, st);
+    if (rc) return rc;
+    for (int axis = 0; axis < 3; ++axis) ax[axis].tab = dtab + axis * kTabDoubles;
+  }
   int* dflag = nullptr;
   PBG_CUDA(cudaMallocAsync(&dflag, sizeof(int), st));
   const int init = INT_MAX;
@@ -819,6 +1050,7 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
       }
       if (rc) {
         cudaFreeAsync(dflag, st);
+        cudaFreeAsync(dtab, st);
         return rc;
       }
     }
@@ -828,6 +1060,7 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
   int dstep = INT_MAX;
   PBG_CUDA(cudaMemcpyAsync(&dstep, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
   PBG_CUDA(cudaFreeAsync(dflag, st));
+  PBG_CUDA(cudaFreeAsync(dtab, st));
   PBG_CUDA(cudaStreamSynchronize(st));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
@@ -874,5 +1107,13 @@ extern "C" PBG_API int pbg_sweep(const pbg_grid* g, const pbg_palette* pal,
   a.rho = src;  // never read (no source terms)
   a.cn = cn ? 1 : 0;
   a.cnc = cn ? factor / (g->h * g->h) : 0.0;
-  return launch_sweep(a, axis, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  double* dtab = nullptr;
+  const int axes[1] = {axis};
+  rc = upload_tables(&a, 1, axes, &dtab, st);
+  if (rc) return rc;
+  a.tab = dtab;
+  rc = launch_sweep(a, axis, st);
+  cudaFreeAsync(dtab, st);
+  return rc;
 }

@@ -31,7 +31,7 @@ def test_version_and_layout():
     assert lib.pbg_version() == 1
     for n, pitch in ((65, 96), (97, 128), (129, 160), (257, 288), (513, 544)):
         p, ne = nat.layout((n, n, n))
-        assert p == pitch and ne == n * n * pitch
+        assert p == pitch and ne == n * n * pitch + 64
         assert (1 + nat.PBG_OFFSET) % 32 == 0  # interior k=1 is 256-byte aligned
 
 
