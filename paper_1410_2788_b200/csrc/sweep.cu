@@ -39,6 +39,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -90,6 +91,9 @@ struct SweepArgs {
   const double* acc;
   const double* tab;
   AxisCoef co;
+  // Table of the dominant segment kind (interior, palette 0 = solvent) as kernel parameters:
+  // with unrolled rows the compiler folds these into constant-bank operands (no loads).
+  double tmid[5 * kTabRows];
   int cn;
   double cnc;  // cn_f / h^2
   int pro;
@@ -105,6 +109,7 @@ struct SweepArgs {
   int step;
   double thr;
   int check;
+  int dbg;  // experiments only: 1 = stage + store (no solve)
 };
 
 // Asynchronous global->shared copies (LDGSTS): issued back to back, no register round trip.
@@ -152,27 +157,6 @@ __device__ __forceinline__ void row_coefs(const AxisCoef& co, int i, int m, uint
   bv = em ? (ep ? co.diag[3] : co.diag[2]) : (ep ? co.diag[1] : co.diag[0]);
 }
 
-// rhs of row i from the stage field (wm, wc, wp = w at rows i-1, i, i+1); schemes.py:290-297
-// and the fold-ins of tridiag.py:216-217.
-template <bool CN>
-__device__ __forceinline__ double row_rhs(const SweepArgs& a, bool row0, bool rowlast,
-                                          uint32_t c, uint32_t em, uint32_t ep, double wm,
-                                          double wc, double wp, const double* rho_at,
-                                          double blo, double bhi) {
-  double r = wc;
-  if (CN) {
-    const double epv = ep ? a.co.eps[1] : a.co.eps[0];
-    const double emv = em ? a.co.eps[1] : a.co.eps[0];
-    const double d2 =
-        __dadd_rn(__dmul_rn(epv, __dsub_rn(wp, wc)), __dmul_rn(emv, __dsub_rn(wm, wc)));
-    r = __dadd_rn(r, __dmul_rn(a.cnc, d2));
-  }
-  if ((c & 16u) && a.has_extra) r = __dadd_rn(r, __dmul_rn(a.extra, *rho_at));
-  if (row0) r = __dadd_rn(r, __dmul_rn(em ? a.co.flo[1] : a.co.flo[0], blo));
-  if (rowlast) r = __dadd_rn(r, __dmul_rn(ep ? a.co.fhi[1] : a.co.fhi[0], bhi));
-  return r;
-}
-
 // Epilogue for the final value x at a node (schemes.py:309-311, 322, 329); y is the
 // prefetched raw field (AOS0) or accumulator (AOS1/2, MAOS1/2) at the node.
 __device__ __forceinline__ double epi_val(const SweepArgs& a, double x, double y, uint32_t c,
@@ -196,8 +180,54 @@ __device__ __forceinline__ double epi_val(const SweepArgs& a, double x, double y
   }
 }
 
+// Reciprocal of a well-conditioned positive pivot: MUFU seed + two Newton steps (~1 ulp,
+// no special-case paths).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
 __device__ __forceinline__ bool is_bad(double v, double thr) {
   return !isfinite(v) || fabs(v) > thr;
+}
+
+// CN explicit half for row values (wm, wc, wp) with the row's eps bits (em, ep).
+__device__ __forceinline__ double cn_term(const SweepArgs& a, uint32_t em, uint32_t ep,
+                                          double wm, double wc, double wp) {
+  const double epv = ep ? a.co.eps[1] : a.co.eps[0];
+  const double emv = em ? a.co.eps[1] : a.co.eps[0];
+  const double d2 =
+      __dadd_rn(__dmul_rn(epv, __dsub_rn(wp, wc)), __dmul_rn(emv, __dsub_rn(wm, wc)));
+  return __dadd_rn(wc, __dmul_rn(a.cnc, d2));
+}
+
+// The rare rhs terms, applied after the stage values in the reference's order
+// (schemes.py:292-296, tridiag.py:216-217): branch source at charged nodes, the low and high
+// Dirichlet fold-ins, and zero rows past the line end.  rho_row(j) points at row i0+j's node.
+template <int S, typename RhoAt>
+__device__ __forceinline__ void rhs_rare(const SweepArgs& a, double (&r)[S],
+                                         unsigned long long amask, unsigned cmask, int i0,
+                                         RhoAt rho_row, double blo, double bhi) {
+  if (a.has_extra && cmask) {
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if ((cmask >> j) & 1u) r[j] = __dadd_rn(r[j], __dmul_rn(a.extra, *rho_row(j)));
+  }
+  if (i0 == 0) r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], blo));
+  const int jlast = a.m - 1 - i0;
+  if (jlast < S) {
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      if (j == jlast)
+        r[j] = __dadd_rn(r[j], __dmul_rn(((amask >> (j + 1)) & 1ull) ? a.co.fhi[1] : a.co.fhi[0],
+                                         bhi));
+      if (j > jlast) r[j] = 0.0;
+    }
+  }
 }
 
 // Per-thread segment state after the local elimination.
@@ -205,6 +235,37 @@ struct SegOut {
   double yF, aF, bF, yL, aL, bL;  // first / last inner row: y, alpha, beta
   double as, bs, cs, rs;          // separator row coefficients and rhs
 };
+
+// Table-driven elimination of a uniform segment (5 fp64 ops per row, no reciprocal).
+template <int S, typename Tab>
+__device__ __forceinline__ void uni_eliminate(double (&r)[S], Tab tab, SegOut& o) {
+  double dyp = 0.0;
+#pragma unroll
+  for (int j = 0; j < S - 1; ++j) {
+    const double dy = fma(-tab(TQ_G, j), dyp, r[j] * tab(TQ_INV, j));
+    r[j] = dy;
+    dyp = dy;
+  }
+  double y = r[S - 2];
+#pragma unroll
+  for (int j = S - 3; j >= 0; --j) {
+    y = fma(-tab(TQ_CP, j), y, r[j]);
+    r[j] = y;
+  }
+  o.yF = r[0];
+  o.yL = r[S - 2];
+  o.aF = tab(TQ_AL, 0);
+  o.bF = tab(TQ_BE, 0);
+  o.aL = tab(TQ_AL, S - 2);
+  o.bL = tab(TQ_BE, S - 2);
+}
+
+template <int S, int WS, typename Tab>
+__device__ __forceinline__ void uni_finish(const double (&r)[S], Tab tab, double tm, double t,
+                                           double* w0) {
+#pragma unroll
+  for (int j = 0; j < S - 1; ++j) w0[j * WS] = fma(tab(TQ_BE, j), t, fma(tab(TQ_AL, j), tm, r[j]));
+}
 
 // Local elimination of one segment.
 //   r[j]   rhs of row i0+j (registers; on exit y_j for a uniform segment)
@@ -234,26 +295,12 @@ __device__ __forceinline__ int seg_eliminate(const SweepArgs& a, double (&r)[S],
     row_coefs(a.co, i0 + S - 1, m, em, ep, o.as, o.bs, o.cs);
   }
   if (ttype >= 0) {
-    const double* Tv = T + (ttype * 2 + (seg_bits ? 1 : 0)) * 5 * kTabRows;
-    double dyp = 0.0;
-#pragma unroll
-    for (int j = 0; j < S - 1; ++j) {
-      const double dy = fma(-Tv[TQ_G * kTabRows + j], dyp, r[j] * Tv[TQ_INV * kTabRows + j]);
-      r[j] = dy;
-      dyp = dy;
+    if (ttype == 0 && seg_bits == 0ull)
+      uni_eliminate<S>(r, [&](int q, int j) { return a.tmid[q * kTabRows + j]; }, o);
+    else {
+      const double* Tv = T + (ttype * 2 + (seg_bits ? 1 : 0)) * 5 * kTabRows;
+      uni_eliminate<S>(r, [&](int q, int j) { return Tv[q * kTabRows + j]; }, o);
     }
-    double y = r[S - 2];
-#pragma unroll
-    for (int j = S - 3; j >= 0; --j) {
-      y = fma(-Tv[TQ_CP * kTabRows + j], y, r[j]);
-      r[j] = y;
-    }
-    o.yF = r[0];
-    o.yL = r[S - 2];
-    o.aF = Tv[TQ_AL * kTabRows];
-    o.bF = Tv[TQ_BE * kTabRows];
-    o.aL = Tv[TQ_AL * kTabRows + S - 2];
-    o.bL = Tv[TQ_BE * kTabRows + S - 2];
     return ttype;
   }
   // General segment: rhs to shared memory, then rolled elimination.
@@ -265,7 +312,7 @@ __device__ __forceinline__ int seg_eliminate(const SweepArgs& a, double (&r)[S],
     const uint32_t em = (c0[j * CST] >> sh) & 1u, ep = (c0[(j + 1) * CST] >> sh) & 1u;
     double av, bv, cv;
     row_coefs(a.co, i0 + j, m, em, ep, av, bv, cv);
-    const double inv = __drcp_rn(fma(-av, cpp, bv));
+    const double inv = fast_rcp(fma(-av, cpp, bv));
     const double cpj = cv * inv;
     const double dy = fma(-av, dyp, w0[j * WS]) * inv;
     const double dA = -(av * dap) * inv;
@@ -302,15 +349,15 @@ __device__ __forceinline__ int seg_eliminate(const SweepArgs& a, double (&r)[S],
 
 // x_j = y_j + alpha_j*tm + beta_j*t for the inner rows, written to w0[j*WS].
 template <int S, int WS>
-__device__ __forceinline__ void seg_finish(int ttype, const double (&r)[S],
+__device__ __forceinline__ void seg_finish(const SweepArgs& a, int ttype, const double (&r)[S],
                                            unsigned long long amask, double tm, double t,
                                            const double* T, double* w0,
                                            const double (&al)[S], const double (&be)[S]) {
-  if (ttype >= 0) {
+  if (ttype == 0 && !(amask & 1ull)) {
+    uni_finish<S, WS>(r, [&](int q, int j) { return a.tmid[q * kTabRows + j]; }, tm, t, w0);
+  } else if (ttype >= 0) {
     const double* Tv = T + (ttype * 2 + (amask & 1ull ? 1 : 0)) * 5 * kTabRows;
-#pragma unroll
-    for (int j = 0; j < S - 1; ++j)
-      w0[j * WS] = fma(Tv[TQ_BE * kTabRows + j], t, fma(Tv[TQ_AL * kTabRows + j], tm, r[j]));
+    uni_finish<S, WS>(r, [&](int q, int j) { return Tv[q * kTabRows + j]; }, tm, t, w0);
   } else {
 #pragma unroll 1
     for (int j = 0; j < S - 1; ++j) w0[j * WS] = fma(be[j], t, fma(al[j], tm, w0[j * WS]));
@@ -336,11 +383,13 @@ __host__ __device__ constexpr int strided_rows() {
   return kSeg * S + 2;
 }
 
-template <int S, bool CN>
-__global__ void __launch_bounds__(256) k_sweep_strided(const SweepArgs a, const int axis) {
+template <int S, bool CN, int LB>
+__global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
+    k_sweep_strided(const SweepArgs a, const int axis) {
   extern __shared__ double sm[];
   if (a.div_step && *((volatile int*)a.div_step) < a.step) return;
-  constexpr int LB = kCols, NT = kCols * kSeg, NR = strided_rows<S>();
+  constexpr int NT = LB * kSeg, NR = strided_rows<S>();
+  constexpr int CPR = LB / 2, RPP = NT / CPR;  // 16-byte chunks per row, rows per pass
   const int lane = threadIdx.x, seg = threadIdx.y;
   const int tid = seg * LB + lane;
   const Layout& L = a.L;
@@ -348,6 +397,7 @@ __global__ void __launch_bounds__(256) k_sweep_strided(const SweepArgs a, const 
   const int k0 = 1 + blockIdx.x * LB;
   const int outer = 1 + blockIdx.y;
   const int ncols = min(LB, L.n2 - 1 - k0);  // active columns in this tile
+  if (ncols <= 0) return;                     // cluster padding block
   long long base;
   int stride;
   if (axis == 0) {
@@ -370,49 +420,67 @@ __global__ void __launch_bounds__(256) k_sweep_strided(const SweepArgs a, const 
   const double* grho = a.rho + base;
 
   // Phase 1: asynchronous staging of the field (+ epilogue operand), codes and tables.
-  for (int c = tid; c < nl * (LB / 2); c += NT) {
-    const int p = c >> 2, q = (c & 3) * 2;
-    const int off = p * stride + q;
-    cp_async16(W + p * LB + q, ((p == 0 || p == nl - 1) ? gface : gsrc) + off);
-    if (needY) cp_async16(Yt + p * LB + q, gy + off);
+  // Thread t copies the 16-byte chunk (t & 3) of rows t/4, t/4 + 64, ...
+  {
+    const int q = (tid % CPR) * 2, p0 = tid / CPR;
+    const long long gstep = (long long)RPP * stride;
+    const double* g = gsrc + p0 * (long long)stride + q;
+    double* w = W + p0 * LB + q;
+#pragma unroll 4
+    for (int p = p0; p < nl; p += RPP, g += gstep, w += RPP * LB) cp_async16(w, g);
+    if (needY) {
+      const double* gyp = gy + p0 * (long long)stride + q;
+      double* yp = Yt + p0 * LB + q;
+#pragma unroll 4
+      for (int p = p0; p < nl; p += RPP, gyp += gstep, yp += RPP * LB) cp_async16(yp, gyp);
+    }
   }
-  for (int p = tid; p < nl; p += NT) cp_async8(C + p * LB, a.codes + base + p * stride);
+  for (int p = tid; p < nl; p += NT) {
+    if (LB == 8) cp_async8(C + p * LB, a.codes + base + (long long)p * stride);
+    else cp_async16(C + p * LB, a.codes + base + (long long)p * stride);
+  }
   for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
   cp_async_wait_all();
   __syncthreads();
-  if (a.pro != PRO_NONE) {  // prologue in place on the interior rows
-    for (int c = LB + tid; c < (nl - 1) * LB; c += NT) {
-      const int p = c >> 3, l = c & 7;
-      W[c] = pro_val(a, W[c], C[c], grho + p * stride + l);
-    }
-    __syncthreads();
+  if (a.pro == PRO_FLOW && tid < 2 * LB) {  // flow stages see the Dirichlet faces
+    const int p = tid < LB ? 0 : nl - 1, l = tid % LB;
+    W[p * LB + l] = gface[(long long)p * stride + l];
   }
+  if (a.pro != PRO_NONE) {  // prologue in place on the interior rows
+    const int l = tid % LB;
+    for (int p = 1 + tid / LB; p < nl - 1; p += NT / LB)
+      W[p * LB + l] = pro_val(a, W[p * LB + l], C[p * LB + l], grho + (long long)p * stride + l);
+  }
+  __syncthreads();
 
+  if (a.dbg == 1) goto store;
+  {
   // Phase 2: rhs of the own rows (registers), local elimination.
   const bool active = lane < ncols;
   const int i0 = seg * S;
   double r[S];
   unsigned long long amask = 0;
+  unsigned cmask = 0;
 #pragma unroll
   for (int j = 0; j <= S; ++j) {
-    const int p = i0 + j + 1;
-    if (p < nl) amask |= (unsigned long long)((C[p * LB + lane] >> sh) & 1u) << j;
+    const uint32_t c = C[(i0 + j + 1) * LB + lane];  // rows past nl: unused garbage bits
+    amask |= (unsigned long long)((c >> sh) & 1u) << j;
+    if (j < S) cmask |= ((c >> 4) & 1u) << j;
   }
-  const int jlast = m - 1 - i0;
   double blo = 0.0, bhi = 0.0;
   if (active && i0 == 0) blo = a.bnd[base + lane];
   if (active && i0 <= m - 1 && m - 1 < i0 + S) bhi = a.bnd[base + (long long)(m + 1) * stride + lane];
+  {
+    const double* wrow = W + (i0 + 1) * LB + lane;
 #pragma unroll
-  for (int j = 0; j < S; ++j) {
-    const int i = i0 + j, p = i + 1;
-    if (i < m) {
-      const double* wp = W + p * LB + lane;
-      r[j] = row_rhs<CN>(a, j == 0 && i0 == 0, j == jlast, C[p * LB + lane], (uint32_t)(amask >> j) & 1u,
-                         (uint32_t)(amask >> (j + 1)) & 1u, CN ? wp[-LB] : 0.0, wp[0],
-                         CN ? wp[LB] : 0.0, grho + p * stride + lane, blo, bhi);
-    } else {
-      r[j] = 0.0;
+    for (int j = 0; j < S; ++j) {
+      const double wc = wrow[j * LB];
+      r[j] = CN ? cn_term(a, (uint32_t)(amask >> j) & 1u, (uint32_t)(amask >> (j + 1)) & 1u,
+                          wrow[(j - 1) * LB], wc, wrow[(j + 1) * LB])
+                : wc;
     }
+    const double* rrow = grho + (i0 + 1) * stride + lane;
+    rhs_rare<S>(a, r, amask, cmask, i0, [&](int j) { return rrow + j * stride; }, blo, bhi);
   }
   __syncthreads();  // all stencil reads of W done; rows are private from here on
 
@@ -443,7 +511,7 @@ __global__ void __launch_bounds__(256) k_sweep_strided(const SweepArgs a, const 
 #pragma unroll
   for (int d = 1; d < kSeg; d <<= 1) {
     sA[tid] = A;
-    sB[tid] = __drcp_rn(B);
+    sB[tid] = fast_rcp(B);
     sC[tid] = Cc;
     sR[tid] = R;
     __syncthreads();
@@ -469,32 +537,42 @@ __global__ void __launch_bounds__(256) k_sweep_strided(const SweepArgs a, const 
     B = B + k1 * Cm + k2 * Ap;
     R = R + k1 * Rm + k2 * Rp;
   }
-  const double t = R / B;
+  const double t = R * fast_rcp(B);
   sA[tid] = t;
   __syncthreads();
   const double tm = (seg > 0) ? sA[tid - LB] : 0.0;
 
   // Phase 4: reconstruct the inner rows, separator = t.
-  seg_finish<S, LB>(ttype, r, amask, tm, t, T, w0, al, be);
+  seg_finish<S, LB>(a, ttype, r, amask, tm, t, T, w0, al, be);
   if (i0 + S - 1 < m) W[(i0 + S) * LB + lane] = t;
   __syncthreads();
-
+  }
+store:
   // Phase 5: epilogue + coalesced store of the interior rows.
   bool bad = false;
   double* gdst = a.dst + base;
   if (a.epi == EPI_STORE && !a.check) {
-    for (int c = LB + tid; c < (m + 1) * LB; c += NT) {
-      const int p = c >> 3, l = c & 7;
-      if (l < ncols) gdst[p * stride + l] = W[c];
+    const int q = (tid % CPR) * 2, p0 = 1 + tid / CPR;  // 16-byte chunks
+    const long long gstep = (long long)RPP * stride;
+    double* g = gdst + p0 * (long long)stride + q;
+    const double* w = W + p0 * LB + q;
+    if (q + 1 < ncols) {
+#pragma unroll 4
+      for (int p = p0; p <= m; p += RPP, g += gstep, w += RPP * LB)
+        *reinterpret_cast<double2*>(g) = *reinterpret_cast<const double2*>(w);
+    } else if (q < ncols) {
+      for (int p = p0; p <= m; p += RPP, g += gstep, w += RPP * LB) *g = *w;
     }
   } else {
-    for (int c = LB + tid; c < (m + 1) * LB; c += NT) {
-      const int p = c >> 3, l = c & 7;
-      if (l >= ncols) continue;
-      const int off = p * stride + l;
-      const double x = epi_val(a, W[c], needY ? Yt[c] : 0.0, C[c], grho + off);
-      gdst[off] = x;
-      bad |= is_bad(x, a.thr);
+    const int l = tid % LB;
+    if (l < ncols) {
+      for (int p = 1 + tid / LB; p <= m; p += NT / LB) {
+        const int c = p * LB + l;
+        const long long off = (long long)p * stride + l;
+        const double x = epi_val(a, W[c], needY ? Yt[c] : 0.0, C[c], grho + off);
+        gdst[off] = x;
+        bad |= is_bad(x, a.thr);
+      }
     }
   }
   if (a.check) {
@@ -548,9 +626,11 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
   if (live) {
     const double* gface = (a.pro == PRO_FLOW ? a.bnd : a.src) + rb;
     const double* gy = (needY == 1 ? a.src : a.acc) + rb;
-    for (int e = lane; e < n2; e += 32) {
-      cp_async8(buf + cpos<S>(e), ((e == 0 || e == n2 - 1) ? gface : gsrc) + e);
-      if (needY) cp_async8(ybuf + e, gy + e);
+#pragma unroll 4
+    for (int e = lane; e < n2; e += 32) cp_async8(buf + cpos<S>(e), gsrc + e);
+    if (needY) {
+#pragma unroll 4
+      for (int e = lane; e < n2; e += 32) cp_async8(ybuf + e, gy + e);
     }
     const int nch = (n2 + kOff + 15) / 16;
     for (int q = lane; q < nch; q += 32) cp_async16(craw + 16 * q, a.codes + (rb - kOff) + 16 * q);
@@ -558,6 +638,10 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
   cp_async_wait_all();
   __syncthreads();  // tables are shared by the block
   if (!live) return;
+  if (a.pro == PRO_FLOW && lane < 2) {  // flow stages see the Dirichlet faces
+    const int e = lane ? n2 - 1 : 0;
+    buf[cpos<S>(e)] = a.bnd[rb + e];
+  }
   if (a.pro != PRO_NONE) {
     for (int e = lane + 1; e < n2 - 1; e += 32)
       buf[cpos<S>(e)] = pro_val(a, buf[cpos<S>(e)], cbuf[e], grho + e);
@@ -567,26 +651,25 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
   const int i0 = lane * S;
   double r[S];
   unsigned long long amask = 0;
+  unsigned cmask = 0;
 #pragma unroll
   for (int j = 0; j <= S; ++j) {
-    const int p = i0 + j + 1;
-    if (p < n2) amask |= (unsigned long long)((cbuf[p] >> 3) & 1u) << j;
+    const uint32_t c = cbuf[i0 + j + 1];  // past the row end: unused garbage bits
+    amask |= (unsigned long long)((c >> 3) & 1u) << j;
+    if (j < S) cmask |= ((c >> 4) & 1u) << j;
   }
-  const int jlast = m - 1 - i0;
   double blo = 0.0, bhi = 0.0;
   if (i0 == 0) blo = a.bnd[rb];
   if (i0 <= m - 1 && m - 1 < i0 + S) bhi = a.bnd[rb + m + 1];
 #pragma unroll
   for (int j = 0; j < S; ++j) {
-    const int i = i0 + j, p = i + 1;
-    if (i < m) {
-      r[j] = row_rhs<CN>(a, j == 0 && i0 == 0, j == jlast, cbuf[p], (uint32_t)(amask >> j) & 1u,
-                         (uint32_t)(amask >> (j + 1)) & 1u, CN ? buf[cpos<S>(p - 1)] : 0.0,
-                         buf[cpos<S>(p)], CN ? buf[cpos<S>(p + 1)] : 0.0, grho + p, blo, bhi);
-    } else {
-      r[j] = 0.0;
-    }
+    const int p = i0 + j + 1;
+    const double wc = buf[cpos<S>(p)];
+    r[j] = CN ? cn_term(a, (uint32_t)(amask >> j) & 1u, (uint32_t)(amask >> (j + 1)) & 1u,
+                        buf[cpos<S>(p - 1)], wc, buf[cpos<S>(p + 1)])
+              : wc;
   }
+  rhs_rare<S>(a, r, amask, cmask, i0, [&](int j) { return grho + i0 + j + 1; }, blo, bhi);
   __syncwarp();
 
   double al[S], be[S];
@@ -603,7 +686,7 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
   reduced_row(o, yFn, aFn, bFn, A, B, Cc, R);
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    const double iB = __drcp_rn(B);
+    const double iB = fast_rcp(B);
     double Am = __shfl_up_sync(0xffffffffu, A, d);
     double iBm = __shfl_up_sync(0xffffffffu, iB, d);
     double Cm = __shfl_up_sync(0xffffffffu, Cc, d);
@@ -630,11 +713,11 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
     B = B + k1 * Cm + k2 * Ap;
     R = R + k1 * Rm + k2 * Rp;
   }
-  const double t = R / B;
+  const double t = R * fast_rcp(B);
   double tm = __shfl_up_sync(0xffffffffu, t, 1);
   if (lane == 0) tm = 0.0;
 
-  seg_finish<S, 1>(ttype, r, amask, tm, t, T, w0, al, be);
+  seg_finish<S, 1>(a, ttype, r, amask, tm, t, T, w0, al, be);
   if (i0 + S - 1 < m) buf[cpos<S>(i0 + S)] = t;
   __syncwarp();
 
@@ -664,19 +747,27 @@ static int seg_S(int m) {
   return 0;
 }
 
-template <int S, bool CN>
-static void launch_strided_SC(const SweepArgs& a, int axis, cudaStream_t st) {
+template <int S, bool CN, int LB>
+static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
   const int nouter = (axis == 0 ? a.L.n1 : a.L.n0) - 2;
-  dim3 grid((a.L.n2 - 2 + kCols - 1) / kCols, nouter);
-  dim3 block(kCols, kSeg);
+  dim3 grid((a.L.n2 - 2 + LB - 1) / LB, nouter);
+  dim3 block(LB, kSeg);
   const size_t NR = strided_rows<S>();
   const size_t tiles = epi_needs(a.epi) ? 2 : 1;
   const size_t smem =
-      sizeof(double) * (kTabDoubles + tiles * NR * kCols + 4 * kCols * kSeg) + NR * kCols;
+      sizeof(double) * (kTabDoubles + tiles * NR * LB + 4 * LB * kSeg) + NR * LB;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_sweep_strided<S, CN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_sweep_strided<S, CN, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  k_sweep_strided<S, CN><<<grid, block, smem, st>>>(a, axis);
+  k_sweep_strided<S, CN, LB><<<grid, block, smem, st>>>(a, axis);
+}
+
+// Axis 0 rows are one field plane apart (MB strides): 128-byte row chunks keep DRAM pages
+// and TLB entries busy (64-byte chunks run at ~55% of copy bandwidth there, measured).
+template <int S, bool CN>
+static void launch_strided_SC(const SweepArgs& a, int axis, cudaStream_t st) {
+  if (axis == 0) launch_strided_SCL<S, CN, 16>(a, axis, st);
+  else launch_strided_SCL<S, CN, 8>(a, axis, st);
 }
 
 template <int S>
@@ -823,6 +914,12 @@ static int upload_tables(const SweepArgs ax[], int naxes, const int axes[], doub
   // the host vector dies here; make the copy complete before returning
   PBG_CUDA(cudaStreamSynchronize(st));
   return PBG_OK;
+}
+
+static void fill_tmid(SweepArgs& a, int axis) {
+  std::vector<double> t(kTabDoubles);
+  make_tables(a.co, sweep_S(axis, a.m), t.data());
+  memcpy(a.tmid, t.data(), sizeof(a.tmid));  // type 0 (interior), palette 0
 }
 
 static int launch_sweep(const SweepArgs& a, int axis, cudaStream_t st) {
@@ -988,6 +1085,10 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
         break;
     }
     a.check = (axis == 2) && d->check_divergence;
+    {
+      const char* dbg = getenv("PBG_DEBUG_SKELETON");
+      a.dbg = dbg ? atoi(dbg) : 0;
+    }
     ax[axis] = a;
   }
 
@@ -996,7 +1097,10 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
     const int axes[3] = {0, 1, 2};
     rc = upload_tables(ax, 3, axes, &dtab, st);
     if (rc) return rc;
-    for (int axis = 0; axis < 3; ++axis) ax[axis].tab = dtab + axis * kTabDoubles;
+    for (int axis = 0; axis < 3; ++axis) {
+      ax[axis].tab = dtab + axis * kTabDoubles;
+      fill_tmid(ax[axis], axis);
+    }
   }
   int* dflag = nullptr;
   PBG_CUDA(cudaMallocAsync(&dflag, sizeof(int), st));
@@ -1113,6 +1217,7 @@ extern "C" PBG_API int pbg_sweep(const pbg_grid* g, const pbg_palette* pal,
   rc = upload_tables(&a, 1, axes, &dtab, st);
   if (rc) return rc;
   a.tab = dtab;
+  fill_tmid(a, axis);
   rc = launch_sweep(a, axis, st);
   cudaFreeAsync(dtab, st);
   return rc;
