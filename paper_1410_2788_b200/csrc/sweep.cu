@@ -61,7 +61,6 @@ enum {
 };
 
 constexpr int kSeg = 32;   // segments per line
-constexpr int kCols = 8;   // k columns per strided tile (64-byte row segments)
 
 struct AxisCoef {
   double diag[4];  // [em*2 + ep]  1 + f*(e_plus + e_minus)
@@ -89,7 +88,10 @@ struct SweepArgs {
   const double* rho;
   double* dst;
   const double* acc;
-  const double* tab;
+  const double* tab;   // uniform-segment tables (kTabDoubles)
+  const double* minv;  // 32x32 inverse of the clean-line reduced system
+  const unsigned long long* desc;  // per-segment descriptors (2 words), see k_build_desc
+  int static_ok;       // the clean-line reduced inverse applies to this axis (32*S in {m, m+1})
   AxisCoef co;
   // Table of the dominant segment kind (interior, palette 0 = solvent) as kernel parameters:
   // with unrolled rows the compiler folds these into constant-bank operands (no loads).
@@ -236,6 +238,12 @@ struct SegOut {
   double as, bs, cs, rs;          // separator row coefficients and rhs
 };
 
+// Node bits for the pointwise prologue / epilogue in the layout of the old 1-byte codes
+// (bit 0 solute, bit 4 charged), taken from a segment descriptor.
+__device__ __forceinline__ uint32_t node_bits(unsigned long long w1, int bit) {
+  return (uint32_t)((w1 >> bit) & 1ull) | ((uint32_t)((w1 >> (32 + bit)) & 1ull) << 4);
+}
+
 // Table-driven elimination of a uniform segment (5 fp64 ops per row, no reciprocal).
 template <int S, typename Tab>
 __device__ __forceinline__ void uni_eliminate(double (&r)[S], Tab tab, SegOut& o) {
@@ -267,38 +275,39 @@ __device__ __forceinline__ void uni_finish(const double (&r)[S], Tab tab, double
   for (int j = 0; j < S - 1; ++j) w0[j * WS] = fma(tab(TQ_BE, j), t, fma(tab(TQ_AL, j), tm, r[j]));
 }
 
+// Table type of a segment whose S nodes carry the same eps bit: 0 interior, 1 first, 2 last
+// (separator is the padding row m); -1 if the segment must be eliminated on the fly.
+template <int S>
+__device__ __forceinline__ int seg_type(unsigned long long amask, int i0, int m, int first) {
+  const unsigned long long allm = (1ull << S) - 1ull, bits = amask & allm;
+  if (bits != 0ull && bits != allm) return -1;
+  if (i0 + S <= m) return first ? 1 : 0;
+  if (i0 + S - 1 == m && !first) return 2;
+  return -1;
+}
+
 // Local elimination of one segment.
 //   r[j]   rhs of row i0+j (registers; on exit y_j for a uniform segment)
 //   amask  bit j = eps bit (sweep axis) of the node of row i0+j, j = 0..S (S = next node)
 //   T      shared-memory copy of the uniform tables for this axis
-//   w0/ws  shared-memory slots of rows j = 0..S-2 (general path keeps y_j there)
-//   c0/cst shared-memory codes of the same nodes (general path)
+//   w0/WS  shared-memory slots of rows j = 0..S-2 (general path keeps y_j there)
 //   al/be  L1-resident local arrays for the general path
-// Returns the table type (0 interior, 1 first, 2 last) for a uniform segment, -1 otherwise.
-template <int S, int WS, int CST>
+// Returns the table type (>= 0) or -1 (general segment).
+template <int S, int WS>
 __device__ __forceinline__ int seg_eliminate(const SweepArgs& a, double (&r)[S],
-                                              unsigned long long amask, int i0, int first,
-                                              int sh, const double* T, double* w0,
-                                              const uint8_t* c0, double (&al)[S],
-                                              double (&be)[S], SegOut& o) {
+                                             unsigned long long amask, int i0, int first,
+                                             const double* T, double* w0, double (&al)[S],
+                                             double (&be)[S], SegOut& o) {
   const int m = a.m;
-  const unsigned long long allm = (1ull << S) - 1ull;
-  const unsigned long long seg_bits = amask & allm;
-  int ttype = -1;
-  if (seg_bits == 0ull || seg_bits == allm) {
-    if (i0 + S <= m) ttype = first ? 1 : 0;
-    else if (i0 + S - 1 == m && !first) ttype = 2;
-  }
+  const int ttype = seg_type<S>(amask, i0, m, first);
   o.rs = r[S - 1];
-  {
-    const uint32_t em = (uint32_t)(amask >> (S - 1)) & 1u, ep = (uint32_t)(amask >> S) & 1u;
-    row_coefs(a.co, i0 + S - 1, m, em, ep, o.as, o.bs, o.cs);
-  }
+  row_coefs(a.co, i0 + S - 1, m, (uint32_t)(amask >> (S - 1)) & 1u,
+            (uint32_t)(amask >> S) & 1u, o.as, o.bs, o.cs);
   if (ttype >= 0) {
-    if (ttype == 0 && seg_bits == 0ull)
+    if (ttype == 0 && !(amask & 1ull)) {
       uni_eliminate<S>(r, [&](int q, int j) { return a.tmid[q * kTabRows + j]; }, o);
-    else {
-      const double* Tv = T + (ttype * 2 + (seg_bits ? 1 : 0)) * 5 * kTabRows;
+    } else {
+      const double* Tv = T + (ttype * 2 + (int)(amask & 1ull)) * 5 * kTabRows;
       uni_eliminate<S>(r, [&](int q, int j) { return Tv[q * kTabRows + j]; }, o);
     }
     return ttype;
@@ -309,7 +318,7 @@ __device__ __forceinline__ int seg_eliminate(const SweepArgs& a, double (&r)[S],
   double cpp = 0.0, dyp = 0.0, dap = 1.0, lastinv = 0.0, lastc = 0.0;
 #pragma unroll 1
   for (int j = 0; j < S - 1; ++j) {
-    const uint32_t em = (c0[j * CST] >> sh) & 1u, ep = (c0[(j + 1) * CST] >> sh) & 1u;
+    const uint32_t em = (uint32_t)(amask >> j) & 1u, ep = (uint32_t)(amask >> (j + 1)) & 1u;
     double av, bv, cv;
     row_coefs(a.co, i0 + j, m, em, ep, av, bv, cv);
     const double inv = fast_rcp(fma(-av, cpp, bv));
@@ -356,7 +365,7 @@ __device__ __forceinline__ void seg_finish(const SweepArgs& a, int ttype, const 
   if (ttype == 0 && !(amask & 1ull)) {
     uni_finish<S, WS>(r, [&](int q, int j) { return a.tmid[q * kTabRows + j]; }, tm, t, w0);
   } else if (ttype >= 0) {
-    const double* Tv = T + (ttype * 2 + (amask & 1ull ? 1 : 0)) * 5 * kTabRows;
+    const double* Tv = T + (ttype * 2 + (int)(amask & 1ull)) * 5 * kTabRows;
     uni_finish<S, WS>(r, [&](int q, int j) { return Tv[q * kTabRows + j]; }, tm, t, w0);
   } else {
 #pragma unroll 1
@@ -375,12 +384,19 @@ __device__ __forceinline__ void reduced_row(const SegOut& o, double yFn, double 
 }
 
 // ---------------------------------------------------------------------------------------
-// Strided axes (0, 1).  blockDim = (8 columns, 32 segments); block (x = k group, y = outer).
-// Shared memory: tables | W[NR][8] stage/solution | Y[NR][8] (AOS/MAOS) | 4x256 scratch |
-// codes C[NR][8].
+// Strided axes (0, 1).  blockDim = (LB columns, 32 segments); block (x = k group, y = outer).
+// Shared memory: tables | reduced inverse | W[NR][LB] stage/solution | Y[NR][LB] (AOS/MAOS)
+// | 4x(LB*32) scratch | descriptors D[32][LB][2].
 template <int S>
 __host__ __device__ constexpr int strided_rows() {
   return kSeg * S + 2;
+}
+
+template <int LB>
+__host__ __device__ constexpr size_t strided_smem(int S, bool needY) {
+  return sizeof(double) * (kTabDoubles + kSeg * kSeg + (needY ? 2 : 1) * (size_t)(kSeg * S + 2) * LB +
+                           4 * LB * kSeg) +
+         sizeof(unsigned long long) * 2 * kSeg * LB;
 }
 
 template <int S, bool CN, int LB>
@@ -397,7 +413,7 @@ __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
   const int k0 = 1 + blockIdx.x * LB;
   const int outer = 1 + blockIdx.y;
   const int ncols = min(LB, L.n2 - 1 - k0);  // active columns in this tile
-  if (ncols <= 0) return;                     // cluster padding block
+  const int K = L.n2 - 2;
   long long base;
   int stride;
   if (axis == 0) {
@@ -409,18 +425,16 @@ __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
   }
   const int needY = epi_needs(a.epi);
   double* T = sm;
-  double* W = T + kTabDoubles;
+  double* Mi = T + kTabDoubles;
+  double* W = Mi + kSeg * kSeg;
   double* Yt = W + NR * LB;
   double* X = Yt + (needY ? NR * LB : 0);
-  uint8_t* C = reinterpret_cast<uint8_t*>(X + 4 * NT);
-  const int sh = 1 + axis;
+  unsigned long long* D = reinterpret_cast<unsigned long long*>(X + 4 * NT);
   const double* gsrc = a.src + base;
-  const double* gface = (a.pro == PRO_FLOW ? a.bnd : a.src) + base;
   const double* gy = (needY == 1 ? a.src : a.acc) + base;
   const double* grho = a.rho + base;
 
-  // Phase 1: asynchronous staging of the field (+ epilogue operand), codes and tables.
-  // Thread t copies the 16-byte chunk (t & 3) of rows t/4, t/4 + 64, ...
+  // Phase 1: asynchronous staging of the field (+ epilogue operand), descriptors, tables.
   {
     const int q = (tid % CPR) * 2, p0 = tid / CPR;
     const long long gstep = (long long)RPP * stride;
@@ -435,117 +449,132 @@ __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
       for (int p = p0; p < nl; p += RPP, gyp += gstep, yp += RPP * LB) cp_async16(yp, gyp);
     }
   }
-  for (int p = tid; p < nl; p += NT) {
-    if (LB == 8) cp_async8(C + p * LB, a.codes + base + (long long)p * stride);
-    else cp_async16(C + p * LB, a.codes + base + (long long)p * stride);
-  }
+  cp_async16(D + 2 * tid, a.desc + 2 * (((long long)(outer - 1) * kSeg + seg) * K + (k0 - 1 + lane)));
   for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
+  if (a.static_ok)
+    for (int c = tid; c < kSeg * kSeg / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
   cp_async_wait_all();
   __syncthreads();
   if (a.pro == PRO_FLOW && tid < 2 * LB) {  // flow stages see the Dirichlet faces
     const int p = tid < LB ? 0 : nl - 1, l = tid % LB;
-    W[p * LB + l] = gface[(long long)p * stride + l];
+    W[p * LB + l] = a.bnd[base + (long long)p * stride + l];
   }
   if (a.pro != PRO_NONE) {  // prologue in place on the interior rows
     const int l = tid % LB;
-    for (int p = 1 + tid / LB; p < nl - 1; p += NT / LB)
-      W[p * LB + l] = pro_val(a, W[p * LB + l], C[p * LB + l], grho + (long long)p * stride + l);
+    for (int p = 1 + tid / LB; p < nl - 1; p += NT / LB) {
+      const int sg = (p - 1) / S;
+      const uint32_t c = node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
+      W[p * LB + l] = pro_val(a, W[p * LB + l], c, grho + (long long)p * stride + l);
+    }
   }
   __syncthreads();
 
   if (a.dbg == 1) goto store;
   {
-  // Phase 2: rhs of the own rows (registers), local elimination.
-  const bool active = lane < ncols;
-  const int i0 = seg * S;
-  double r[S];
-  unsigned long long amask = 0;
-  unsigned cmask = 0;
+    // Phase 2: rhs of the own rows (registers), local elimination.
+    const bool active = lane < ncols;
+    const int i0 = seg * S;
+    const unsigned long long amask = D[2 * tid];
+    const unsigned cmask = (unsigned)(D[2 * tid + 1] >> 32);
+    double r[S];
+    double blo = 0.0, bhi = 0.0;
+    if (active && i0 == 0) blo = a.bnd[base + lane];
+    if (active && i0 <= m - 1 && m - 1 < i0 + S) bhi = a.bnd[base + (long long)(m + 1) * stride + lane];
+    {
+      const double* wrow = W + (i0 + 1) * LB + lane;
 #pragma unroll
-  for (int j = 0; j <= S; ++j) {
-    const uint32_t c = C[(i0 + j + 1) * LB + lane];  // rows past nl: unused garbage bits
-    amask |= (unsigned long long)((c >> sh) & 1u) << j;
-    if (j < S) cmask |= ((c >> 4) & 1u) << j;
-  }
-  double blo = 0.0, bhi = 0.0;
-  if (active && i0 == 0) blo = a.bnd[base + lane];
-  if (active && i0 <= m - 1 && m - 1 < i0 + S) bhi = a.bnd[base + (long long)(m + 1) * stride + lane];
-  {
-    const double* wrow = W + (i0 + 1) * LB + lane;
-#pragma unroll
-    for (int j = 0; j < S; ++j) {
-      const double wc = wrow[j * LB];
-      r[j] = CN ? cn_term(a, (uint32_t)(amask >> j) & 1u, (uint32_t)(amask >> (j + 1)) & 1u,
-                          wrow[(j - 1) * LB], wc, wrow[(j + 1) * LB])
-                : wc;
+      for (int j = 0; j < S; ++j) {
+        const double wc = wrow[j * LB];
+        r[j] = CN ? cn_term(a, (uint32_t)(amask >> j) & 1u, (uint32_t)(amask >> (j + 1)) & 1u,
+                            wrow[(j - 1) * LB], wc, wrow[(j + 1) * LB])
+                  : wc;
+      }
+      const double* rrow = grho + (i0 + 1) * stride + lane;
+      rhs_rare<S>(a, r, amask, cmask, i0, [&](int j) { return rrow + j * stride; }, blo, bhi);
     }
-    const double* rrow = grho + (i0 + 1) * stride + lane;
-    rhs_rare<S>(a, r, amask, cmask, i0, [&](int j) { return rrow + j * stride; }, blo, bhi);
-  }
-  __syncthreads();  // all stencil reads of W done; rows are private from here on
+    // clean tile: every line of the tile is one dielectric (palette 0) end to end
+    const bool clean = __syncthreads_and(!active || amask == 0ull) && a.static_ok;
 
-  double al[S], be[S];
-  SegOut o;
-  double* w0 = W + (i0 + 1) * LB + lane;
-  const int ttype = seg_eliminate<S, LB, LB>(a, r, amask, i0, seg == 0, sh, T, w0,
-                                            C + (i0 + 1) * LB + lane, al, be, o);
+    double al[S], be[S];
+    SegOut o;
+    double* w0 = W + (i0 + 1) * LB + lane;
+    const int ttype = seg_eliminate<S, LB>(a, r, amask, i0, seg == 0, T, w0, al, be, o);
 
-  // Phase 3: reduced system over the 32 separators of each line (PCR in shared memory).
-  double* sA = X;
-  double* sB = X + NT;
-  double* sC = X + 2 * NT;
-  double* sR = X + 3 * NT;
-  sA[tid] = o.yF;
-  sB[tid] = o.aF;
-  sC[tid] = o.bF;
-  __syncthreads();
-  double yFn = 0.0, aFn = 0.0, bFn = 0.0;
-  if (seg + 1 < kSeg) {
-    yFn = sA[tid + LB];
-    aFn = sB[tid + LB];
-    bFn = sC[tid + LB];
-  }
-  __syncthreads();
-  double A, B, Cc, R;
-  reduced_row(o, yFn, aFn, bFn, A, B, Cc, R);
+    // Phase 3: reduced system over the 32 separators of each line.
+    double* sA = X;
+    double* sB = X + NT;
+    double* sC = X + 2 * NT;
+    double* sR = X + 3 * NT;
+    double t, tm;
+    if (clean) {  // static inverse: one exchange of y_F, one of R, then two dot products
+      sA[tid] = o.yF;
+      __syncthreads();
+      const double yFn = (seg + 1 < kSeg) ? sA[tid + LB] : 0.0;
+      sR[tid] = o.rs - o.as * o.yL - o.cs * yFn;
+      __syncthreads();
+      const int k1 = seg > 0 ? seg - 1 : 0;  // transposed inverse: column q at Mi[q*32]
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll 8
+      for (int q = 0; q < kSeg; ++q) {
+        const double Rq = sR[q * LB + lane];
+        s0 = fma(Mi[q * kSeg + seg], Rq, s0);
+        s1 = fma(Mi[q * kSeg + k1], Rq, s1);
+      }
+      t = s0;
+      tm = seg > 0 ? s1 : 0.0;
+    } else {  // parallel cyclic reduction
+      sA[tid] = o.yF;
+      sB[tid] = o.aF;
+      sC[tid] = o.bF;
+      __syncthreads();
+      double yFn = 0.0, aFn = 0.0, bFn = 0.0;
+      if (seg + 1 < kSeg) {
+        yFn = sA[tid + LB];
+        aFn = sB[tid + LB];
+        bFn = sC[tid + LB];
+      }
+      __syncthreads();
+      double A, B, Cc, R;
+      reduced_row(o, yFn, aFn, bFn, A, B, Cc, R);
 #pragma unroll
-  for (int d = 1; d < kSeg; d <<= 1) {
-    sA[tid] = A;
-    sB[tid] = fast_rcp(B);
-    sC[tid] = Cc;
-    sR[tid] = R;
+      for (int d = 1; d < kSeg; d <<= 1) {
+        sA[tid] = A;
+        sB[tid] = fast_rcp(B);
+        sC[tid] = Cc;
+        sR[tid] = R;
+        __syncthreads();
+        double Am = 0.0, iBm = 1.0, Cm = 0.0, Rm = 0.0, Ap = 0.0, iBp = 1.0, Cp = 0.0, Rp = 0.0;
+        if (seg >= d) {
+          const int q = tid - d * LB;
+          Am = sA[q];
+          iBm = sB[q];
+          Cm = sC[q];
+          Rm = sR[q];
+        }
+        if (seg + d < kSeg) {
+          const int q = tid + d * LB;
+          Ap = sA[q];
+          iBp = sB[q];
+          Cp = sC[q];
+          Rp = sR[q];
+        }
+        __syncthreads();
+        const double k1 = -A * iBm, k2 = -Cc * iBp;
+        A = k1 * Am;
+        Cc = k2 * Cp;
+        B = B + k1 * Cm + k2 * Ap;
+        R = R + k1 * Rm + k2 * Rp;
+      }
+      t = R * fast_rcp(B);
+      sA[tid] = t;
+      __syncthreads();
+      tm = (seg > 0) ? sA[tid - LB] : 0.0;
+    }
+
+    // Phase 4: reconstruct the inner rows, separator = t.
+    seg_finish<S, LB>(a, ttype, r, amask, tm, t, T, w0, al, be);
+    if (i0 + S - 1 < m) W[(i0 + S) * LB + lane] = t;
     __syncthreads();
-    double Am = 0.0, iBm = 1.0, Cm = 0.0, Rm = 0.0, Ap = 0.0, iBp = 1.0, Cp = 0.0, Rp = 0.0;
-    if (seg >= d) {
-      const int q = tid - d * LB;
-      Am = sA[q];
-      iBm = sB[q];
-      Cm = sC[q];
-      Rm = sR[q];
-    }
-    if (seg + d < kSeg) {
-      const int q = tid + d * LB;
-      Ap = sA[q];
-      iBp = sB[q];
-      Cp = sC[q];
-      Rp = sR[q];
-    }
-    __syncthreads();
-    const double k1 = -A * iBm, k2 = -Cc * iBp;
-    A = k1 * Am;
-    Cc = k2 * Cp;
-    B = B + k1 * Cm + k2 * Ap;
-    R = R + k1 * Rm + k2 * Rp;
-  }
-  const double t = R * fast_rcp(B);
-  sA[tid] = t;
-  __syncthreads();
-  const double tm = (seg > 0) ? sA[tid - LB] : 0.0;
-
-  // Phase 4: reconstruct the inner rows, separator = t.
-  seg_finish<S, LB>(a, ttype, r, amask, tm, t, T, w0, al, be);
-  if (i0 + S - 1 < m) W[(i0 + S) * LB + lane] = t;
-  __syncthreads();
   }
 store:
   // Phase 5: epilogue + coalesced store of the interior rows.
@@ -568,8 +597,10 @@ store:
     if (l < ncols) {
       for (int p = 1 + tid / LB; p <= m; p += NT / LB) {
         const int c = p * LB + l;
+        const int sg = (p - 1) / S;
+        const uint32_t bits = node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
         const long long off = (long long)p * stride + l;
-        const double x = epi_val(a, W[c], needY ? Yt[c] : 0.0, C[c], grho + off);
+        const double x = epi_val(a, W[c], needY ? Yt[c] : 0.0, bits, grho + off);
         gdst[off] = x;
         bad |= is_bad(x, a.thr);
       }
@@ -601,18 +632,18 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
   extern __shared__ double sm[];
   if (a.div_step && *((volatile int*)a.div_step) < a.step) return;
   constexpr int BUF = contig_buf_doubles<S>();
-  constexpr int CBUF = 32 * S + 64;
   constexpr int W = kContigWarps;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int needY = epi_needs(a.epi);
   const int YB = needY ? 32 * S + 2 : 0;
   double* T = sm;
-  double* buf = T + kTabDoubles + warp * (BUF + YB);
+  double* Mi = T + kTabDoubles;
+  double* buf = Mi + kSeg * kSeg + warp * (BUF + YB + kSeg);
   double* ybuf = buf + BUF;
-  uint8_t* craw = reinterpret_cast<uint8_t*>(T + kTabDoubles + W * (BUF + YB)) + warp * CBUF;
-  const uint8_t* cbuf = craw + kOff;  // cbuf[e] = code of node e
 
   for (int c = threadIdx.x; c < kTabDoubles / 2; c += 32 * W) cp_async16(T + 2 * c, a.tab + 2 * c);
+  if (a.static_ok)
+    for (int c = threadIdx.x; c < kSeg * kSeg / 2; c += 32 * W) cp_async16(Mi + 2 * c, a.minv + 2 * c);
   const int line = blockIdx.x * W + warp;
   const bool live = line < nlines;
   const Layout& L = a.L;
@@ -621,10 +652,10 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
   const long long rb = L.at(ii, jj, 0);
   const double* gsrc = a.src + rb;
   const double* grho = a.rho + rb;
+  unsigned long long dw0 = 0, dw1 = 0;
 
   // Phase 1: asynchronous staging.
   if (live) {
-    const double* gface = (a.pro == PRO_FLOW ? a.bnd : a.src) + rb;
     const double* gy = (needY == 1 ? a.src : a.acc) + rb;
 #pragma unroll 4
     for (int e = lane; e < n2; e += 32) cp_async8(buf + cpos<S>(e), gsrc + e);
@@ -632,8 +663,9 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
 #pragma unroll 4
       for (int e = lane; e < n2; e += 32) cp_async8(ybuf + e, gy + e);
     }
-    const int nch = (n2 + kOff + 15) / 16;
-    for (int q = lane; q < nch; q += 32) cp_async16(craw + 16 * q, a.codes + (rb - kOff) + 16 * q);
+    const unsigned long long* dp = a.desc + 2 * ((long long)line * kSeg + lane);
+    dw0 = dp[0];
+    dw1 = dp[1];
   }
   cp_async_wait_all();
   __syncthreads();  // tables are shared by the block
@@ -643,21 +675,19 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
     buf[cpos<S>(e)] = a.bnd[rb + e];
   }
   if (a.pro != PRO_NONE) {
-    for (int e = lane + 1; e < n2 - 1; e += 32)
-      buf[cpos<S>(e)] = pro_val(a, buf[cpos<S>(e)], cbuf[e], grho + e);
+    for (int e0 = 1; e0 < n2 - 1; e0 += 32) {  // warp-uniform trip count (shuffles inside)
+      const int e = e0 + lane;
+      const int sg = min((e - 1) / S, kSeg - 1);
+      const uint32_t c = node_bits(__shfl_sync(0xffffffffu, dw1, sg), (e - 1) - sg * S);
+      if (e < n2 - 1) buf[cpos<S>(e)] = pro_val(a, buf[cpos<S>(e)], c, grho + e);
+    }
     __syncwarp();
   }
 
   const int i0 = lane * S;
+  const unsigned long long amask = dw0;
+  const unsigned cmask = (unsigned)(dw1 >> 32);
   double r[S];
-  unsigned long long amask = 0;
-  unsigned cmask = 0;
-#pragma unroll
-  for (int j = 0; j <= S; ++j) {
-    const uint32_t c = cbuf[i0 + j + 1];  // past the row end: unused garbage bits
-    amask |= (unsigned long long)((c >> 3) & 1u) << j;
-    if (j < S) cmask |= ((c >> 4) & 1u) << j;
-  }
   double blo = 0.0, bhi = 0.0;
   if (i0 == 0) blo = a.bnd[rb];
   if (i0 <= m - 1 && m - 1 < i0 + S) bhi = a.bnd[rb + m + 1];
@@ -670,52 +700,70 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
               : wc;
   }
   rhs_rare<S>(a, r, amask, cmask, i0, [&](int j) { return grho + i0 + j + 1; }, blo, bhi);
+  const bool clean = __all_sync(0xffffffffu, amask == 0ull) && a.static_ok;
   __syncwarp();
 
   double al[S], be[S];
   SegOut o;
   double* w0 = buf + cpos<S>(i0 + 1);
-  const int ttype = seg_eliminate<S, 1, 1>(a, r, amask, i0, lane == 0, 3, T, w0, cbuf + i0 + 1,
-                                          al, be, o);
+  const int ttype = seg_eliminate<S, 1>(a, r, amask, i0, lane == 0, T, w0, al, be, o);
 
-  double yFn = __shfl_down_sync(0xffffffffu, o.yF, 1);
-  double aFn = __shfl_down_sync(0xffffffffu, o.aF, 1);
-  double bFn = __shfl_down_sync(0xffffffffu, o.bF, 1);
-  if (lane == 31) yFn = aFn = bFn = 0.0;
-  double A, B, Cc, R;
-  reduced_row(o, yFn, aFn, bFn, A, B, Cc, R);
+  const double yFn0 = __shfl_down_sync(0xffffffffu, o.yF, 1);
+  double t, tm;
+  if (clean) {  // static inverse of the clean-line reduced system
+    double* sR = ybuf + YB;  // 32 doubles per warp after the row buffers
+    sR[lane] = o.rs - o.as * o.yL - o.cs * (lane == 31 ? 0.0 : yFn0);
+    __syncwarp();
+    const int k1 = lane > 0 ? lane - 1 : 0;  // transposed inverse: column q at Mi[q*32]
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll 8
+    for (int q = 0; q < kSeg; ++q) {
+      const double Rq = sR[q];  // broadcast
+      s0 = fma(Mi[q * kSeg + lane], Rq, s0);
+      s1 = fma(Mi[q * kSeg + k1], Rq, s1);
+    }
+    t = s0;
+    tm = lane > 0 ? s1 : 0.0;
+  } else {
+    double yFn = yFn0;
+    double aFn = __shfl_down_sync(0xffffffffu, o.aF, 1);
+    double bFn = __shfl_down_sync(0xffffffffu, o.bF, 1);
+    if (lane == 31) yFn = aFn = bFn = 0.0;
+    double A, B, Cc, R;
+    reduced_row(o, yFn, aFn, bFn, A, B, Cc, R);
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const double iB = fast_rcp(B);
-    double Am = __shfl_up_sync(0xffffffffu, A, d);
-    double iBm = __shfl_up_sync(0xffffffffu, iB, d);
-    double Cm = __shfl_up_sync(0xffffffffu, Cc, d);
-    double Rm = __shfl_up_sync(0xffffffffu, R, d);
-    double Ap = __shfl_down_sync(0xffffffffu, A, d);
-    double iBp = __shfl_down_sync(0xffffffffu, iB, d);
-    double Cp = __shfl_down_sync(0xffffffffu, Cc, d);
-    double Rp = __shfl_down_sync(0xffffffffu, R, d);
-    if (lane < d) {
-      Am = 0.0;
-      iBm = 1.0;
-      Cm = 0.0;
-      Rm = 0.0;
+    for (int d = 1; d < 32; d <<= 1) {
+      const double iB = fast_rcp(B);
+      double Am = __shfl_up_sync(0xffffffffu, A, d);
+      double iBm = __shfl_up_sync(0xffffffffu, iB, d);
+      double Cm = __shfl_up_sync(0xffffffffu, Cc, d);
+      double Rm = __shfl_up_sync(0xffffffffu, R, d);
+      double Ap = __shfl_down_sync(0xffffffffu, A, d);
+      double iBp = __shfl_down_sync(0xffffffffu, iB, d);
+      double Cp = __shfl_down_sync(0xffffffffu, Cc, d);
+      double Rp = __shfl_down_sync(0xffffffffu, R, d);
+      if (lane < d) {
+        Am = 0.0;
+        iBm = 1.0;
+        Cm = 0.0;
+        Rm = 0.0;
+      }
+      if (lane + d >= 32) {
+        Ap = 0.0;
+        iBp = 1.0;
+        Cp = 0.0;
+        Rp = 0.0;
+      }
+      const double k1 = -A * iBm, k2 = -Cc * iBp;
+      A = k1 * Am;
+      Cc = k2 * Cp;
+      B = B + k1 * Cm + k2 * Ap;
+      R = R + k1 * Rm + k2 * Rp;
     }
-    if (lane + d >= 32) {
-      Ap = 0.0;
-      iBp = 1.0;
-      Cp = 0.0;
-      Rp = 0.0;
-    }
-    const double k1 = -A * iBm, k2 = -Cc * iBp;
-    A = k1 * Am;
-    Cc = k2 * Cp;
-    B = B + k1 * Cm + k2 * Ap;
-    R = R + k1 * Rm + k2 * Rp;
+    t = R * fast_rcp(B);
+    tm = __shfl_up_sync(0xffffffffu, t, 1);
+    if (lane == 0) tm = 0.0;
   }
-  const double t = R * fast_rcp(B);
-  double tm = __shfl_up_sync(0xffffffffu, t, 1);
-  if (lane == 0) tm = 0.0;
 
   seg_finish<S, 1>(a, ttype, r, amask, tm, t, T, w0, al, be);
   if (i0 + S - 1 < m) buf[cpos<S>(i0 + S)] = t;
@@ -726,10 +774,15 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
   if (a.epi == EPI_STORE && !a.check) {
     for (int p = lane + 1; p <= m; p += 32) gdst[p] = buf[cpos<S>(p)];
   } else {
-    for (int p = lane + 1; p <= m; p += 32) {
-      const double x = epi_val(a, buf[cpos<S>(p)], needY ? ybuf[p] : 0.0, cbuf[p], grho + p);
-      gdst[p] = x;
-      bad |= is_bad(x, a.thr);
+    for (int p0 = 1; p0 <= m; p0 += 32) {  // warp-uniform trip count (shuffles inside)
+      const int p = p0 + lane;
+      const int sg = min((p - 1) / S, kSeg - 1);
+      const uint32_t bits = node_bits(__shfl_sync(0xffffffffu, dw1, sg), (p - 1) - sg * S);
+      if (p <= m) {
+        const double x = epi_val(a, buf[cpos<S>(p)], needY ? ybuf[p] : 0.0, bits, grho + p);
+        gdst[p] = x;
+        bad |= is_bad(x, a.thr);
+      }
     }
   }
   if (a.check) {
@@ -738,10 +791,57 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
 }
 
 // ---------------------------------------------------------------------------------------
+// Segment descriptors, built once per march and axis from the 1-byte node codes:
+//   word 0: bit j = eps bit (axis) of the node of row i0+j, j = 0..S (zero past node m+1)
+//   word 1: bits 0..S-1 solute bit of the nodes of rows i0..i0+S-1; bits 32.. charged bits
+// Layout: strided axes ((outer-1)*32 + seg)*K + (k-1); contiguous axis line*32 + seg.
+__global__ void k_build_desc(const Layout L, int axis, int S, const uint8_t* __restrict__ codes,
+                             unsigned long long* __restrict__ desc) {
+  const int m = (axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2)) - 2;
+  long long nseg;
+  if (axis == 2) nseg = (long long)(L.n0 - 2) * (L.n1 - 2) * kSeg;
+  else nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * kSeg * (L.n2 - 2);
+  const int sh = 1 + axis;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nseg;
+       t += (long long)gridDim.x * blockDim.x) {
+    long long base, stride;
+    int seg;
+    if (axis == 2) {
+      const long long line = t / kSeg;
+      seg = (int)(t % kSeg);
+      base = L.at(1 + (int)(line / (L.n1 - 2)), 1 + (int)(line % (L.n1 - 2)), 0);
+      stride = 1;
+    } else {
+      const int K = L.n2 - 2;
+      const int k = 1 + (int)(t % K);
+      const long long os = t / K;
+      seg = (int)(os % kSeg);
+      const int outer = 1 + (int)(os / kSeg);
+      base = axis == 0 ? L.at(0, outer, k) : L.at(outer, 0, k);
+      stride = axis == 0 ? L.s0 : L.pitch;
+    }
+    const int i0 = seg * S;
+    unsigned long long w0 = 0, w1 = 0;
+    for (int j = 0; j <= S; ++j) {
+      const int p = i0 + j + 1;
+      if (p > m + 1) break;
+      const uint32_t c = codes[base + p * stride];
+      w0 |= (unsigned long long)((c >> sh) & 1u) << j;
+      if (j < S && p <= m) {
+        w1 |= (unsigned long long)(c & 1u) << j;
+        w1 |= (unsigned long long)((c >> 4) & 1u) << (32 + j);
+      }
+    }
+    desc[2 * t] = w0;
+    desc[2 * t + 1] = w1;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // Host-side launch helpers.
 
 static int seg_S(int m) {
-  const int opts[] = {2, 3, 4, 6, 8, 12, 16, 24, 32};
+  const int opts[] = {2, 3, 4, 6, 8, 12, 16, 24};
   for (int s : opts)
     if (kSeg * s >= m) return s;
   return 0;
@@ -752,10 +852,7 @@ static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
   const int nouter = (axis == 0 ? a.L.n1 : a.L.n0) - 2;
   dim3 grid((a.L.n2 - 2 + LB - 1) / LB, nouter);
   dim3 block(LB, kSeg);
-  const size_t NR = strided_rows<S>();
-  const size_t tiles = epi_needs(a.epi) ? 2 : 1;
-  const size_t smem =
-      sizeof(double) * (kTabDoubles + tiles * NR * LB + 4 * LB * kSeg) + NR * LB;
+  const size_t smem = strided_smem<LB>(S, epi_needs(a.epi) != 0);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_sweep_strided<S, CN, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
@@ -781,8 +878,8 @@ static void launch_contig_SC(const SweepArgs& a, cudaStream_t st) {
   const int W = kContigWarps;
   const int nlines = (a.L.n0 - 2) * (a.L.n1 - 2);
   const size_t yb = epi_needs(a.epi) ? 32 * S + 2 : 0;
-  const size_t smem = sizeof(double) * kTabDoubles +
-                      (size_t)W * ((contig_buf_doubles<S>() + yb) * sizeof(double) + (32 * S + 64));
+  const size_t smem = sizeof(double) * (kTabDoubles + kSeg * kSeg) +
+                      (size_t)W * (contig_buf_doubles<S>() + yb + kSeg) * sizeof(double);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_sweep_contig<S, CN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
@@ -805,8 +902,7 @@ static void launch_contig_S(const SweepArgs& a, cudaStream_t st) {
     case 12: CALL(12); break;                                                           \
     case 16: CALL(16); break;                                                           \
     case 24: CALL(24); break;                                                           \
-    case 32: CALL(32); break;                                                           \
-    default: return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 1024)"); \
+    default: return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 768)"); \
   }
 
 static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
@@ -824,8 +920,6 @@ static int launch_contig(const SweepArgs& a, cudaStream_t st) {
   PBG_LAUNCH_CHECK("k_sweep_contig");
   return PBG_OK;
 }
-
-static int sweep_S(int /*axis*/, int m) { return seg_S(m); }
 
 // Tridiagonal row tables for one axis: f = factor / h^2 (tridiag.py:165, 179-181, 199-202).
 static AxisCoef make_axis_coef(const double eps[2], double factor, double h) {
@@ -878,6 +972,56 @@ static void make_tables(const AxisCoef& co, int S, double* out) {
   }
 }
 
+// Dense inverse of the reduced (separator) system of a clean line: every node carries eps
+// palette 0, segment k uses table type first / interior / last.  Valid when 32*S is m or
+// m + 1 (the last separator is row m-1 or the padding row m).
+static bool make_reduced_inverse(const AxisCoef& co, const double* tab, int S, int m,
+                                 double* minv) {
+  if (!(kSeg * S == m || kSeg * S == m + 1)) return false;
+  auto T = [&](int type, int q, int j) { return tab[(type * 2) * 5 * kTabRows + q * kTabRows + j]; };
+  auto type_of = [&](int k) { return k == 0 ? 1 : ((k == kSeg - 1 && kSeg * S == m + 1) ? 2 : 0); };
+  double A[kSeg], B[kSeg], C[kSeg];
+  for (int k = 0; k < kSeg; ++k) {
+    const int ty = type_of(k), i = k * S + S - 1;
+    if (i >= m) {
+      A[k] = 0.0;
+      B[k] = 1.0;
+      C[k] = 0.0;
+      continue;
+    }
+    const double as = co.sub[0], bs = co.diag[0], cs = (i == m - 1) ? 0.0 : co.sup[0];
+    double aFn = 0.0, bFn = 0.0;
+    if (k + 1 < kSeg) {
+      aFn = T(type_of(k + 1), TQ_AL, 0);
+      bFn = T(type_of(k + 1), TQ_BE, 0);
+    }
+    A[k] = as * T(ty, TQ_AL, S - 2);
+    B[k] = bs + as * T(ty, TQ_BE, S - 2) + cs * aFn;
+    C[k] = cs * bFn;
+  }
+  double M[kSeg][2 * kSeg];
+  for (int r = 0; r < kSeg; ++r)
+    for (int c = 0; c < 2 * kSeg; ++c) M[r][c] = 0.0;
+  for (int r = 0; r < kSeg; ++r) {
+    if (r > 0) M[r][r - 1] = A[r];
+    M[r][r] = B[r];
+    if (r + 1 < kSeg) M[r][r + 1] = C[r];
+    M[r][kSeg + r] = 1.0;
+  }
+  for (int c = 0; c < kSeg; ++c) {  // Gauss-Jordan, diagonally dominant: no pivoting
+    const double piv = M[c][c];
+    for (int q = 0; q < 2 * kSeg; ++q) M[c][q] /= piv;
+    for (int r = 0; r < kSeg; ++r) {
+      if (r == c || M[r][c] == 0.0) continue;
+      const double f = M[r][c];
+      for (int q = 0; q < 2 * kSeg; ++q) M[r][q] -= f * M[c][q];
+    }
+  }
+  for (int r = 0; r < kSeg; ++r)  // stored transposed: minv[q*32 + k] = inverse[k][q]
+    for (int c = 0; c < kSeg; ++c) minv[c * kSeg + r] = M[r][kSeg + c];
+  return true;
+}
+
 static void set_decays(SweepArgs& a, double d0, double d1) {
   a.decay0 = d0;
   a.decay1 = d1;
@@ -899,27 +1043,45 @@ static SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, 
   return a;
 }
 
-// Device copy of the axes' tables for one launch sequence (stream ordered).
-static int upload_tables(const SweepArgs ax[], int naxes, const int axes[], double** dtab,
-                         cudaStream_t st) {
-  std::vector<double> host((size_t)naxes * kTabDoubles);
-  for (int q = 0; q < naxes; ++q) {
-    const int S = sweep_S(axes[q], ax[q].m);
-    if (S < 2) return fail(PBG_E_UNSUPPORTED, "line too long (m > 1024)");
-    make_tables(ax[q].co, S, host.data() + (size_t)q * kTabDoubles);
-  }
-  PBG_CUDA(cudaMallocAsync(dtab, host.size() * sizeof(double), st));
-  PBG_CUDA(cudaMemcpyAsync(*dtab, host.data(), host.size() * sizeof(double),
+// Per-launch-sequence device data of one axis: tables, reduced inverse, segment descriptors.
+struct AxisAux {
+  double* buf = nullptr;
+  unsigned long long* desc = nullptr;
+};
+
+static long long desc_segments(const Layout& L, int axis) {
+  if (axis == 2) return (long long)(L.n0 - 2) * (L.n1 - 2) * kSeg;
+  return (long long)((axis == 0 ? L.n1 : L.n0) - 2) * kSeg * (L.n2 - 2);
+}
+
+static int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
+                        cudaStream_t st) {
+  const int S = seg_S(a.m);
+  if (S < 2) return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 768)");
+  std::vector<double> host(kTabDoubles + kSeg * kSeg, 0.0);
+  make_tables(a.co, S, host.data());
+  memcpy(a.tmid, host.data(), sizeof(a.tmid));  // type 0 (interior), palette 0
+  a.static_ok = make_reduced_inverse(a.co, host.data(), S, a.m, host.data() + kTabDoubles) ? 1 : 0;
+  PBG_CUDA(cudaMallocAsync(&aux.buf, host.size() * sizeof(double), st));
+  PBG_CUDA(cudaMemcpyAsync(aux.buf, host.data(), host.size() * sizeof(double),
                            cudaMemcpyHostToDevice, st));
-  // the host vector dies here; make the copy complete before returning
-  PBG_CUDA(cudaStreamSynchronize(st));
+  const long long nseg = desc_segments(a.L, axis);
+  // +64 words of slack: tiles past the last interior column read (unused) descriptors
+  PBG_CUDA(cudaMallocAsync(&aux.desc, (2 * nseg + 64) * sizeof(unsigned long long), st));
+  k_build_desc<<<148 * 8, 256, 0, st>>>(a.L, axis, S, codes, aux.desc);
+  PBG_LAUNCH_CHECK("k_build_desc");
+  PBG_CUDA(cudaStreamSynchronize(st));  // host staging vector dies here
+  a.tab = aux.buf;
+  a.minv = aux.buf + kTabDoubles;
+  a.desc = aux.desc;
   return PBG_OK;
 }
 
-static void fill_tmid(SweepArgs& a, int axis) {
-  std::vector<double> t(kTabDoubles);
-  make_tables(a.co, sweep_S(axis, a.m), t.data());
-  memcpy(a.tmid, t.data(), sizeof(a.tmid));  // type 0 (interior), palette 0
+static void release_axis(AxisAux& aux, cudaStream_t st) {
+  if (aux.buf) cudaFreeAsync(aux.buf, st);
+  if (aux.desc) cudaFreeAsync(aux.desc, st);
+  aux.buf = nullptr;
+  aux.desc = nullptr;
 }
 
 static int launch_sweep(const SweepArgs& a, int axis, cudaStream_t st) {
@@ -1092,14 +1254,12 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
     ax[axis] = a;
   }
 
-  double* dtab = nullptr;
-  {
-    const int axes[3] = {0, 1, 2};
-    rc = upload_tables(ax, 3, axes, &dtab, st);
-    if (rc) return rc;
-    for (int axis = 0; axis < 3; ++axis) {
-      ax[axis].tab = dtab + axis * kTabDoubles;
-      fill_tmid(ax[axis], axis);
+  AxisAux aux[3];
+  for (int axis = 0; axis < 3; ++axis) {
+    rc = prepare_axis(ax[axis], axis, d->codes, aux[axis], st);
+    if (rc) {
+      for (int q = 0; q < 3; ++q) release_axis(aux[q], st);
+      return rc;
     }
   }
   int* dflag = nullptr;
@@ -1154,7 +1314,7 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
       }
       if (rc) {
         cudaFreeAsync(dflag, st);
-        cudaFreeAsync(dtab, st);
+        for (int q = 0; q < 3; ++q) release_axis(aux[q], st);
         return rc;
       }
     }
@@ -1164,7 +1324,7 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
   int dstep = INT_MAX;
   PBG_CUDA(cudaMemcpyAsync(&dstep, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
   PBG_CUDA(cudaFreeAsync(dflag, st));
-  PBG_CUDA(cudaFreeAsync(dtab, st));
+  for (int q = 0; q < 3; ++q) release_axis(aux[q], st);
   PBG_CUDA(cudaStreamSynchronize(st));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
@@ -1212,13 +1372,10 @@ extern "C" PBG_API int pbg_sweep(const pbg_grid* g, const pbg_palette* pal,
   a.cn = cn ? 1 : 0;
   a.cnc = cn ? factor / (g->h * g->h) : 0.0;
   cudaStream_t st = (cudaStream_t)stream;
-  double* dtab = nullptr;
-  const int axes[1] = {axis};
-  rc = upload_tables(&a, 1, axes, &dtab, st);
+  AxisAux aux;
+  rc = prepare_axis(a, axis, codes, aux, st);
   if (rc) return rc;
-  a.tab = dtab;
-  fill_tmid(a, axis);
   rc = launch_sweep(a, axis, st);
-  cudaFreeAsync(dtab, st);
+  release_axis(aux, st);
   return rc;
 }
