@@ -207,31 +207,6 @@ __device__ __forceinline__ double cn_term(const SweepArgs& a, uint32_t em, uint3
   return __dadd_rn(wc, __dmul_rn(a.cnc, d2));
 }
 
-// The rare rhs terms, applied after the stage values in the reference's order
-// (schemes.py:292-296, tridiag.py:216-217): branch source at charged nodes, the low and high
-// Dirichlet fold-ins, and zero rows past the line end.  rho_row(j) points at row i0+j's node.
-template <int S, typename RhoAt>
-__device__ __forceinline__ void rhs_rare(const SweepArgs& a, double (&r)[S],
-                                         unsigned long long amask, unsigned cmask, int i0,
-                                         RhoAt rho_row, double blo, double bhi) {
-  if (a.has_extra && cmask) {
-#pragma unroll
-    for (int j = 0; j < S; ++j)
-      if ((cmask >> j) & 1u) r[j] = __dadd_rn(r[j], __dmul_rn(a.extra, *rho_row(j)));
-  }
-  if (i0 == 0) r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], blo));
-  const int jlast = a.m - 1 - i0;
-  if (jlast < S) {
-#pragma unroll
-    for (int j = 0; j < S; ++j) {
-      if (j == jlast)
-        r[j] = __dadd_rn(r[j], __dmul_rn(((amask >> (j + 1)) & 1ull) ? a.co.fhi[1] : a.co.fhi[0],
-                                         bhi));
-      if (j > jlast) r[j] = 0.0;
-    }
-  }
-}
-
 // Per-thread segment state after the local elimination.
 struct SegOut {
   double yF, aF, bF, yL, aL, bL;  // first / last inner row: y, alpha, beta
@@ -399,13 +374,39 @@ __host__ __device__ constexpr size_t strided_smem(int S, bool needY) {
          sizeof(unsigned long long) * 2 * kSeg * LB;
 }
 
+// High Dirichlet fold of row m-1 (tridiag.py:217): owned by segment (m-1)/S at row (m-1)%S,
+// both launch-uniform, so the static-index select below runs in one thread per line.
+template <int S>
+__device__ __forceinline__ void fold_high(const SweepArgs& a, double (&r)[S],
+                                          unsigned long long amask, double bhi) {
+  const int jl = (a.m - 1) % S;
+#pragma unroll
+  for (int j = 0; j < S; ++j)
+    if (j == jl)
+      r[j] = __dadd_rn(r[j], __dmul_rn(((amask >> (j + 1)) & 1ull) ? a.co.fhi[1] : a.co.fhi[0],
+                                       bhi));
+}
+
+// Sparse per-owner fix-up at the charged nodes of a segment: *slot(j) += coef * rho(j).
+template <typename Slot, typename RhoAt>
+__device__ __forceinline__ void charged_fixup(unsigned cmask, double coef, Slot slot,
+                                              RhoAt rho_row) {
+  while (cmask) {
+    const int j = __ffs(cmask) - 1;
+    cmask &= cmask - 1;
+    double* v = slot(j);
+    *v = __dadd_rn(*v, __dmul_rn(coef, *rho_row(j)));
+  }
+}
+
 template <int S, bool CN, int LB>
 __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
     k_sweep_strided(const SweepArgs a, const int axis) {
   extern __shared__ double sm[];
-  if (a.div_step && *((volatile int*)a.div_step) < a.step) return;
   constexpr int NT = LB * kSeg, NR = strided_rows<S>();
   constexpr int CPR = LB / 2, RPP = NT / CPR;  // 16-byte chunks per row, rows per pass
+  // divergence flag: issue the load now, decide after staging
+  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
   const int lane = threadIdx.x, seg = threadIdx.y;
   const int tid = seg * LB + lane;
   const Layout& L = a.L;
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
   const double* grho = a.rho + base;
 
   // Phase 1: asynchronous staging of the field (+ epilogue operand), descriptors, tables.
-  {
+  if (a.dbg != 2) {
     const int q = (tid % CPR) * 2, p0 = tid / CPR;
     const long long gstep = (long long)RPP * stride;
     const double* g = gsrc + p0 * (long long)stride + q;
@@ -453,33 +454,39 @@ __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
   for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
   if (a.static_ok)
     for (int c = tid; c < kSeg * kSeg / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
+  for (int c = nl * LB + tid; c < NR * LB; c += NT) W[c] = 0.0;  // rows past the far face
   cp_async_wait_all();
   __syncthreads();
-  if (a.pro == PRO_FLOW && tid < 2 * LB) {  // flow stages see the Dirichlet faces
-    const int p = tid < LB ? 0 : nl - 1, l = tid % LB;
-    W[p * LB + l] = a.bnd[base + (long long)p * stride + l];
-  }
-  if (a.pro != PRO_NONE) {  // prologue in place on the interior rows
+  if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
+
+  const int i0 = seg * S;
+  const unsigned long long amask = D[2 * tid];
+  const unsigned cmask = (unsigned)(D[2 * tid + 1] >> 32);
+  const double* rrow = grho + (i0 + 1) * stride + lane;
+  auto rho_row = [&](int j) { return rrow + j * stride; };
+  double* w0 = W + (i0 + 1) * LB + lane;
+  if (a.pro == PRO_FLOW) {  // flow stage: interior rows transformed, faces = Dirichlet data
+    if (tid < 2 * LB) {
+      const int p = tid < LB ? 0 : nl - 1, l = tid % LB;
+      W[p * LB + l] = a.bnd[base + (long long)p * stride + l];
+    }
     const int l = tid % LB;
     for (int p = 1 + tid / LB; p < nl - 1; p += NT / LB) {
       const int sg = (p - 1) / S;
       const uint32_t c = node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
-      W[p * LB + l] = pro_val(a, W[p * LB + l], c, grho + (long long)p * stride + l);
+      W[p * LB + l] = flow_at(a, W[p * LB + l], c, a.pm);
     }
+    __syncthreads();
+  } else if (a.pro == PRO_SRC) {  // w = u + dta*rho at the charged nodes only
+    if (cmask) charged_fixup(cmask, a.pro_coef, [&](int j) { return w0 + j * LB; }, rho_row);
+    __syncthreads();
   }
-  __syncthreads();
 
   if (a.dbg == 1) goto store;
   {
     // Phase 2: rhs of the own rows (registers), local elimination.
     const bool active = lane < ncols;
-    const int i0 = seg * S;
-    const unsigned long long amask = D[2 * tid];
-    const unsigned cmask = (unsigned)(D[2 * tid + 1] >> 32);
     double r[S];
-    double blo = 0.0, bhi = 0.0;
-    if (active && i0 == 0) blo = a.bnd[base + lane];
-    if (active && i0 <= m - 1 && m - 1 < i0 + S) bhi = a.bnd[base + (long long)(m + 1) * stride + lane];
     {
       const double* wrow = W + (i0 + 1) * LB + lane;
 #pragma unroll
@@ -489,15 +496,21 @@ __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
                             wrow[(j - 1) * LB], wc, wrow[(j + 1) * LB])
                   : wc;
       }
-      const double* rrow = grho + (i0 + 1) * stride + lane;
-      rhs_rare<S>(a, r, amask, cmask, i0, [&](int j) { return rrow + j * stride; }, blo, bhi);
     }
+    if (a.has_extra && cmask) {
+#pragma unroll
+      for (int j = 0; j < S; ++j)
+        if ((cmask >> j) & 1u) r[j] = __dadd_rn(r[j], __dmul_rn(a.extra, *rho_row(j)));
+    }
+    if (seg == 0 && active)
+      r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], a.bnd[base + lane]));
+    if (seg == (m - 1) / S && active)
+      fold_high<S>(a, r, amask, a.bnd[base + (long long)(m + 1) * stride + lane]);
     // clean tile: every line of the tile is one dielectric (palette 0) end to end
     const bool clean = __syncthreads_and(!active || amask == 0ull) && a.static_ok;
 
     double al[S], be[S];
     SegOut o;
-    double* w0 = W + (i0 + 1) * LB + lane;
     const int ttype = seg_eliminate<S, LB>(a, r, amask, i0, seg == 0, T, w0, al, be, o);
 
     // Phase 3: reduced system over the 32 separators of each line.
@@ -571,43 +584,63 @@ __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
       tm = (seg > 0) ? sA[tid - LB] : 0.0;
     }
 
-    // Phase 4: reconstruct the inner rows, separator = t.
+    // Phase 4: reconstruct the inner rows, separator = t; sparse source epilogue (LODIE1).
     seg_finish<S, LB>(a, ttype, r, amask, tm, t, T, w0, al, be);
     if (i0 + S - 1 < m) W[(i0 + S) * LB + lane] = t;
+    if (a.epi == EPI_SRC && cmask)
+      charged_fixup(cmask, a.epi_coef, [&](int j) { return w0 + j * LB; }, rho_row);
     __syncthreads();
   }
 store:
   // Phase 5: epilogue + coalesced store of the interior rows.
-  bool bad = false;
-  double* gdst = a.dst + base;
-  if (a.epi == EPI_STORE && !a.check) {
-    const int q = (tid % CPR) * 2, p0 = 1 + tid / CPR;  // 16-byte chunks
-    const long long gstep = (long long)RPP * stride;
-    double* g = gdst + p0 * (long long)stride + q;
-    const double* w = W + p0 * LB + q;
-    if (q + 1 < ncols) {
+  {
+    bool bad = false;
+    double* gdst = a.dst + base;
+    const int epi = a.epi;
+    if ((epi == EPI_STORE || epi == EPI_SRC || epi == EPI_MAOS0) && !a.check) {
+      const int q = (tid % CPR) * 2, p0 = 1 + tid / CPR;  // 16-byte chunks
+      const long long gstep = (long long)RPP * stride;
+      double* g = gdst + p0 * (long long)stride + q;
+      const double* w = W + p0 * LB + q;
+      if (a.dbg == 2) {
+        if (W[tid] == 12345.678) gdst[0] = 0.0;  // keep the solve alive
+      } else if (q + 1 < ncols) {
 #pragma unroll 4
-      for (int p = p0; p <= m; p += RPP, g += gstep, w += RPP * LB)
-        *reinterpret_cast<double2*>(g) = *reinterpret_cast<const double2*>(w);
-    } else if (q < ncols) {
-      for (int p = p0; p <= m; p += RPP, g += gstep, w += RPP * LB) *g = *w;
-    }
-  } else {
-    const int l = tid % LB;
-    if (l < ncols) {
-      for (int p = 1 + tid / LB; p <= m; p += NT / LB) {
-        const int c = p * LB + l;
+        for (int p = p0; p <= m; p += RPP, g += gstep, w += RPP * LB)
+          *reinterpret_cast<double2*>(g) = *reinterpret_cast<const double2*>(w);
+      } else if (q < ncols) {
+        for (int p = p0; p <= m; p += RPP, g += gstep, w += RPP * LB) *g = *w;
+      }
+    } else {
+      const int l = tid % LB;
+      auto loop = [&](auto f) {
+        if (l >= ncols) return;
+        for (int p = 1 + tid / LB; p <= m; p += NT / LB) {
+          const int c = p * LB + l;
+          const double x = f(c, p);
+          gdst[(long long)p * stride + l] = x;
+          bad |= is_bad(x, a.thr);
+        }
+      };
+      auto solute = [&](int p) {
         const int sg = (p - 1) / S;
-        const uint32_t bits = node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
-        const long long off = (long long)p * stride + l;
-        const double x = epi_val(a, W[c], needY ? Yt[c] : 0.0, bits, grho + off);
-        gdst[off] = x;
-        bad |= is_bad(x, a.thr);
+        return node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
+      };
+      switch (epi) {
+        case EPI_FLOW: loop([&](int c, int p) { return flow_at(a, W[c], solute(p), 1.0); }); break;
+        case EPI_AOS0:
+          loop([&](int c, int p) { return __dadd_rn(flow_at(a, Yt[c], solute(p), a.pm), W[c]); });
+          break;
+        case EPI_AOS1:
+        case EPI_MAOS1: loop([&](int c, int) { return __dadd_rn(Yt[c], W[c]); }); break;
+        case EPI_AOS2: loop([&](int c, int) { return __dmul_rn(0.25, __dadd_rn(Yt[c], W[c])); }); break;
+        case EPI_MAOS2: loop([&](int c, int) { return __ddiv_rn(__dadd_rn(Yt[c], W[c]), 3.0); }); break;
+        default: loop([&](int c, int) { return W[c]; }); break;
       }
     }
-  }
-  if (a.check) {
-    if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicMin(a.div_step, a.step);
+    if (a.check) {
+      if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicMin(a.div_step, a.step);
+    }
   }
 }
 
@@ -630,9 +663,9 @@ constexpr int kContigWarps = 8;
 template <int S, bool CN>
 __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const int nlines) {
   extern __shared__ double sm[];
-  if (a.div_step && *((volatile int*)a.div_step) < a.step) return;
   constexpr int BUF = contig_buf_doubles<S>();
   constexpr int W = kContigWarps;
+  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int needY = epi_needs(a.epi);
   const int YB = needY ? 32 * S + 2 : 0;
@@ -663,34 +696,39 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
 #pragma unroll 4
       for (int e = lane; e < n2; e += 32) cp_async8(ybuf + e, gy + e);
     }
+    for (int e = n2 + lane; e <= 32 * S + 1; e += 32) buf[cpos<S>(e)] = 0.0;  // past the face
     const unsigned long long* dp = a.desc + 2 * ((long long)line * kSeg + lane);
     dw0 = dp[0];
     dw1 = dp[1];
   }
   cp_async_wait_all();
   __syncthreads();  // tables are shared by the block
-  if (!live) return;
-  if (a.pro == PRO_FLOW && lane < 2) {  // flow stages see the Dirichlet faces
-    const int e = lane ? n2 - 1 : 0;
-    buf[cpos<S>(e)] = a.bnd[rb + e];
-  }
-  if (a.pro != PRO_NONE) {
-    for (int e0 = 1; e0 < n2 - 1; e0 += 32) {  // warp-uniform trip count (shuffles inside)
-      const int e = e0 + lane;
-      const int sg = min((e - 1) / S, kSeg - 1);
-      const uint32_t c = node_bits(__shfl_sync(0xffffffffu, dw1, sg), (e - 1) - sg * S);
-      if (e < n2 - 1) buf[cpos<S>(e)] = pro_val(a, buf[cpos<S>(e)], c, grho + e);
-    }
-    __syncwarp();
-  }
+  if (!live || dstep < a.step) return;
 
   const int i0 = lane * S;
   const unsigned long long amask = dw0;
   const unsigned cmask = (unsigned)(dw1 >> 32);
+  double* w0 = buf + cpos<S>(i0 + 1);
+  auto rho_row = [&](int j) { return grho + i0 + j + 1; };
+  if (a.pro == PRO_FLOW) {
+    if (lane < 2) {  // flow stages see the Dirichlet faces
+      const int e = lane ? n2 - 1 : 0;
+      buf[cpos<S>(e)] = a.bnd[rb + e];
+    }
+    for (int e0 = 1; e0 < n2 - 1; e0 += 32) {  // warp-uniform trip count (shuffles inside)
+      const int e = e0 + lane;
+      const int sg = min((e - 1) / S, kSeg - 1);
+      const uint32_t c = node_bits(__shfl_sync(0xffffffffu, dw1, sg), (e - 1) - sg * S);
+      if (e < n2 - 1) buf[cpos<S>(e)] = flow_at(a, buf[cpos<S>(e)], c, a.pm);
+    }
+    __syncwarp();
+  } else if (a.pro == PRO_SRC) {
+    if (cmask)
+      charged_fixup(cmask, a.pro_coef, [&](int j) { return buf + cpos<S>(i0 + 1 + j); }, rho_row);
+    __syncwarp();
+  }
+
   double r[S];
-  double blo = 0.0, bhi = 0.0;
-  if (i0 == 0) blo = a.bnd[rb];
-  if (i0 <= m - 1 && m - 1 < i0 + S) bhi = a.bnd[rb + m + 1];
 #pragma unroll
   for (int j = 0; j < S; ++j) {
     const int p = i0 + j + 1;
@@ -699,13 +737,18 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
                         buf[cpos<S>(p - 1)], wc, buf[cpos<S>(p + 1)])
               : wc;
   }
-  rhs_rare<S>(a, r, amask, cmask, i0, [&](int j) { return grho + i0 + j + 1; }, blo, bhi);
+  if (a.has_extra && cmask) {
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if ((cmask >> j) & 1u) r[j] = __dadd_rn(r[j], __dmul_rn(a.extra, *rho_row(j)));
+  }
+  if (lane == 0) r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], a.bnd[rb]));
+  if (lane == (m - 1) / S) fold_high<S>(a, r, amask, a.bnd[rb + m + 1]);
   const bool clean = __all_sync(0xffffffffu, amask == 0ull) && a.static_ok;
   __syncwarp();
 
   double al[S], be[S];
   SegOut o;
-  double* w0 = buf + cpos<S>(i0 + 1);
   const int ttype = seg_eliminate<S, 1>(a, r, amask, i0, lane == 0, T, w0, al, be, o);
 
   const double yFn0 = __shfl_down_sync(0xffffffffu, o.yF, 1);
@@ -767,22 +810,42 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
 
   seg_finish<S, 1>(a, ttype, r, amask, tm, t, T, w0, al, be);
   if (i0 + S - 1 < m) buf[cpos<S>(i0 + S)] = t;
+  if (a.epi == EPI_SRC && cmask)
+    charged_fixup(cmask, a.epi_coef, [&](int j) { return buf + cpos<S>(i0 + 1 + j); }, rho_row);
   __syncwarp();
 
   bool bad = false;
   double* gdst = a.dst + rb;
-  if (a.epi == EPI_STORE && !a.check) {
+  const int epi = a.epi;
+  if ((epi == EPI_STORE || epi == EPI_SRC || epi == EPI_MAOS0) && !a.check) {
     for (int p = lane + 1; p <= m; p += 32) gdst[p] = buf[cpos<S>(p)];
   } else {
-    for (int p0 = 1; p0 <= m; p0 += 32) {  // warp-uniform trip count (shuffles inside)
-      const int p = p0 + lane;
-      const int sg = min((p - 1) / S, kSeg - 1);
-      const uint32_t bits = node_bits(__shfl_sync(0xffffffffu, dw1, sg), (p - 1) - sg * S);
-      if (p <= m) {
-        const double x = epi_val(a, buf[cpos<S>(p)], needY ? ybuf[p] : 0.0, bits, grho + p);
-        gdst[p] = x;
-        bad |= is_bad(x, a.thr);
+    auto loop = [&](auto f) {
+      for (int p0 = 1; p0 <= m; p0 += 32) {  // warp-uniform trip count (shuffles inside)
+        const int p = p0 + lane;
+        const int sg = min((p - 1) / S, kSeg - 1);
+        const uint32_t bits = node_bits(__shfl_sync(0xffffffffu, dw1, sg), (p - 1) - sg * S);
+        if (p <= m) {
+          const double x = f(p, bits);
+          gdst[p] = x;
+          bad |= is_bad(x, a.thr);
+        }
       }
+    };
+    switch (epi) {
+      case EPI_FLOW: loop([&](int p, uint32_t c) { return flow_at(a, buf[cpos<S>(p)], c, 1.0); }); break;
+      case EPI_AOS0:
+        loop([&](int p, uint32_t c) { return __dadd_rn(flow_at(a, ybuf[p], c, a.pm), buf[cpos<S>(p)]); });
+        break;
+      case EPI_AOS1:
+      case EPI_MAOS1: loop([&](int p, uint32_t) { return __dadd_rn(ybuf[p], buf[cpos<S>(p)]); }); break;
+      case EPI_AOS2:
+        loop([&](int p, uint32_t) { return __dmul_rn(0.25, __dadd_rn(ybuf[p], buf[cpos<S>(p)])); });
+        break;
+      case EPI_MAOS2:
+        loop([&](int p, uint32_t) { return __ddiv_rn(__dadd_rn(ybuf[p], buf[cpos<S>(p)]), 3.0); });
+        break;
+      default: loop([&](int p, uint32_t) { return buf[cpos<S>(p)]; }); break;
     }
   }
   if (a.check) {
