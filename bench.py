@@ -167,11 +167,11 @@ def e2e_measure(p, c, dp, nsteps):
     rho = p.rho._dev
     n0, n1, n2 = g.shape
     pitch = dp.gs.pitch
-    rd = rho.view(n0, n1, pitch)[:, :, nat.PBG_OFFSET:nat.PBG_OFFSET + n2]
+    rd = rho[:n0 * n1 * pitch].view(n0, n1, pitch)[:, :, nat.PBG_OFFSET:nat.PBG_OFFSET + n2]
     flat = torch.nonzero(rd.reshape(-1)).reshape(-1)
     idx_h = flat.cpu().numpy().astype(np.int64)
     val_h = rd.reshape(-1)[flat].cpu().numpy()
-    bnd = dp.bnd.view(n0, n1, pitch)[:, :, nat.PBG_OFFSET:nat.PBG_OFFSET + n2]
+    bnd = dp.bnd[:n0 * n1 * pitch].view(n0, n1, pitch)[:, :, nat.PBG_OFFSET:nat.PBG_OFFSET + n2]
     fc = torch.cat([bnd[0].reshape(-1), bnd[-1].reshape(-1), bnd[:, 0].reshape(-1),
                     bnd[:, -1].reshape(-1), bnd[:, :, 0].reshape(-1), bnd[:, :, -1].reshape(-1)])
     faces_h = torch.empty(fc.numel(), dtype=torch.float64, pin_memory=True)
@@ -215,9 +215,10 @@ def oracle_slab(p, dp, nplanes):
     n0, n1, n2 = g.shape
     pitch = dp.gs.pitch
     sl = slice(nat.PBG_OFFSET, nat.PBG_OFFSET + n2)
-    codes = dp.codes.view(n0, n1, pitch)[:nplanes, :, sl].cpu().numpy()
-    rho = dp.rho.view(n0, n1, pitch)[:nplanes, :, sl].cpu().numpy().copy()
-    bv = dp.bnd.view(n0, n1, pitch)[:nplanes, :, sl].cpu().numpy().copy()
+    nn = n0 * n1 * pitch
+    codes = dp.codes[:nn].view(n0, n1, pitch)[:nplanes, :, sl].cpu().numpy()
+    rho = dp.rho[:nn].view(n0, n1, pitch)[:nplanes, :, sl].cpu().numpy().copy()
+    bv = dp.bnd[:nn].view(n0, n1, pitch)[:nplanes, :, sl].cpu().numpy().copy()
     rho[-1] = 0.0
     eps = dp.pal.as_tuple()[0]
     k2p = dp.pal.as_tuple()[1]
