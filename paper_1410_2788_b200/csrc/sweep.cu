@@ -60,7 +60,7 @@ enum {
   EPI_MAOS2 = 8
 };
 
-constexpr int kSeg = 32;   // segments per line
+constexpr int kSeg = 32;   // segments per line, contiguous axis (one warp lane each)
 
 struct AxisCoef {
   double diag[4];  // [em*2 + ep]  1 + f*(e_plus + e_minus)
@@ -362,16 +362,16 @@ __device__ __forceinline__ void reduced_row(const SegOut& o, double yFn, double 
 // Strided axes (0, 1).  blockDim = (LB columns, 32 segments); block (x = k group, y = outer).
 // Shared memory: tables | reduced inverse | W[NR][LB] stage/solution | Y[NR][LB] (AOS/MAOS)
 // | 4x(LB*32) scratch | descriptors D[32][LB][2].
-template <int S>
+template <int S, int P>
 __host__ __device__ constexpr int strided_rows() {
-  return kSeg * S + 2;
+  return P * S + 2;
 }
 
 template <int LB>
-__host__ __device__ constexpr size_t strided_smem(int S, bool needY) {
-  return sizeof(double) * (kTabDoubles + kSeg * kSeg + (needY ? 2 : 1) * (size_t)(kSeg * S + 2) * LB +
-                           4 * LB * kSeg) +
-         sizeof(unsigned long long) * 2 * kSeg * LB;
+__host__ __device__ constexpr size_t strided_smem(int S, int kSegS, bool needY) {
+  return sizeof(double) * (kTabDoubles + kSegS * kSegS + (needY ? 2 : 1) * (size_t)(kSegS * S + 2) * LB +
+                           4 * LB * kSegS) +
+         sizeof(unsigned long long) * 2 * kSegS * LB;
 }
 
 // High Dirichlet fold of row m-1 (tridiag.py:217): owned by segment (m-1)/S at row (m-1)%S,
@@ -399,11 +399,11 @@ __device__ __forceinline__ void charged_fixup(unsigned cmask, double coef, Slot 
   }
 }
 
-template <int S, bool CN, int LB>
-__global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
+template <int S, int kSegS, bool CN, int LB>
+__global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 4 : (LB * kSegS <= 256 ? 3 : 2))
     k_sweep_strided(const SweepArgs a, const int axis) {
   extern __shared__ double sm[];
-  constexpr int NT = LB * kSeg, NR = strided_rows<S>();
+  constexpr int NT = LB * kSegS, NR = strided_rows<S, kSegS>();
   constexpr int CPR = LB / 2, RPP = NT / CPR;  // 16-byte chunks per row, rows per pass
   // divergence flag: issue the load now, decide after staging
   const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
   const int needY = epi_needs(a.epi);
   double* T = sm;
   double* Mi = T + kTabDoubles;
-  double* W = Mi + kSeg * kSeg;
+  double* W = Mi + kSegS * kSegS;
   double* Yt = W + NR * LB;
   double* X = Yt + (needY ? NR * LB : 0);
   unsigned long long* D = reinterpret_cast<unsigned long long*>(X + 4 * NT);
@@ -450,10 +450,10 @@ __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
       for (int p = p0; p < nl; p += RPP, gyp += gstep, yp += RPP * LB) cp_async16(yp, gyp);
     }
   }
-  cp_async16(D + 2 * tid, a.desc + 2 * (((long long)(outer - 1) * kSeg + seg) * K + (k0 - 1 + lane)));
+  cp_async16(D + 2 * tid, a.desc + 2 * (((long long)(outer - 1) * kSegS + seg) * K + (k0 - 1 + lane)));
   for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
   if (a.static_ok)
-    for (int c = tid; c < kSeg * kSeg / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
+    for (int c = tid; c < kSegS * kSegS / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
   for (int c = nl * LB + tid; c < NR * LB; c += NT) W[c] = 0.0;  // rows past the far face
   cp_async_wait_all();
   __syncthreads();
@@ -522,16 +522,16 @@ __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
     if (clean) {  // static inverse: one exchange of y_F, one of R, then two dot products
       sA[tid] = o.yF;
       __syncthreads();
-      const double yFn = (seg + 1 < kSeg) ? sA[tid + LB] : 0.0;
+      const double yFn = (seg + 1 < kSegS) ? sA[tid + LB] : 0.0;
       sR[tid] = o.rs - o.as * o.yL - o.cs * yFn;
       __syncthreads();
       const int k1 = seg > 0 ? seg - 1 : 0;  // transposed inverse: column q at Mi[q*32]
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll 8
-      for (int q = 0; q < kSeg; ++q) {
+      for (int q = 0; q < kSegS; ++q) {
         const double Rq = sR[q * LB + lane];
-        s0 = fma(Mi[q * kSeg + seg], Rq, s0);
-        s1 = fma(Mi[q * kSeg + k1], Rq, s1);
+        s0 = fma(Mi[q * kSegS + seg], Rq, s0);
+        s1 = fma(Mi[q * kSegS + k1], Rq, s1);
       }
       t = s0;
       tm = seg > 0 ? s1 : 0.0;
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
       sC[tid] = o.bF;
       __syncthreads();
       double yFn = 0.0, aFn = 0.0, bFn = 0.0;
-      if (seg + 1 < kSeg) {
+      if (seg + 1 < kSegS) {
         yFn = sA[tid + LB];
         aFn = sB[tid + LB];
         bFn = sC[tid + LB];
@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
       double A, B, Cc, R;
       reduced_row(o, yFn, aFn, bFn, A, B, Cc, R);
 #pragma unroll
-      for (int d = 1; d < kSeg; d <<= 1) {
+      for (int d = 1; d < kSegS; d <<= 1) {
         sA[tid] = A;
         sB[tid] = fast_rcp(B);
         sC[tid] = Cc;
@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(LB * kSeg, LB == 8 ? 3 : 2)
           Cm = sC[q];
           Rm = sR[q];
         }
-        if (seg + d < kSeg) {
+        if (seg + d < kSegS) {
           const int q = tid + d * LB;
           Ap = sA[q];
           iBp = sB[q];
@@ -858,12 +858,13 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
 //   word 0: bit j = eps bit (axis) of the node of row i0+j, j = 0..S (zero past node m+1)
 //   word 1: bits 0..S-1 solute bit of the nodes of rows i0..i0+S-1; bits 32.. charged bits
 // Layout: strided axes ((outer-1)*32 + seg)*K + (k-1); contiguous axis line*32 + seg.
-__global__ void k_build_desc(const Layout L, int axis, int S, const uint8_t* __restrict__ codes,
+__global__ void k_build_desc(const Layout L, int axis, int S, int P,
+                             const uint8_t* __restrict__ codes,
                              unsigned long long* __restrict__ desc) {
   const int m = (axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2)) - 2;
   long long nseg;
   if (axis == 2) nseg = (long long)(L.n0 - 2) * (L.n1 - 2) * kSeg;
-  else nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * kSeg * (L.n2 - 2);
+  else nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * (L.n2 - 2);
   const int sh = 1 + axis;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nseg;
        t += (long long)gridDim.x * blockDim.x) {
@@ -878,8 +879,8 @@ __global__ void k_build_desc(const Layout L, int axis, int S, const uint8_t* __r
       const int K = L.n2 - 2;
       const int k = 1 + (int)(t % K);
       const long long os = t / K;
-      seg = (int)(os % kSeg);
-      const int outer = 1 + (int)(os / kSeg);
+      seg = (int)(os % P);
+      const int outer = 1 + (int)(os / P);
       base = axis == 0 ? L.at(0, outer, k) : L.at(outer, 0, k);
       stride = axis == 0 ? L.s0 : L.pitch;
     }
@@ -903,37 +904,43 @@ __global__ void k_build_desc(const Layout L, int axis, int S, const uint8_t* __r
 // ---------------------------------------------------------------------------------------
 // Host-side launch helpers.
 
-static int seg_S(int m) {
-  const int opts[] = {2, 3, 4, 6, 8, 12, 16, 24};
+static int seg_S(int m, int P) {
+  const int opts[] = {2, 3, 4, 6, 8, 12, 16, 24, 32};
   for (int s : opts)
-    if (kSeg * s >= m) return s;
+    if (P * s >= m) return s;
   return 0;
 }
+// Strided axes: segments of ~16 rows (registers and occupancy balance, measured); the
+// contiguous axis always uses the 32 lanes of a warp.
+static int seg_P(int axis, int m) {
+  if (axis == 2) return kSeg;
+  return m <= 128 ? 8 : (m <= 256 ? 16 : 32);
+}
 
-template <int S, bool CN, int LB>
+template <int S, int P, bool CN, int LB>
 static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
   const int nouter = (axis == 0 ? a.L.n1 : a.L.n0) - 2;
   dim3 grid((a.L.n2 - 2 + LB - 1) / LB, nouter);
-  dim3 block(LB, kSeg);
-  const size_t smem = strided_smem<LB>(S, epi_needs(a.epi) != 0);
+  dim3 block(LB, P);
+  const size_t smem = strided_smem<LB>(S, P, epi_needs(a.epi) != 0);
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_sweep_strided<S, CN, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-  k_sweep_strided<S, CN, LB><<<grid, block, smem, st>>>(a, axis);
+    cudaFuncSetAttribute(k_sweep_strided<S, P, CN, LB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_sweep_strided<S, P, CN, LB><<<grid, block, smem, st>>>(a, axis);
 }
 
 // Axis 0 rows are one field plane apart (MB strides): 128-byte row chunks keep DRAM pages
 // and TLB entries busy (64-byte chunks run at ~55% of copy bandwidth there, measured).
-template <int S, bool CN>
+template <int S, int P, bool CN>
 static void launch_strided_SC(const SweepArgs& a, int axis, cudaStream_t st) {
-  if (axis == 0) launch_strided_SCL<S, CN, 16>(a, axis, st);
-  else launch_strided_SCL<S, CN, 8>(a, axis, st);
+  if (axis == 0) launch_strided_SCL<S, P, CN, 16>(a, axis, st);
+  else launch_strided_SCL<S, P, CN, 8>(a, axis, st);
 }
 
-template <int S>
-static void launch_strided_S(const SweepArgs& a, int axis, cudaStream_t st) {
-  if (a.cn) launch_strided_SC<S, true>(a, axis, st);
-  else launch_strided_SC<S, false>(a, axis, st);
+template <int S, int P>
+static void launch_strided_SP(const SweepArgs& a, int axis, cudaStream_t st) {
+  if (a.cn) launch_strided_SC<S, P, true>(a, axis, st);
+  else launch_strided_SC<S, P, false>(a, axis, st);
 }
 
 template <int S, bool CN>
@@ -965,20 +972,32 @@ static void launch_contig_S(const SweepArgs& a, cudaStream_t st) {
     case 12: CALL(12); break;                                                           \
     case 16: CALL(16); break;                                                           \
     case 24: CALL(24); break;                                                           \
+    case 32: CALL(32); break;                                                           \
     default: return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 768)"); \
   }
 
 static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
-#define PBG_STRIDED(S) launch_strided_S<S>(a, axis, st)
-  PBG_DISPATCH_S(seg_S(a.m), PBG_STRIDED)
-#undef PBG_STRIDED
+  const int P = seg_P(axis, a.m), S = seg_S(a.m, P);
+  if (P == 8) {
+#define PBG_STRIDED8(S) launch_strided_SP<S, 8>(a, axis, st)
+    PBG_DISPATCH_S(S, PBG_STRIDED8)
+#undef PBG_STRIDED8
+  } else if (P == 16 && S == 16) {
+    launch_strided_SP<16, 16>(a, axis, st);
+  } else if (P == 32 && S == 16) {
+    launch_strided_SP<16, 32>(a, axis, st);
+  } else if (P == 32 && S == 32) {
+    launch_strided_SP<32, 32>(a, axis, st);
+  } else {
+    return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 1024)");
+  }
   PBG_LAUNCH_CHECK("k_sweep_strided");
   return PBG_OK;
 }
 
 static int launch_contig(const SweepArgs& a, cudaStream_t st) {
 #define PBG_CONTIG(S) launch_contig_S<S>(a, st)
-  PBG_DISPATCH_S(seg_S(a.m), PBG_CONTIG)
+  PBG_DISPATCH_S(seg_S(a.m, kSeg), PBG_CONTIG)
 #undef PBG_CONTIG
   PBG_LAUNCH_CHECK("k_sweep_contig");
   return PBG_OK;
@@ -1038,13 +1057,13 @@ static void make_tables(const AxisCoef& co, int S, double* out) {
 // Dense inverse of the reduced (separator) system of a clean line: every node carries eps
 // palette 0, segment k uses table type first / interior / last.  Valid when 32*S is m or
 // m + 1 (the last separator is row m-1 or the padding row m).
-static bool make_reduced_inverse(const AxisCoef& co, const double* tab, int S, int m,
+static bool make_reduced_inverse(const AxisCoef& co, const double* tab, int S, int m, int P,
                                  double* minv) {
-  if (!(kSeg * S == m || kSeg * S == m + 1)) return false;
+  if (!(P * S == m || P * S == m + 1)) return false;
   auto T = [&](int type, int q, int j) { return tab[(type * 2) * 5 * kTabRows + q * kTabRows + j]; };
-  auto type_of = [&](int k) { return k == 0 ? 1 : ((k == kSeg - 1 && kSeg * S == m + 1) ? 2 : 0); };
+  auto type_of = [&](int k) { return k == 0 ? 1 : ((k == P - 1 && P * S == m + 1) ? 2 : 0); };
   double A[kSeg], B[kSeg], C[kSeg];
-  for (int k = 0; k < kSeg; ++k) {
+  for (int k = 0; k < P; ++k) {
     const int ty = type_of(k), i = k * S + S - 1;
     if (i >= m) {
       A[k] = 0.0;
@@ -1054,7 +1073,7 @@ static bool make_reduced_inverse(const AxisCoef& co, const double* tab, int S, i
     }
     const double as = co.sub[0], bs = co.diag[0], cs = (i == m - 1) ? 0.0 : co.sup[0];
     double aFn = 0.0, bFn = 0.0;
-    if (k + 1 < kSeg) {
+    if (k + 1 < P) {
       aFn = T(type_of(k + 1), TQ_AL, 0);
       bFn = T(type_of(k + 1), TQ_BE, 0);
     }
@@ -1062,26 +1081,26 @@ static bool make_reduced_inverse(const AxisCoef& co, const double* tab, int S, i
     B[k] = bs + as * T(ty, TQ_BE, S - 2) + cs * aFn;
     C[k] = cs * bFn;
   }
-  double M[kSeg][2 * kSeg];
-  for (int r = 0; r < kSeg; ++r)
-    for (int c = 0; c < 2 * kSeg; ++c) M[r][c] = 0.0;
-  for (int r = 0; r < kSeg; ++r) {
+  static thread_local double M[kSeg][2 * kSeg];
+  for (int r = 0; r < P; ++r)
+    for (int c = 0; c < 2 * P; ++c) M[r][c] = 0.0;
+  for (int r = 0; r < P; ++r) {
     if (r > 0) M[r][r - 1] = A[r];
     M[r][r] = B[r];
-    if (r + 1 < kSeg) M[r][r + 1] = C[r];
-    M[r][kSeg + r] = 1.0;
+    if (r + 1 < P) M[r][r + 1] = C[r];
+    M[r][P + r] = 1.0;
   }
-  for (int c = 0; c < kSeg; ++c) {  // Gauss-Jordan, diagonally dominant: no pivoting
+  for (int c = 0; c < P; ++c) {  // Gauss-Jordan, diagonally dominant: no pivoting
     const double piv = M[c][c];
-    for (int q = 0; q < 2 * kSeg; ++q) M[c][q] /= piv;
-    for (int r = 0; r < kSeg; ++r) {
+    for (int q = 0; q < 2 * P; ++q) M[c][q] /= piv;
+    for (int r = 0; r < P; ++r) {
       if (r == c || M[r][c] == 0.0) continue;
       const double f = M[r][c];
-      for (int q = 0; q < 2 * kSeg; ++q) M[r][q] -= f * M[c][q];
+      for (int q = 0; q < 2 * P; ++q) M[r][q] -= f * M[c][q];
     }
   }
-  for (int r = 0; r < kSeg; ++r)  // stored transposed: minv[q*32 + k] = inverse[k][q]
-    for (int c = 0; c < kSeg; ++c) minv[c * kSeg + r] = M[r][kSeg + c];
+  for (int r = 0; r < P; ++r)  // stored transposed: minv[q*32 + k] = inverse[k][q]
+    for (int c = 0; c < P; ++c) minv[c * P + r] = M[r][P + c];
   return true;
 }
 
@@ -1112,26 +1131,28 @@ struct AxisAux {
   unsigned long long* desc = nullptr;
 };
 
-static long long desc_segments(const Layout& L, int axis) {
+static long long desc_segments(const Layout& L, int axis, int P) {
   if (axis == 2) return (long long)(L.n0 - 2) * (L.n1 - 2) * kSeg;
-  return (long long)((axis == 0 ? L.n1 : L.n0) - 2) * kSeg * (L.n2 - 2);
+  return (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * (L.n2 - 2);
 }
 
 static int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
                         cudaStream_t st) {
-  const int S = seg_S(a.m);
+  const int P = seg_P(axis, a.m);
+  const int S = seg_S(a.m, P);
   if (S < 2) return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 768)");
   std::vector<double> host(kTabDoubles + kSeg * kSeg, 0.0);
   make_tables(a.co, S, host.data());
   memcpy(a.tmid, host.data(), sizeof(a.tmid));  // type 0 (interior), palette 0
-  a.static_ok = make_reduced_inverse(a.co, host.data(), S, a.m, host.data() + kTabDoubles) ? 1 : 0;
+  a.static_ok =
+      make_reduced_inverse(a.co, host.data(), S, a.m, P, host.data() + kTabDoubles) ? 1 : 0;
   PBG_CUDA(cudaMallocAsync(&aux.buf, host.size() * sizeof(double), st));
   PBG_CUDA(cudaMemcpyAsync(aux.buf, host.data(), host.size() * sizeof(double),
                            cudaMemcpyHostToDevice, st));
-  const long long nseg = desc_segments(a.L, axis);
+  const long long nseg = desc_segments(a.L, axis, P);
   // +64 words of slack: tiles past the last interior column read (unused) descriptors
   PBG_CUDA(cudaMallocAsync(&aux.desc, (2 * nseg + 64) * sizeof(unsigned long long), st));
-  k_build_desc<<<148 * 8, 256, 0, st>>>(a.L, axis, S, codes, aux.desc);
+  k_build_desc<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, codes, aux.desc);
   PBG_LAUNCH_CHECK("k_build_desc");
   PBG_CUDA(cudaStreamSynchronize(st));  // host staging vector dies here
   a.tab = aux.buf;
