@@ -660,51 +660,36 @@ __host__ __device__ constexpr int contig_buf_doubles() {
 
 constexpr int kContigWarps = 8;
 
-template <int S, bool CN>
-__global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const int nlines) {
-  extern __shared__ double sm[];
-  constexpr int BUF = contig_buf_doubles<S>();
-  constexpr int W = kContigWarps;
-  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int needY = epi_needs(a.epi);
-  const int YB = needY ? 32 * S + 2 : 0;
-  double* T = sm;
-  double* Mi = T + kTabDoubles;
-  double* buf = Mi + kSeg * kSeg + warp * (BUF + YB + kSeg);
-  double* ybuf = buf + BUF;
-
-  for (int c = threadIdx.x; c < kTabDoubles / 2; c += 32 * W) cp_async16(T + 2 * c, a.tab + 2 * c);
-  if (a.static_ok)
-    for (int c = threadIdx.x; c < kSeg * kSeg / 2; c += 32 * W) cp_async16(Mi + 2 * c, a.minv + 2 * c);
-  const int line = blockIdx.x * W + warp;
-  const bool live = line < nlines;
+// Stage one row into a warp's buffers: field (+ epilogue operand) by cp.async, zero past the
+// far face.  Returns nothing; the caller commits the cp.async group.
+template <int S>
+__device__ __forceinline__ void contig_stage(const SweepArgs& a, int line, int needY, int lane,
+                                             double* buf, double* ybuf) {
   const Layout& L = a.L;
-  const int m = a.m, n2 = L.n2;
-  const int ii = 1 + line / (L.n1 - 2), jj = 1 + line % (L.n1 - 2);
-  const long long rb = L.at(ii, jj, 0);
+  const int n2 = L.n2;
+  const long long rb = L.at(1 + line / (L.n1 - 2), 1 + line % (L.n1 - 2), 0);
   const double* gsrc = a.src + rb;
-  const double* grho = a.rho + rb;
-  unsigned long long dw0 = 0, dw1 = 0;
-
-  // Phase 1: asynchronous staging.
-  if (live) {
+#pragma unroll 4
+  for (int e = lane; e < n2; e += 32) cp_async8(buf + cpos<S>(e), gsrc + e);
+  if (needY) {
     const double* gy = (needY == 1 ? a.src : a.acc) + rb;
 #pragma unroll 4
-    for (int e = lane; e < n2; e += 32) cp_async8(buf + cpos<S>(e), gsrc + e);
-    if (needY) {
-#pragma unroll 4
-      for (int e = lane; e < n2; e += 32) cp_async8(ybuf + e, gy + e);
-    }
-    for (int e = n2 + lane; e <= 32 * S + 1; e += 32) buf[cpos<S>(e)] = 0.0;  // past the face
-    const unsigned long long* dp = a.desc + 2 * ((long long)line * kSeg + lane);
-    dw0 = dp[0];
-    dw1 = dp[1];
+    for (int e = lane; e < n2; e += 32) cp_async8(ybuf + e, gy + e);
   }
-  cp_async_wait_all();
-  __syncthreads();  // tables are shared by the block
-  if (!live || dstep < a.step) return;
+  for (int e = n2 + lane; e <= 32 * S + 1; e += 32) buf[cpos<S>(e)] = 0.0;
+}
 
+// Solve one staged row (warp-wide) and store it.  Returns the lane's divergence flag.
+template <int S, bool CN>
+__device__ __forceinline__ bool contig_solve(const SweepArgs& a, int line, int lane,
+                                             const double* T, const double* Mi, double* buf,
+                                             const double* ybuf, double* sR,
+                                             unsigned long long dw0, unsigned long long dw1,
+                                             int needY) {
+  const Layout& L = a.L;
+  const int m = a.m, n2 = L.n2;
+  const long long rb = L.at(1 + line / (L.n1 - 2), 1 + line % (L.n1 - 2), 0);
+  const double* grho = a.rho + rb;
   const int i0 = lane * S;
   const unsigned long long amask = dw0;
   const unsigned cmask = (unsigned)(dw1 >> 32);
@@ -754,7 +739,6 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
   const double yFn0 = __shfl_down_sync(0xffffffffu, o.yF, 1);
   double t, tm;
   if (clean) {  // static inverse of the clean-line reduced system
-    double* sR = ybuf + YB;  // 32 doubles per warp after the row buffers
     sR[lane] = o.rs - o.as * o.yL - o.cs * (lane == 31 ? 0.0 : yFn0);
     __syncwarp();
     const int k1 = lane > 0 ? lane - 1 : 0;  // transposed inverse: column q at Mi[q*32]
@@ -817,37 +801,75 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
   bool bad = false;
   double* gdst = a.dst + rb;
   const int epi = a.epi;
-  if ((epi == EPI_STORE || epi == EPI_SRC || epi == EPI_MAOS0) && !a.check) {
-    for (int p = lane + 1; p <= m; p += 32) gdst[p] = buf[cpos<S>(p)];
-  } else {
-    auto loop = [&](auto f) {
-      for (int p0 = 1; p0 <= m; p0 += 32) {  // warp-uniform trip count (shuffles inside)
-        const int p = p0 + lane;
-        const int sg = min((p - 1) / S, kSeg - 1);
-        const uint32_t bits = node_bits(__shfl_sync(0xffffffffu, dw1, sg), (p - 1) - sg * S);
-        if (p <= m) {
-          const double x = f(p, bits);
-          gdst[p] = x;
-          bad |= is_bad(x, a.thr);
-        }
+  if (epi == EPI_STORE || epi == EPI_SRC || epi == EPI_MAOS0) {
+    if (a.check) {
+      for (int p = lane + 1; p <= m; p += 32) {
+        const double x = buf[cpos<S>(p)];
+        gdst[p] = x;
+        bad |= is_bad(x, a.thr);
       }
-    };
-    switch (epi) {
-      case EPI_FLOW: loop([&](int p, uint32_t c) { return flow_at(a, buf[cpos<S>(p)], c, 1.0); }); break;
-      case EPI_AOS0:
-        loop([&](int p, uint32_t c) { return __dadd_rn(flow_at(a, ybuf[p], c, a.pm), buf[cpos<S>(p)]); });
-        break;
-      case EPI_AOS1:
-      case EPI_MAOS1: loop([&](int p, uint32_t) { return __dadd_rn(ybuf[p], buf[cpos<S>(p)]); }); break;
-      case EPI_AOS2:
-        loop([&](int p, uint32_t) { return __dmul_rn(0.25, __dadd_rn(ybuf[p], buf[cpos<S>(p)])); });
-        break;
-      case EPI_MAOS2:
-        loop([&](int p, uint32_t) { return __ddiv_rn(__dadd_rn(ybuf[p], buf[cpos<S>(p)]), 3.0); });
-        break;
-      default: loop([&](int p, uint32_t) { return buf[cpos<S>(p)]; }); break;
+    } else {
+      for (int p = lane + 1; p <= m; p += 32) gdst[p] = buf[cpos<S>(p)];
+    }
+  } else if (epi == EPI_FLOW || epi == EPI_AOS0) {
+    for (int p0 = 1; p0 <= m; p0 += 32) {  // warp-uniform trip count (shuffles inside)
+      const int p = p0 + lane;
+      const int sg = min((p - 1) / S, kSeg - 1);
+      const uint32_t bits = node_bits(__shfl_sync(0xffffffffu, dw1, sg), (p - 1) - sg * S);
+      if (p <= m) {
+        const double x = epi == EPI_FLOW
+                             ? flow_at(a, buf[cpos<S>(p)], bits, 1.0)
+                             : __dadd_rn(flow_at(a, ybuf[p], bits, a.pm), buf[cpos<S>(p)]);
+        gdst[p] = x;
+        bad |= is_bad(x, a.thr);
+      }
+    }
+  } else {
+    for (int p = lane + 1; p <= m; p += 32) {
+      const double y = ybuf[p], x0 = buf[cpos<S>(p)];
+      double x;
+      if (epi == EPI_AOS2) x = __dmul_rn(0.25, __dadd_rn(y, x0));
+      else if (epi == EPI_MAOS2) x = __ddiv_rn(__dadd_rn(y, x0), 3.0);
+      else x = __dadd_rn(y, x0);  // AOS1 / MAOS1
+      gdst[p] = x;
+      bad |= is_bad(x, a.thr);
     }
   }
+  return bad;
+}
+
+// One warp per row; blocks of kContigWarps rows share the staged tables.
+template <int S, bool CN>
+__global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const int nlines) {
+  extern __shared__ double sm[];
+  constexpr int BUF = contig_buf_doubles<S>();
+  constexpr int W = kContigWarps;
+  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int needY = epi_needs(a.epi);
+  const int YB = needY ? 32 * S + 2 : 0;
+  double* T = sm;
+  double* Mi = T + kTabDoubles;
+  double* buf = Mi + kSeg * kSeg + warp * (BUF + YB + kSeg);
+  double* ybuf = buf + BUF;
+  double* sR = ybuf + YB;
+
+  for (int c = threadIdx.x; c < kTabDoubles / 2; c += 32 * W) cp_async16(T + 2 * c, a.tab + 2 * c);
+  if (a.static_ok)
+    for (int c = threadIdx.x; c < kSeg * kSeg / 2; c += 32 * W) cp_async16(Mi + 2 * c, a.minv + 2 * c);
+  const int line = blockIdx.x * W + warp;
+  const bool live = line < nlines;
+  unsigned long long dw0 = 0, dw1 = 0;
+  if (live) {
+    contig_stage<S>(a, line, needY, lane, buf, ybuf);
+    const unsigned long long* dp = a.desc + 2 * ((long long)line * kSeg + lane);
+    dw0 = dp[0];
+    dw1 = dp[1];
+  }
+  cp_async_wait_all();
+  __syncthreads();  // tables are shared by the block
+  if (!live || dstep < a.step) return;
+  const bool bad = contig_solve<S, CN>(a, line, lane, T, Mi, buf, ybuf, sR, dw0, dw1, needY);
   if (a.check) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(a.div_step, a.step);
   }
