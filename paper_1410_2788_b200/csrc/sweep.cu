@@ -91,6 +91,7 @@ struct SweepArgs {
   const double* tab;   // uniform-segment tables (kTabDoubles)
   const double* minv;  // 32x32 inverse of the clean-line reduced system
   const unsigned long long* desc;  // per-segment descriptors (2 words), see k_build_desc
+  const double* gfac;  // precomputed factors of general segments (5 x kTabRows each)
   int static_ok;       // the clean-line reduced inverse applies to this axis (32*S in {m, m+1})
   AxisCoef co;
   // Table of the dominant segment kind (interior, palette 0 = solvent) as kernel parameters:
@@ -261,91 +262,47 @@ __device__ __forceinline__ int seg_type(unsigned long long amask, int i0, int m,
   return -1;
 }
 
-// Local elimination of one segment.
-//   r[j]   rhs of row i0+j (registers; on exit y_j for a uniform segment)
-//   amask  bit j = eps bit (sweep axis) of the node of row i0+j, j = 0..S (S = next node)
-//   T      shared-memory copy of the uniform tables for this axis
-//   w0/WS  shared-memory slots of rows j = 0..S-2 (general path keeps y_j there)
-//   al/be  L1-resident local arrays for the general path
-// Returns the table type (>= 0) or -1 (general segment).
-template <int S, int WS>
-__device__ __forceinline__ int seg_eliminate(const SweepArgs& a, double (&r)[S],
-                                             unsigned long long amask, int i0, int first,
-                                             const double* T, double* w0, double (&al)[S],
-                                             double (&be)[S], SegOut& o) {
+// Descriptor word 0: bits 0..S eps bits, bits 34.. (slot + 1) of a general segment's
+// precomputed factors (0 = uniform segment, tables).
+constexpr int kSlotShift = 34;
+__host__ __device__ __forceinline__ unsigned long long eps_bits(unsigned long long w0, int S) {
+  return w0 & ((2ull << S) - 1ull);
+}
+
+// Elimination of one segment, always table driven: the dominant kind (interior segment,
+// palette 0) reads kernel-parameter tables when the whole warp is of that kind; otherwise
+// each lane reads its own table (shared-memory uniform tables, or the per-segment factors a
+// general segment got at march setup, k_seg_factors).  Returns the table pointer for the
+// finish step (nullptr = parameter tables).
+template <int S>
+__device__ __forceinline__ const double* seg_eliminate(const SweepArgs& a, double (&r)[S],
+                                                       unsigned long long amask, int i0,
+                                                       int first, const double* T, SegOut& o) {
   const int m = a.m;
   const int ttype = seg_type<S>(amask, i0, m, first);
   o.rs = r[S - 1];
   row_coefs(a.co, i0 + S - 1, m, (uint32_t)(amask >> (S - 1)) & 1u,
             (uint32_t)(amask >> S) & 1u, o.as, o.bs, o.cs);
-  if (ttype >= 0) {
-    if (ttype == 0 && !(amask & 1ull)) {
-      uni_eliminate<S>(r, [&](int q, int j) { return a.tmid[q * kTabRows + j]; }, o);
-    } else {
-      const double* Tv = T + (ttype * 2 + (int)(amask & 1ull)) * 5 * kTabRows;
-      uni_eliminate<S>(r, [&](int q, int j) { return Tv[q * kTabRows + j]; }, o);
-    }
-    return ttype;
+  if (__all_sync(0xffffffffu, ttype == 0 && !(amask & 1ull))) {
+    uni_eliminate<S>(r, [&](int q, int j) { return a.tmid[q * kTabRows + j]; }, o);
+    return nullptr;
   }
-  // General segment: rhs to shared memory, then rolled elimination.
-#pragma unroll
-  for (int j = 0; j < S - 1; ++j) w0[j * WS] = r[j];
-  double cpp = 0.0, dyp = 0.0, dap = 1.0, lastinv = 0.0, lastc = 0.0;
-#pragma unroll 1
-  for (int j = 0; j < S - 1; ++j) {
-    const uint32_t em = (uint32_t)(amask >> j) & 1u, ep = (uint32_t)(amask >> (j + 1)) & 1u;
-    double av, bv, cv;
-    row_coefs(a.co, i0 + j, m, em, ep, av, bv, cv);
-    const double inv = fast_rcp(fma(-av, cpp, bv));
-    const double cpj = cv * inv;
-    const double dy = fma(-av, dyp, w0[j * WS]) * inv;
-    const double dA = -(av * dap) * inv;
-    w0[j * WS] = dy;
-    al[j] = dA;
-    be[j] = cpj;
-    cpp = cpj;
-    dyp = dy;
-    dap = dA;
-    lastinv = inv;
-    lastc = cv;
-  }
-  double bb = -lastc * lastinv;
-  double y = w0[(S - 2) * WS], aa = al[S - 2];
-  be[S - 2] = bb;
-  o.yL = y;
-  o.aL = aa;
-  o.bL = bb;
-#pragma unroll 1
-  for (int j = S - 3; j >= 0; --j) {
-    const double c = be[j];
-    y = fma(-c, y, w0[j * WS]);
-    aa = fma(-c, aa, al[j]);
-    bb = -c * bb;
-    w0[j * WS] = y;
-    al[j] = aa;
-    be[j] = bb;
-  }
-  o.yF = w0[0];
-  o.aF = al[0];
-  o.bF = be[0];
-  return -1;
+  const double* Tv =
+      ttype >= 0 ? T + (ttype * 2 + (int)(amask & 1ull)) * 5 * kTabRows
+                 : a.gfac + (long long)((amask >> kSlotShift) - 1ull) * 5 * kTabRows;
+  uni_eliminate<S>(r, [&](int q, int j) { return Tv[q * kTabRows + j]; }, o);
+  return Tv;
 }
 
 // x_j = y_j + alpha_j*tm + beta_j*t for the inner rows, written to w0[j*WS].
 template <int S, int WS>
-__device__ __forceinline__ void seg_finish(const SweepArgs& a, int ttype, const double (&r)[S],
-                                           unsigned long long amask, double tm, double t,
-                                           const double* T, double* w0,
-                                           const double (&al)[S], const double (&be)[S]) {
-  if (ttype == 0 && !(amask & 1ull)) {
+__device__ __forceinline__ void seg_finish(const SweepArgs& a, const double* Tv,
+                                           const double (&r)[S], double tm, double t,
+                                           double* w0) {
+  if (Tv == nullptr)
     uni_finish<S, WS>(r, [&](int q, int j) { return a.tmid[q * kTabRows + j]; }, tm, t, w0);
-  } else if (ttype >= 0) {
-    const double* Tv = T + (ttype * 2 + (int)(amask & 1ull)) * 5 * kTabRows;
+  else
     uni_finish<S, WS>(r, [&](int q, int j) { return Tv[q * kTabRows + j]; }, tm, t, w0);
-  } else {
-#pragma unroll 1
-    for (int j = 0; j < S - 1; ++j) w0[j * WS] = fma(be[j], t, fma(al[j], tm, w0[j * WS]));
-  }
 }
 
 // Reduced-system coefficients of separator k (needs the next segment's first-row values).
@@ -436,7 +393,7 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 4 : (LB * kSeg
   const double* grho = a.rho + base;
 
   // Phase 1: asynchronous staging of the field (+ epilogue operand), descriptors, tables.
-  if (a.dbg != 2) {
+  if (a.dbg < 2) {
     const int q = (tid % CPR) * 2, p0 = tid / CPR;
     const long long gstep = (long long)RPP * stride;
     const double* g = gsrc + p0 * (long long)stride + q;
@@ -460,8 +417,10 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 4 : (LB * kSeg
   if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
 
   const int i0 = seg * S;
-  const unsigned long long amask = D[2 * tid];
-  const unsigned cmask = (unsigned)(D[2 * tid + 1] >> 32);
+  // columns past the last interior one read unrelated descriptor words: neutralise them
+  const bool act = lane < ncols;
+  const unsigned long long amask = act ? D[2 * tid] : 0ull;
+  const unsigned cmask = act ? (unsigned)(D[2 * tid + 1] >> 32) : 0u;
   const double* rrow = grho + (i0 + 1) * stride + lane;
   auto rho_row = [&](int j) { return rrow + j * stride; };
   double* w0 = W + (i0 + 1) * LB + lane;
@@ -507,11 +466,16 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 4 : (LB * kSeg
     if (seg == (m - 1) / S && active)
       fold_high<S>(a, r, amask, a.bnd[base + (long long)(m + 1) * stride + lane]);
     // clean tile: every line of the tile is one dielectric (palette 0) end to end
-    const bool clean = __syncthreads_and(!active || amask == 0ull) && a.static_ok;
+    const bool clean = __syncthreads_and(!active || eps_bits(amask, S) == 0ull) && a.static_ok;
 
-    double al[S], be[S];
     SegOut o;
-    const int ttype = seg_eliminate<S, LB>(a, r, amask, i0, seg == 0, T, w0, al, be, o);
+    const double* Tv = nullptr;
+    if (a.dbg == 4) {
+      o.yF = r[0]; o.aF = r[1]; o.bF = r[2]; o.yL = r[3]; o.aL = r[4]; o.bL = r[5];
+      o.as = r[6]; o.bs = 1.0; o.cs = r[7]; o.rs = r[8];
+    } else {
+      Tv = seg_eliminate<S>(a, r, amask, i0, seg == 0, T, o);
+    }
 
     // Phase 3: reduced system over the 32 separators of each line.
     double* sA = X;
@@ -519,7 +483,10 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 4 : (LB * kSeg
     double* sC = X + 2 * NT;
     double* sR = X + 3 * NT;
     double t, tm;
-    if (clean) {  // static inverse: one exchange of y_F, one of R, then two dot products
+    if (a.dbg == 3) {
+      t = o.yF + o.rs;
+      tm = o.yL;
+    } else if (clean) {  // static inverse: one exchange of y_F, one of R, then two dot products
       sA[tid] = o.yF;
       __syncthreads();
       const double yFn = (seg + 1 < kSegS) ? sA[tid + LB] : 0.0;
@@ -585,7 +552,8 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 4 : (LB * kSeg
     }
 
     // Phase 4: reconstruct the inner rows, separator = t; sparse source epilogue (LODIE1).
-    seg_finish<S, LB>(a, ttype, r, amask, tm, t, T, w0, al, be);
+    if (a.dbg == 4) { w0[0] = t + tm; } else
+    seg_finish<S, LB>(a, Tv, r, tm, t, w0);
     if (i0 + S - 1 < m) W[(i0 + S) * LB + lane] = t;
     if (a.epi == EPI_SRC && cmask)
       charged_fixup(cmask, a.epi_coef, [&](int j) { return w0 + j * LB; }, rho_row);
@@ -602,7 +570,7 @@ store:
       const long long gstep = (long long)RPP * stride;
       double* g = gdst + p0 * (long long)stride + q;
       const double* w = W + p0 * LB + q;
-      if (a.dbg == 2) {
+      if (a.dbg >= 2) {
         if (W[tid] == 12345.678) gdst[0] = 0.0;  // keep the solve alive
       } else if (q + 1 < ncols) {
 #pragma unroll 4
@@ -729,12 +697,11 @@ __device__ __forceinline__ bool contig_solve(const SweepArgs& a, int line, int l
   }
   if (lane == 0) r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], a.bnd[rb]));
   if (lane == (m - 1) / S) fold_high<S>(a, r, amask, a.bnd[rb + m + 1]);
-  const bool clean = __all_sync(0xffffffffu, amask == 0ull) && a.static_ok;
+  const bool clean = __all_sync(0xffffffffu, eps_bits(amask, S) == 0ull) && a.static_ok;
   __syncwarp();
 
-  double al[S], be[S];
   SegOut o;
-  const int ttype = seg_eliminate<S, 1>(a, r, amask, i0, lane == 0, T, w0, al, be, o);
+  const double* Tv = seg_eliminate<S>(a, r, amask, i0, lane == 0, T, o);
 
   const double yFn0 = __shfl_down_sync(0xffffffffu, o.yF, 1);
   double t, tm;
@@ -792,7 +759,7 @@ __device__ __forceinline__ bool contig_solve(const SweepArgs& a, int line, int l
     if (lane == 0) tm = 0.0;
   }
 
-  seg_finish<S, 1>(a, ttype, r, amask, tm, t, T, w0, al, be);
+  seg_finish<S, 1>(a, Tv, r, tm, t, w0);
   if (i0 + S - 1 < m) buf[cpos<S>(i0 + S)] = t;
   if (a.epi == EPI_SRC && cmask)
     charged_fixup(cmask, a.epi_coef, [&](int j) { return buf + cpos<S>(i0 + 1 + j); }, rho_row);
@@ -920,6 +887,69 @@ __global__ void k_build_desc(const Layout L, int axis, int S, int P,
     }
     desc[2 * t] = w0;
     desc[2 * t + 1] = w1;
+  }
+}
+
+// General segments (not one dielectric, or partial at the line end): their LU factors,
+// alpha and beta are static for the march, so they are computed once here (same
+// recurrences as the uniform tables, per-row coefficients) and read like a table by the
+// sweeps.  Pass 0 counts, pass 1 assigns slots (atomic; values do not depend on the slot)
+// and writes factors + slot into descriptor word 0.
+__global__ void k_seg_factors(const Layout L, int axis, int S, int P, AxisCoef co, int pass,
+                              unsigned long long* __restrict__ desc, int* __restrict__ counter,
+                              double* __restrict__ gfac) {
+  const int m = (axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2)) - 2;
+  long long nseg;
+  if (axis == 2) nseg = (long long)(L.n0 - 2) * (L.n1 - 2) * P;
+  else nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * (L.n2 - 2);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nseg;
+       t += (long long)gridDim.x * blockDim.x) {
+    int seg;
+    if (axis == 2) seg = (int)(t % P);
+    else seg = (int)((t / (L.n2 - 2)) % P);
+    const int i0 = seg * S, first = seg == 0;
+    const unsigned long long w0 = desc[2 * t];
+    const unsigned long long eb = eps_bits(w0, S);
+    const unsigned long long allm = (1ull << S) - 1ull, bits = eb & allm;
+    bool general = true;
+    if (bits == 0ull || bits == allm) {
+      if (i0 + S <= m) general = false;
+      else if (i0 + S - 1 == m && !first) general = false;
+    }
+    if (!general) continue;
+    if (pass == 0) {
+      atomicAdd(counter, 1);
+      continue;
+    }
+    const int slot = atomicAdd(counter, 1);
+    double* F = gfac + (long long)slot * 5 * kTabRows;
+    double cpp = 0.0, dap = 1.0, lastinv = 0.0, lastc = 0.0;
+    for (int j = 0; j < S - 1; ++j) {
+      double av, bv, cv;
+      row_coefs(co, i0 + j, m, (uint32_t)(eb >> j) & 1u, (uint32_t)(eb >> (j + 1)) & 1u, av, bv,
+                cv);
+      const double inv = 1.0 / (bv - av * cpp);
+      const double cpj = cv * inv;
+      const double da = -(av * dap) * inv;
+      F[TQ_INV * kTabRows + j] = inv;
+      F[TQ_G * kTabRows + j] = av * inv;
+      F[TQ_CP * kTabRows + j] = cpj;
+      F[TQ_AL * kTabRows + j] = da;  // forward values, replaced by alpha below
+      cpp = cpj;
+      dap = da;
+      lastinv = inv;
+      lastc = cv;
+    }
+    double bb = -lastc * lastinv, aa = F[TQ_AL * kTabRows + S - 2];
+    F[TQ_BE * kTabRows + S - 2] = bb;
+    for (int j = S - 3; j >= 0; --j) {
+      const double c = F[TQ_CP * kTabRows + j];
+      aa = F[TQ_AL * kTabRows + j] - c * aa;
+      bb = -c * bb;
+      F[TQ_AL * kTabRows + j] = aa;
+      F[TQ_BE * kTabRows + j] = bb;
+    }
+    desc[2 * t] = w0 | ((unsigned long long)(slot + 1) << kSlotShift);
   }
 }
 
@@ -1151,6 +1181,7 @@ static SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, 
 struct AxisAux {
   double* buf = nullptr;
   unsigned long long* desc = nullptr;
+  double* gfac = nullptr;
 };
 
 static long long desc_segments(const Layout& L, int axis, int P) {
@@ -1176,7 +1207,23 @@ static int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& a
   PBG_CUDA(cudaMallocAsync(&aux.desc, (2 * nseg + 64) * sizeof(unsigned long long), st));
   k_build_desc<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, codes, aux.desc);
   PBG_LAUNCH_CHECK("k_build_desc");
-  PBG_CUDA(cudaStreamSynchronize(st));  // host staging vector dies here
+  int* counter = nullptr;
+  PBG_CUDA(cudaMallocAsync(&counter, sizeof(int), st));
+  PBG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
+  k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, a.co, 0, aux.desc, counter, nullptr);
+  PBG_LAUNCH_CHECK("k_seg_factors");
+  int ngen = 0;
+  PBG_CUDA(cudaMemcpyAsync(&ngen, counter, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PBG_CUDA(cudaStreamSynchronize(st));  // also: the host staging vector dies here
+  PBG_CUDA(cudaMallocAsync(&aux.gfac, ((size_t)ngen + 1) * 5 * kTabRows * sizeof(double), st));
+  if (ngen > 0) {
+    PBG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
+    k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, a.co, 1, aux.desc, counter,
+                                           aux.gfac);
+    PBG_LAUNCH_CHECK("k_seg_factors");
+  }
+  PBG_CUDA(cudaFreeAsync(counter, st));
+  a.gfac = aux.gfac;
   a.tab = aux.buf;
   a.minv = aux.buf + kTabDoubles;
   a.desc = aux.desc;
@@ -1186,8 +1233,10 @@ static int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& a
 static void release_axis(AxisAux& aux, cudaStream_t st) {
   if (aux.buf) cudaFreeAsync(aux.buf, st);
   if (aux.desc) cudaFreeAsync(aux.desc, st);
+  if (aux.gfac) cudaFreeAsync(aux.gfac, st);
   aux.buf = nullptr;
   aux.desc = nullptr;
+  aux.gfac = nullptr;
 }
 
 static int launch_sweep(const SweepArgs& a, int axis, cudaStream_t st) {
