@@ -135,9 +135,11 @@ __host__ __device__ __forceinline__ int epi_needs(int epi) {
                                 : 0);
 }
 
+// One inlined flow evaluation: select the palette constants first (a ternary over two calls
+// is if-converted by the compiler into two full evaluations).
 __device__ __forceinline__ double flow_at(const SweepArgs& a, double w, uint32_t c, double pm) {
-  return (c & 1u) ? sinh_flow_fast(w, a.decay1, a.sat1, pm)
-                  : sinh_flow_fast(w, a.decay0, a.sat0, pm);
+  const bool s = (c & 1u) != 0;
+  return sinh_flow_fast(w, s ? a.decay1 : a.decay0, s ? a.sat1 : a.sat0, pm);
 }
 
 __device__ __forceinline__ double pro_val(const SweepArgs& a, double v, uint32_t c,
@@ -779,14 +781,16 @@ __device__ __forceinline__ bool contig_solve(const SweepArgs& a, int line, int l
       for (int p = lane + 1; p <= m; p += 32) gdst[p] = buf[cpos<S>(p)];
     }
   } else if (epi == EPI_FLOW || epi == EPI_AOS0) {
+    const bool aos0 = epi == EPI_AOS0;
+    const double pm = aos0 ? a.pm : 1.0;
     for (int p0 = 1; p0 <= m; p0 += 32) {  // warp-uniform trip count (shuffles inside)
       const int p = p0 + lane;
       const int sg = min((p - 1) / S, kSeg - 1);
       const uint32_t bits = node_bits(__shfl_sync(0xffffffffu, dw1, sg), (p - 1) - sg * S);
       if (p <= m) {
-        const double x = epi == EPI_FLOW
-                             ? flow_at(a, buf[cpos<S>(p)], bits, 1.0)
-                             : __dadd_rn(flow_at(a, ybuf[p], bits, a.pm), buf[cpos<S>(p)]);
+        const double xs = buf[cpos<S>(p)];
+        const double f = flow_at(a, aos0 ? ybuf[p] : xs, bits, pm);
+        const double x = aos0 ? __dadd_rn(f, xs) : f;
         gdst[p] = x;
         bad |= is_bad(x, a.thr);
       }
