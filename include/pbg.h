@@ -199,6 +199,42 @@ PBG_API int pbg_sweep(const pbg_grid* g, const pbg_palette* pal, const uint8_t* 
                       int32_t axis, double factor, int32_t cn, const double* src,
                       const double* bnd, double* dst, void* stream);
 
+/* ---------------------------------------------------------------------------------------
+ * Slab-decomposed march (no reference counterpart -- the reference is
+ * single-process).  The grid is split along axis 0; rank r owns a contiguous range of
+ * interior planes and describes its LOCAL grid in d: n[0] = owned planes + 2, plane 0 and
+ * plane n[0]-1 are the global faces on the first / last rank and ghost planes otherwise
+ * (their initial contents: the neighbours' initial values).  codes, rho, initial and work[]
+ * are the local slabs of the global pitched buffers (planes [first-1, last+1]), which share
+ * the global layout.  Variants: LODIE1, LODIE2, LODCN2.
+ *
+ * Exchange buffers (device, owned by the caller): send holds pbg_slab_exchange_elems(local)
+ * doubles, recv nranks times that; after every *pack / step_a call the caller all-gathers
+ * send into recv in rank order (ncclAllGather, or a device copy when all partitions live on
+ * one GPU) on the same stream before the next call.
+ *
+ *   create            computes this rank's static responses into send  -> all-gather
+ *   setup             keeps the gathered responses
+ *   per step:  [halo_pack -> all-gather -> halo_unpack]   (CN only)
+ *              step_a  (chunk solve, end rows + divergence flag into send) -> all-gather
+ *              step_b  (interface solve, axis-0 chunk sweep, axis-1, axis-2 sweeps)
+ *   flag_pack -> all-gather -> finish  (steps taken / divergence agreed over all ranks;
+ *                                       *result_slot indexes work[] as in pbg_march)
+ * Results equal pbg_march on the whole grid up to reassociation (parity tests). */
+typedef struct pbg_slab pbg_slab;
+PBG_API int64_t pbg_slab_exchange_elems(const pbg_grid* local);
+PBG_API int pbg_slab_create(const pbg_march_desc* d, int32_t rank, int32_t nranks,
+                            double* send, double* recv, pbg_slab** out, void* stream);
+PBG_API int pbg_slab_setup(pbg_slab* h, void* stream);
+PBG_API int pbg_slab_halo_pack(pbg_slab* h, void* stream);
+PBG_API int pbg_slab_halo_unpack(pbg_slab* h, void* stream);
+PBG_API int pbg_slab_step_a(pbg_slab* h, void* stream);
+PBG_API int pbg_slab_step_b(pbg_slab* h, void* stream);
+PBG_API int pbg_slab_flag_pack(pbg_slab* h, void* stream);
+PBG_API int pbg_slab_finish(pbg_slab* h, int32_t* steps_taken, int32_t* diverged_step,
+                            int32_t* result_slot, void* stream);
+PBG_API int pbg_slab_destroy(pbg_slab* h, void* stream);
+
 /* nonlinear_step (schemes.py:106-120) on n contiguous elements with per-element kappa2:
  * out = pm * flow(w; decay = exp(-coef * kappa2)), coef = rate*dt/alpha. */
 PBG_API int pbg_flow_dense(int64_t n, const double* w, const double* kappa2, double coef,

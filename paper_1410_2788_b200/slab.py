@@ -1,0 +1,275 @@
+"""Slab-decomposed march across ranks.
+
+The grid is split along axis 0 into contiguous slabs of interior planes, one per rank
+(`slab_ranges`).  Every step runs the rank-local phase A (chunk solve of the axis-0 lines
+with zero ghost values, end rows only), one all-gather of the chunk end rows, and phase B
+(interface solve, axis-0 chunk sweep with the neighbours' end values, local axis-1/2
+sweeps with the fused source and flow).  `include/pbg.h` (pbg_slab_*) documents the
+algebra; the result equals the single-device march up to reassociation.
+
+Exchanges are pluggable:
+  * `GroupExchange`  one partition per process, `torch.distributed` all-gather (NCCL over
+    NVLink on the GPU box; gloo in the CPU tests of the orchestration);
+  * `LocalExchange`  several partitions in one process on one GPU, exchange by device copy
+    (how the multi-rank algebra is tested with a single GPU).
+
+The reference (pbsplit) is single-process; this module has no reference counterpart and
+only the LOD variants LODIE1, LODIE2 and LODCN2 shard (AOS/MAOS/LODCN1 stay single-device).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as nat
+from .grid import ScalarField
+from .schemes import MarchConfig, MarchReport, _resolve_alpha, device_problem, parse_variant
+
+SLAB_SCHEMES = ("LODIE1", "LODIE2", "LODCN2")
+MAX_RANKS = 16
+
+
+def slab_ranges(n0: int, nranks: int):
+    """Owned global interior planes [first, stop) per rank: contiguous, sizes differ by <= 1."""
+    m = int(n0) - 2
+    if not (1 <= nranks <= MAX_RANKS):
+        raise ValueError(f"nranks must be in 1..{MAX_RANKS}")
+    if m < nranks:
+        raise ValueError(f"{m} interior planes cannot be split over {nranks} ranks")
+    base, extra = divmod(m, nranks)
+    out, first = [], 1
+    for r in range(nranks):
+        cnt = base + (1 if r < extra else 0)
+        out.append((first, first + cnt))
+        first += cnt
+    return out
+
+
+def run_slabs(parts, exchange, nsteps: int, cn: bool):
+    """Drive the partitions of this process through setup, `nsteps` steps and the final flag
+    agreement.  `parts` are this process's partitions (all of them for LocalExchange, one
+    for GroupExchange); each exposes create-time `send`/`recv` buffers and the phase calls."""
+    exchange.gather(parts)  # static responses (computed at creation)
+    for p in parts:
+        p.setup()
+    for _ in range(nsteps):
+        if cn:
+            for p in parts:
+                p.halo_pack()
+            exchange.gather(parts)
+            for p in parts:
+                p.halo_unpack()
+        for p in parts:
+            p.step_a()
+        exchange.gather(parts)
+        for p in parts:
+            p.step_b()
+    for p in parts:
+        p.flag_pack()
+    exchange.gather(parts)
+    return [p.finish() for p in parts]
+
+
+class LocalExchange:
+    """All partitions live in this process and share one `recv` buffer."""
+
+    def gather(self, parts):
+        E = parts[0].send.numel()
+        recv = parts[0].recv
+        for r, p in enumerate(parts):
+            recv[r * E:(r + 1) * E].copy_(p.send)
+
+
+class GroupExchange:
+    """One partition per process; all-gather over a torch.distributed group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.nccl = dist.get_backend(group) == "nccl"
+
+    def gather(self, parts):
+        (p,) = parts
+        if self.nccl:
+            self.dist.all_gather_into_tensor(p.recv, p.send, group=self.group)
+        else:
+            n = p.recv.numel() // p.send.numel()
+            self.dist.all_gather(list(p.recv.view(n, -1).unbind(0)), p.send, group=self.group)
+
+
+class DeviceSlab:
+    """One rank's slab on the device: local copies of the global buffers' planes
+    [first-1, stop] (same pitched layout) and a native pbg_slab handle."""
+
+    def __init__(self, dp, variant, dt, alpha, nsteps, threshold, rank, nranks, first, stop,
+                 initial_dev, recv=None, check_divergence=True):
+        torch = nat.torch_cuda()
+        self.lib = nat.lib()
+        g = dp.grid
+        n0, n1, n2 = g.shape
+        pitch, _ = nat.layout(g.shape)
+        plane = n1 * pitch
+        self.rank, self.nranks, self.first, self.stop = rank, nranks, first, stop
+        self.plane = plane
+        nl0 = stop - first + 2
+        lgs = nat.PbgGrid()
+        for a in range(3):
+            lgs.n[a] = dp.gs.n[a]
+            lgs.lo[a] = dp.gs.lo[a]
+        lgs.n[0] = nl0
+        lgs.lo[0] = dp.gs.lo[0] + (first - 1) * dp.gs.h
+        lgs.pitch = dp.gs.pitch
+        lgs.h = dp.gs.h
+        self.gs = lgs
+        nloc = nl0 * plane + 64
+        lo, hi = (first - 1) * plane, (stop + 1) * plane
+
+        def slab(t):
+            out = torch.zeros(nloc, dtype=t.dtype, device=t.device)
+            out[:hi - lo].copy_(t[lo:hi])
+            return out
+
+        self.codes = slab(dp.codes)
+        self.rho = slab(dp.rho)
+        self.work = (slab(dp.bnd), slab(dp.bnd))
+        self.initial = slab(initial_dev)
+        E = int(self.lib.pbg_slab_exchange_elems(ctypes.byref(lgs)))
+        self.send = torch.empty(E, dtype=torch.float64, device="cuda")
+        self.recv = recv if recv is not None else torch.empty(nranks * E, dtype=torch.float64,
+                                                              device="cuda")
+        d = nat.PbgMarchDesc()
+        d.grid = lgs
+        d.pal = dp.pal
+        d.variant = nat.VARIANT_IDS[variant]
+        d.aos_literal = 0
+        d.dt = float(dt)
+        d.alpha = float(alpha)
+        d.divergence_threshold = float(threshold)
+        d.nsteps = int(nsteps)
+        d.check_divergence = 1 if check_divergence else 0
+        d.codes = self.codes.data_ptr()
+        d.rho = self.rho.data_ptr()
+        d.initial = self.initial.data_ptr()
+        d.work[0] = self.work[0].data_ptr()
+        d.work[1] = self.work[1].data_ptr()
+        self.desc = d
+        self.handle = ctypes.c_void_p()
+        nat.check(self.lib.pbg_slab_create(ctypes.byref(d), int(rank), int(nranks),
+                                           nat.ptr(self.send), nat.ptr(self.recv),
+                                           ctypes.byref(self.handle), nat.stream_ptr()))
+
+    def _call(self, fn):
+        nat.check(fn(self.handle, nat.stream_ptr()))
+
+    def setup(self):
+        self._call(self.lib.pbg_slab_setup)
+
+    def halo_pack(self):
+        self._call(self.lib.pbg_slab_halo_pack)
+
+    def halo_unpack(self):
+        self._call(self.lib.pbg_slab_halo_unpack)
+
+    def step_a(self):
+        self._call(self.lib.pbg_slab_step_a)
+
+    def step_b(self):
+        self._call(self.lib.pbg_slab_step_b)
+
+    def flag_pack(self):
+        self._call(self.lib.pbg_slab_flag_pack)
+
+    def finish(self):
+        taken, dstep, slot = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        nat.check(self.lib.pbg_slab_finish(self.handle, ctypes.byref(taken),
+                                           ctypes.byref(dstep), ctypes.byref(slot),
+                                           nat.stream_ptr()))
+        return taken.value, (dstep.value or None), self.work[slot.value]
+
+    def owned(self, local_field):
+        """The owned planes of a local field (flat view)."""
+        return local_field[self.plane:(self.stop - self.first + 1) * self.plane]
+
+    def close(self):
+        if self.handle:
+            self.lib.pbg_slab_destroy(self.handle, nat.stream_ptr())
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _check_variant(config: MarchConfig):
+    v = parse_variant(config.variant).value
+    if v not in SLAB_SCHEMES:
+        raise NotImplementedError(f"{v} does not shard across ranks; slab schemes: "
+                                  f"{', '.join(SLAB_SCHEMES)}")
+    return v
+
+
+def make_slabs(problem, config: MarchConfig, ranks, nranks: int, recv=None,
+               initial_dev=None):
+    """DeviceSlab objects for the given ranks of an `nranks`-way split of `problem`."""
+    v = _check_variant(config)
+    dp = device_problem(problem)
+    nsteps = max(1, int(round(config.T / config.dt)))
+    init = initial_dev if initial_dev is not None else problem.initial._device()
+    rng = slab_ranges(problem.grid.shape[0], nranks)
+    return [DeviceSlab(dp, v, config.dt, _resolve_alpha(config.alpha, problem), nsteps,
+                       config.divergence_threshold, r, nranks, rng[r][0], rng[r][1], init,
+                       recv=recv) for r in ranks], nsteps, v.startswith("LODCN")
+
+
+def march_partitioned(problem, config: MarchConfig, nparts: int) -> MarchReport:
+    """march() with the grid split into `nparts` slabs inside this process (one GPU,
+    exchange by device copy).  Same result as march() up to reassociation."""
+    torch = nat.torch_cuda()
+    _check_variant(config)
+    g = problem.grid
+    E = int(nat.lib().pbg_slab_exchange_elems(ctypes.byref(_local_gs(g, 1))))
+    recv = torch.empty(nparts * E, dtype=torch.float64, device="cuda")
+    parts, nsteps, cn = make_slabs(problem, config, range(nparts), nparts, recv=recv)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = run_slabs(parts, LocalExchange(), nsteps, cn)
+    e1.record()
+    torch.cuda.synchronize()
+    final = device_problem(problem).bnd.clone()
+    for p, (_, _, f) in zip(parts, res):
+        plane = p.plane
+        final[p.first * plane:p.stop * plane].copy_(p.owned(f))
+    taken, dstep = res[0][0], res[0][1]
+    for p in parts:
+        p.close()
+    diverged = dstep is not None
+    return MarchReport(final=ScalarField._from_device(g, final, diverged), steps_taken=taken,
+                       diverged=diverged, diverged_step=dstep,
+                       wall_time=e0.elapsed_time(e1) / 1e3)
+
+
+def _local_gs(grid, nl0):
+    gs = nat.grid_struct(grid)
+    gs.n[0] = nl0
+    return gs
+
+
+def march_distributed(problem, config: MarchConfig, group=None):
+    """march() with one slab per torch.distributed rank (NCCL on the GPU box).  Returns
+    (steps_taken, diverged_step, the rank's DeviceSlab, its final local field)."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    (part,), nsteps, cn = make_slabs(problem, config, [rank], world)
+    taken, dstep, final = run_slabs([part], GroupExchange(group), nsteps, cn)[0]
+    return taken, dstep, part, final
+
+
+__all__ = ["SLAB_SCHEMES", "slab_ranges", "run_slabs", "LocalExchange", "GroupExchange",
+           "DeviceSlab", "make_slabs", "march_partitioned", "march_distributed"]

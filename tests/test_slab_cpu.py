@@ -1,0 +1,124 @@
+"""Slab decomposition across ranks, CPU: the orchestration of
+paper_1410_2788_b200.slab.run_slabs with numpy partitions (tests/slab_numpy.py), in one
+process and over a world_size-2 gloo group, against the reference's golden marches."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1410_2788_b200.slab import GroupExchange, LocalExchange, run_slabs, slab_ranges
+from tests.helpers import golden, oracle_protein
+from tests.slab_numpy import NumpySlab
+
+TOL = 1e-12
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def test_slab_ranges_cover_interior_contiguously():
+    for n0 in (3, 10, 65, 513):
+        for n in range(1, min(16, n0 - 2) + 1):
+            rng = slab_ranges(n0, n)
+            assert rng[0][0] == 1 and rng[-1][1] == n0 - 1
+            assert all(a[1] == b[0] for a, b in zip(rng, rng[1:]))
+            sizes = [b - a for a, b in rng]
+            assert min(sizes) >= 1 and max(sizes) - min(sizes) <= 1
+    assert [b - a for a, b in slab_ranges(513, 8)] == [64] * 7 + [63]
+    with pytest.raises(ValueError):
+        slab_ranges(5, 4)
+    with pytest.raises(ValueError):
+        slab_ranges(100, 17)
+
+
+def _parts_local(p, variant, dt, T, nparts, threshold=1e12):
+    rng = slab_ranges(p.grid.shape[0], nparts)
+    E = 4 * (p.grid.shape[1] - 2) * (p.grid.shape[2] - 2) + 1
+    recv = torch.zeros(nparts * E, dtype=torch.float64)
+    return [NumpySlab(p, variant, dt, T, r, nparts, a, b, recv=recv, threshold=threshold)
+            for r, (a, b) in enumerate(rng)]
+
+
+def _assemble(p, parts, results):
+    out = p.bvals.copy()
+    for part, (_, _, u) in zip(parts, results):
+        out[part.first:part.stop] = u[1:-1]
+    return out
+
+
+@pytest.mark.parametrize("variant", ["LODIE1", "LODIE2", "LODCN2"])
+@pytest.mark.parametrize("nparts", [1, 3, 4])
+def test_partitioned_march_matches_reference_golden(variant, nparts):
+    d = golden("march_variants")
+    p = oracle_protein(d)
+    dt, T = float(d["dt"]), float(d["T"])
+    nsteps = max(1, int(round(T / dt)))
+    parts = _parts_local(p, variant, dt, T, nparts)
+    res = run_slabs(parts, LocalExchange(), nsteps, variant.startswith("LODCN"))
+    assert all(r[0] == nsteps and r[1] is None for r in res)
+    assert _rel(_assemble(p, parts, res), d[variant]) <= TOL
+
+
+def test_partitioned_divergence_agrees_over_ranks():
+    d = golden("march_variants")
+    p = oracle_protein(d)
+    parts = _parts_local(p, "LODIE1", 0.3, 3.0, 3, threshold=2.0e3)
+    res = run_slabs(parts, LocalExchange(), 10, False)
+    taken = {r[0] for r in res}
+    dstep = {r[1] for r in res}
+    assert taken == {int(d["div_steps"])} and dstep == {int(d["div_step"])}
+    assert _rel(_assemble(p, parts, res), d["div_final"]) <= TOL
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, variant, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        d = golden("march_variants")
+        p = oracle_protein(d)
+        dt, T = float(d["dt"]), float(d["T"])
+        nsteps = max(1, int(round(T / dt)))
+        a, b = slab_ranges(p.grid.shape[0], world)[rank]
+        part = NumpySlab(p, variant, dt, T, rank, world, a, b)
+        taken, dstep, u = run_slabs([part], GroupExchange(), nsteps,
+                                    variant.startswith("LODCN"))[0]
+        # gather the owned planes on every rank (the decomposition's result exchange)
+        owned = torch.from_numpy(np.ascontiguousarray(u[1:-1]))
+        sizes = [bb - aa for aa, bb in slab_ranges(p.grid.shape[0], world)]
+        n1, n2 = p.grid.shape[1:]
+        bufs = [torch.zeros((s, n1, n2), dtype=torch.float64) for s in sizes]
+        dist.all_gather(bufs, owned)
+        if rank == 0:
+            full = p.bvals.copy()
+            full[1:-1] = torch.cat(bufs).numpy()
+            np.savez(os.path.join(out_dir, f"{variant}.npz"), full=full, taken=taken,
+                     dstep=-1 if dstep is None else dstep)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("variant", ["LODIE2", "LODCN2"])
+def test_gloo_world2_slab_march(tmp_path, variant):
+    world = 2
+    mp.spawn(_gloo_worker, args=(world, _free_port(), variant, str(tmp_path)), nprocs=world,
+             join=True)
+    d = golden("march_variants")
+    r = np.load(tmp_path / f"{variant}.npz")
+    assert int(r["taken"]) == max(1, int(round(float(d["T"]) / float(d["dt"]))))
+    assert int(r["dstep"]) == -1
+    assert _rel(r["full"], d[variant]) <= TOL
