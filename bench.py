@@ -8,8 +8,10 @@ needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c3] [--impl ours|reference]
 
-N > 1 (torchrun, one rank per GPU): every rank marches its own copy (replicas, weak
-scaling); the slab-sharded single-grid solve is the next multi-GPU step.
+N > 1 (torchrun, one rank per GPU, NCCL): the grid is split into axis-0 slabs, one per
+rank (paper_1410_2788_b200.slab: partitioned axis-0 solve, one all-gather of the chunk end
+rows per step) -- strong scaling, `value` = whole-grid updates/s, time = max over ranks.
+`--mode replicas` instead marches an independent copy per rank (weak scaling).
 """
 
 from __future__ import annotations
@@ -41,6 +43,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default=None, choices=["slab", "replicas"],
+                    help="slab-sharded single grid (default for N > 1; with N = 1 it runs "
+                         "the slab path as one NCCL rank) or independent replicas")
     return ap.parse_args()
 
 
@@ -281,13 +286,21 @@ def main():
         return reference_arm(args, world, rank)
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    mode = args.mode or ("slab" if world > 1 else "single")
+    if world > 1 or mode == "slab":
         import torch.distributed as dist
 
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29531")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     c, p, t_asm = build_problem(args.config)
     nint = (c.n - 2) ** 3
+    if dist and mode == "slab":
+        return slab_main(args, c, p, t_asm, world, rank, local, dist)
     d, dp, keep = march_desc(p, c, args.steps)
     run_march(d, max(3, args.warmup))
     torch.cuda.synchronize()
@@ -361,6 +374,101 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def slab_main(args, c, p, t_asm, world, rank, local, dist):
+    """N > 1: one axis-0 slab per rank, NCCL all-gather exchange (strong scaling)."""
+    import torch
+
+    import paper_1410_2788_b200 as pb
+    from paper_1410_2788_b200.slab import GroupExchange, make_slabs, run_slabs, slab_ranges
+
+    nint = (c.n - 2) ** 3
+    cfg = pb.MarchConfig(dt=c.dt, T=c.dt * args.steps, variant=c.variant)
+    (part,), _, cn = make_slabs(p, cfg, [rank], world)
+    ex = GroupExchange()
+    warm = max(3, args.warmup)
+    res = run_slabs([part], ex, warm, cn)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        res = run_slabs([part], ex, args.steps, cn)
+        e1.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    taken, dstep, final = res[0]
+    if dstep is not None:
+        raise RuntimeError(f"slab march diverged at step {dstep}")
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = nint * args.steps / (ms_max / 1e3)
+    own = part.stop - part.first
+    local_nodes = own * (c.n - 2) ** 2
+
+    e2e = None
+    if not args.no_e2e:  # host inputs of the rank's slab -> device, march, owned planes -> host
+        pin = lambda t: torch.empty(t.numel(), dtype=t.dtype, pin_memory=True).copy_(t)
+        host = [pin(part.codes), pin(part.rho), pin(part.work[0])]
+        out_h = torch.empty(part.owned(final).numel(), dtype=torch.float64, pin_memory=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        part.codes.copy_(host[0], non_blocking=True)
+        part.rho.copy_(host[1], non_blocking=True)
+        part.work[0].copy_(host[2], non_blocking=True)
+        part.work[1].copy_(host[2], non_blocking=True)
+        part.initial.copy_(host[2], non_blocking=True)
+        res = run_slabs([part], ex, args.steps, cn)
+        out_h.copy_(part.owned(res[0][2]))
+        torch.cuda.synchronize()
+        tw = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        h2d = sum(h.numel() * h.element_size() for h in host)
+        e2e = {"value": nint * args.steps / float(tw.item()), "unit": "grid-point updates/s",
+               "h2d_bytes_per_step": int(h2d / args.steps),
+               "d2h_bytes_per_step": int(out_h.numel() * 8 / args.steps),
+               "note": "per rank: slab inputs from pinned host buffers, the sharded march, "
+                       "owned planes back to the host; max over ranks"}
+    clocks = clk.summary()
+    if rank == 0:
+        rng = slab_ranges(c.n, world)
+        line = {
+            "metric": "LOD grid-point updates/s (fp64)",
+            "value": value,
+            "unit": "grid-point updates/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": warm,
+            "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded generator, configs.py)",
+            "config": {"workload": c.name, "grid": [c.n] * 3, "atoms": c.n_atoms, "h": c.h,
+                       "variant": c.variant, "dt": c.dt, "interior_nodes": nint,
+                       "parallelism": f"axis-0 slabs x{world} (partitioned solve, NCCL "
+                                      "all-gather of chunk end rows)",
+                       "slab_planes": [b - a for a, b in rng],
+                       "l2": "slabs >> L2, no flush", "assembly_s": round(t_asm, 3)},
+            "roofline": {"bound": "hbm", "achieved": BYTES_LOD * local_nodes /
+                         (ms_max / args.steps / 1e3) / 1e9, "peak": peaks()[0],
+                         "unit": "GB/s", "traffic": None,
+                         "note": "rank-0 step bytes (48 B/owned node) / step time"},
+            "cpu_baseline": None,
+            "e2e": e2e,
+            "gpu_launches": (7 if cn else 5) * args.steps,
+            "clocks": clocks,
+        }
+        line["roofline"]["frac"] = line["roofline"]["achieved"] / line["roofline"]["peak"]
+        print(json.dumps(line), flush=True)
+    part.close()
+    dist.destroy_process_group()
 
 
 def reference_arm(args, world, rank):

@@ -562,7 +562,8 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 4 : (LB * kSeg
 
     // Phase 4: reconstruct the inner rows, separator = t; sparse source epilogue (LODIE1).
     if (a.dbg == 4) { w0[0] = t + tm; } else
-    seg_finish<S, LB>(a, Tv, r, tm, t, w0);
+    if (!a.ends || seg == 0 || seg == (m - 1) / S)  // ends-only: rows 1 and m
+      seg_finish<S, LB>(a, Tv, r, tm, t, w0);
     if (i0 + S - 1 < m) W[(i0 + S) * LB + lane] = t;
     if (a.epi == EPI_SRC && cmask)
       charged_fixup(cmask, a.epi_coef, [&](int j) { return w0 + j * LB; }, rho_row);
