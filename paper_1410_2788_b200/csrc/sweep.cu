@@ -333,9 +333,22 @@ __host__ __device__ constexpr int strided_rows() {
   return P * S + 2;
 }
 
-template <int LB>
+// Row stride (doubles) of one line in the shared tile of a row-tile launch (axis 2): room
+// for rows 0..NR-1 plus one leading slot so that row 1 (global k = 1, 256-byte aligned) is
+// 16-byte aligned, rounded to 2 mod 4 (2-way bank aliasing at most across lines).
+template <int S, int P>
+__host__ __device__ constexpr int rt_stride() {
+  return (((P * S + 2 + 1) + 3) & ~3) + 2;
+}
+
+template <int LB, bool RT>
+__host__ __device__ constexpr size_t tile_doubles(int S, int kSegS) {
+  return RT ? (size_t)LB * ((((kSegS * S + 3) + 3) & ~3) + 2) : (size_t)(kSegS * S + 2) * LB;
+}
+
+template <int LB, bool RT>
 __host__ __device__ constexpr size_t strided_smem(int S, int kSegS, bool needY) {
-  return sizeof(double) * (kTabDoubles + kSegS * kSegS + (needY ? 2 : 1) * (size_t)(kSegS * S + 2) * LB +
+  return sizeof(double) * (kTabDoubles + kSegS * kSegS + (needY ? 2 : 1) * tile_doubles<LB, RT>(S, kSegS) +
                            4 * LB * kSegS) +
          sizeof(unsigned long long) * 2 * kSegS * LB;
 }
@@ -365,11 +378,20 @@ __device__ __forceinline__ void charged_fixup(unsigned cmask, double coef, Slot 
   }
 }
 
-template <int S, int kSegS, bool CN, int LB>
-__global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 4 : (LB * kSegS <= 256 ? 3 : 2))
+// One block = LB lines x kSegS segments (thread (lane, seg) = segment seg of line lane).
+//   RT = false (axes 0, 1): the LB lines are adjacent k columns; the tile is stored row-major
+//        W[p][l] and staged / stored in 16-byte chunks of adjacent columns;
+//   RT = true  (axis 2, "row tiles"): the LB lines are adjacent j rows, each contiguous in
+//        global memory; the tile is stored line-major W[l][p] (stride rt_stride) and staged /
+//        stored as contiguous rows.
+// Block (x = column / row group, y = outer index).
+template <int S, int kSegS, bool CN, int LB, bool RT>
+__global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSegS <= 256 ? 3 : 2))
     k_sweep_strided(const SweepArgs a, const int axis) {
   extern __shared__ double sm[];
   constexpr int NT = LB * kSegS, NR = strided_rows<S, kSegS>();
+  constexpr int RS = rt_stride<S, kSegS>();
+  constexpr int WS = RT ? 1 : LB;  // shared-memory step between consecutive rows of a line
   constexpr int CPR = LB / 2, RPP = NT / CPR;  // 16-byte chunks per row, rows per pass
   // divergence flag: issue the load now, decide after staging
   const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
@@ -377,91 +399,131 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 4 : (LB * kSeg
   const int tid = seg * LB + lane;
   const Layout& L = a.L;
   const int m = a.m, nl = m + 2;
-  const int k0 = 1 + blockIdx.x * LB;
+  const int c0 = 1 + blockIdx.x * LB;  // first line of the tile (k for RT=false, j for RT)
   const int outer = 1 + blockIdx.y;
-  const int ncols = min(LB, L.n2 - 1 - k0);  // active columns in this tile
-  const int K = L.n2 - 2;
+  const int K = (RT ? L.n1 : L.n2) - 2;  // lines per outer index
+  const int ncols = min(LB, K + 1 - c0);  // active lines in this tile
+  // global offset of row p of tile line l: lb(l) + p * gs
   long long base;
   int stride;
-  if (axis == 0) {
-    base = L.at(0, outer, k0);
+  if (RT) {
+    base = L.at(outer, c0, 0);
+    stride = 1;
+  } else if (axis == 0) {
+    base = L.at(0, outer, c0);
     stride = (int)L.s0;
   } else {
-    base = L.at(outer, 0, k0);
+    base = L.at(outer, 0, c0);
     stride = (int)L.pitch;
   }
+  auto lb = [&](int l) { return base + (RT ? (long long)l * L.pitch : (long long)l); };
+  auto sidx = [&](int p, int l) { return RT ? l * RS + 1 + p : p * LB + l; };
   const int needY = epi_needs(a.epi);
+  constexpr int TD = RT ? LB * RS : NR * LB;
   double* T = sm;
   double* Mi = T + kTabDoubles;
   double* W = Mi + kSegS * kSegS;
-  double* Yt = W + NR * LB;
-  double* X = Yt + (needY ? NR * LB : 0);
+  double* Yt = W + TD;
+  double* X = Yt + (needY ? TD : 0);
   unsigned long long* D = reinterpret_cast<unsigned long long*>(X + 4 * NT);
-  const double* gsrc = a.src + base;
-  const double* gy = (needY == 1 ? a.src : a.acc) + base;
-  const double* grho = a.rho + base;
+  const double* gy_all = needY == 1 ? a.src : a.acc;
 
   // Phase 1: asynchronous staging of the field (+ epilogue operand), descriptors, tables.
-  if (a.dbg < 2) {
+  if (RT) {
+    // rows 1..m+1 of each line in 16-byte chunks (row 1 is 256-byte aligned), row 0 alone
+    const int nch = (m + 1) / 2;  // full chunks; an odd last row goes alone
+    for (int l = 0; l < ncols; ++l) {
+      const double* g = a.src + lb(l);
+      double* w = W + l * RS + 1;
+      for (int c = tid; c < nch; c += NT) cp_async16(w + 1 + 2 * c, g + 1 + 2 * c);
+      if (needY) {
+        const double* gy = gy_all + lb(l);
+        double* y = Yt + l * RS + 1;
+        for (int c = tid; c < nch; c += NT) cp_async16(y + 1 + 2 * c, gy + 1 + 2 * c);
+      }
+    }
+    if (tid < ncols) {
+      cp_async8(W + tid * RS + 1, a.src + lb(tid));
+      if ((m + 1) & 1) cp_async8(W + tid * RS + 1 + m + 1, a.src + lb(tid) + m + 1);
+      if (needY) {
+        cp_async8(Yt + tid * RS + 1, gy_all + lb(tid));
+        if ((m + 1) & 1) cp_async8(Yt + tid * RS + 1 + m + 1, gy_all + lb(tid) + m + 1);
+      }
+    }
+    for (int c = tid; c < LB * (NR - nl); c += NT) {  // rows past the far face
+      const int l = c / (NR - nl), p = nl + c % (NR - nl);
+      W[sidx(p, l)] = 0.0;
+    }
+  } else {
     const int q = (tid % CPR) * 2, p0 = tid / CPR;
     const long long gstep = (long long)RPP * stride;
-    const double* g = gsrc + p0 * (long long)stride + q;
+    const double* g = a.src + base + p0 * (long long)stride + q;
     double* w = W + p0 * LB + q;
 #pragma unroll 4
     for (int p = p0; p < nl; p += RPP, g += gstep, w += RPP * LB) cp_async16(w, g);
     if (needY) {
-      const double* gyp = gy + p0 * (long long)stride + q;
+      const double* gyp = gy_all + base + p0 * (long long)stride + q;
       double* yp = Yt + p0 * LB + q;
 #pragma unroll 4
       for (int p = p0; p < nl; p += RPP, gyp += gstep, yp += RPP * LB) cp_async16(yp, gyp);
     }
+    for (int c = nl * LB + tid; c < NR * LB; c += NT) W[c] = 0.0;  // rows past the far face
   }
-  cp_async16(D + 2 * tid, a.desc + 2 * (((long long)(outer - 1) * kSegS + seg) * K + (k0 - 1 + lane)));
+  cp_async16(D + 2 * tid, a.desc + 2 * (((long long)(outer - 1) * kSegS + seg) * K + (c0 - 1 + lane)));
   for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
   if (a.static_ok)
     for (int c = tid; c < kSegS * kSegS / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
-  for (int c = nl * LB + tid; c < NR * LB; c += NT) W[c] = 0.0;  // rows past the far face
   cp_async_wait_all();
   __syncthreads();
   if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
 
   const int i0 = seg * S;
-  // columns past the last interior one read unrelated descriptor words: neutralise them
+  // lines past the last interior one read unrelated descriptor words: neutralise them
   const bool act = lane < ncols;
   const unsigned long long amask = act ? D[2 * tid] : 0ull;
   const unsigned cmask = act ? (unsigned)(D[2 * tid + 1] >> 32) : 0u;
-  const double* rrow = grho + (i0 + 1) * stride + lane;
-  auto rho_row = [&](int j) { return rrow + j * stride; };
-  double* w0 = W + (i0 + 1) * LB + lane;
+  const long long gl = lb(lane);  // this thread's line
+  const double* rrow = a.rho + gl + (long long)(i0 + 1) * stride;
+  auto rho_row = [&](int j) { return rrow + (long long)j * stride; };
+  double* w0 = W + sidx(i0 + 1, lane);
   if (a.pro == PRO_FLOW) {  // flow stage: interior rows transformed, faces = Dirichlet data
     if (tid < 2 * LB) {
-      const int p = tid < LB ? 0 : nl - 1, l = tid % LB;
-      W[p * LB + l] = a.bnd[base + (p == 0 ? 0ll : a.hi_off) + l];
+      const int l = tid % LB;
+      const bool hi = tid >= LB;
+      if (l < ncols) W[sidx(hi ? nl - 1 : 0, l)] = a.bnd[lb(l) + (hi ? a.hi_off : 0ll)];
     }
-    const int l = tid % LB;
-    for (int p = 1 + tid / LB; p < nl - 1; p += NT / LB) {
-      const int sg = (p - 1) / S;
-      const uint32_t c = node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
-      W[p * LB + l] = flow_at(a, W[p * LB + l], c, a.pm);
+    if (RT) {
+      for (int l = 0; l < ncols; ++l)
+        for (int p = 1 + tid; p < nl - 1; p += NT) {
+          const int sg = (p - 1) / S;
+          const uint32_t c = node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
+          W[sidx(p, l)] = flow_at(a, W[sidx(p, l)], c, a.pm);
+        }
+    } else {
+      const int l = tid % LB;
+      for (int p = 1 + tid / LB; p < nl - 1; p += NT / LB) {
+        const int sg = (p - 1) / S;
+        const uint32_t c = node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
+        W[p * LB + l] = flow_at(a, W[p * LB + l], c, a.pm);
+      }
     }
     __syncthreads();
   } else if (a.pro == PRO_SRC) {  // w = u + dta*rho at the charged nodes only
-    if (cmask) charged_fixup(cmask, a.pro_coef, [&](int j) { return w0 + j * LB; }, rho_row);
+    if (cmask) charged_fixup(cmask, a.pro_coef, [&](int j) { return w0 + j * WS; }, rho_row);
     __syncthreads();
   }
 
-  if (a.dbg == 1) goto store;
   {
     // Phase 2: rhs of the own rows (registers), local elimination.
     const bool active = lane < ncols;
     double r[S];
     {
-      const double* wrow = W + (i0 + 1) * LB + lane;
+      const double* wrow = w0;
 #pragma unroll
       for (int j = 0; j < S; ++j) {
-        const double wc = wrow[j * LB];
+        const double wc = wrow[j * WS];
         r[j] = CN ? cn_term(a, (uint32_t)(amask >> j) & 1u, (uint32_t)(amask >> (j + 1)) & 1u,
-                            wrow[(j - 1) * LB], wc, wrow[(j + 1) * LB])
+                            wrow[(j - 1) * WS], wc, wrow[(j + 1) * WS])
                   : wc;
       }
     }
@@ -471,37 +533,27 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 4 : (LB * kSeg
         if ((cmask >> j) & 1u) r[j] = __dadd_rn(r[j], __dmul_rn(a.extra, *rho_row(j)));
     }
     if (seg == 0 && active)
-      r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], a.bnd[base + lane]));
-    if (seg == (m - 1) / S && active)
-      fold_high<S>(a, r, amask, a.bnd[base + a.hi_off + lane]);
+      r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], a.bnd[gl]));
+    if (seg == (m - 1) / S && active) fold_high<S>(a, r, amask, a.bnd[gl + a.hi_off]);
     // clean tile: every line of the tile is one dielectric (palette 0) end to end
     const bool clean = __syncthreads_and(!active || eps_bits(amask, S) == 0ull) && a.static_ok;
 
     SegOut o;
-    const double* Tv = nullptr;
-    if (a.dbg == 4) {
-      o.yF = r[0]; o.aF = r[1]; o.bF = r[2]; o.yL = r[3]; o.aL = r[4]; o.bL = r[5];
-      o.as = r[6]; o.bs = 1.0; o.cs = r[7]; o.rs = r[8];
-    } else {
-      Tv = seg_eliminate<S>(a, r, amask, i0, seg == 0, T, o);
-    }
+    const double* Tv = seg_eliminate<S>(a, r, amask, i0, seg == 0, T, o);
 
-    // Phase 3: reduced system over the 32 separators of each line.
+    // Phase 3: reduced system over the separators of each line.
     double* sA = X;
     double* sB = X + NT;
     double* sC = X + 2 * NT;
     double* sR = X + 3 * NT;
     double t, tm;
-    if (a.dbg == 3) {
-      t = o.yF + o.rs;
-      tm = o.yL;
-    } else if (clean) {  // static inverse: one exchange of y_F, one of R, then two dot products
+    if (clean) {  // static inverse: one exchange of y_F, one of R, then two dot products
       sA[tid] = o.yF;
       __syncthreads();
       const double yFn = (seg + 1 < kSegS) ? sA[tid + LB] : 0.0;
       sR[tid] = o.rs - o.as * o.yL - o.cs * yFn;
       __syncthreads();
-      const int k1 = seg > 0 ? seg - 1 : 0;  // transposed inverse: column q at Mi[q*32]
+      const int k1 = seg > 0 ? seg - 1 : 0;  // transposed inverse: column q at Mi[q*P]
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll 8
       for (int q = 0; q < kSegS; ++q) {
@@ -561,36 +613,67 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 4 : (LB * kSeg
     }
 
     // Phase 4: reconstruct the inner rows, separator = t; sparse source epilogue (LODIE1).
-    if (a.dbg == 4) { w0[0] = t + tm; } else
     if (!a.ends || seg == 0 || seg == (m - 1) / S)  // ends-only: rows 1 and m
-      seg_finish<S, LB>(a, Tv, r, tm, t, w0);
-    if (i0 + S - 1 < m) W[(i0 + S) * LB + lane] = t;
+      seg_finish<S, WS>(a, Tv, r, tm, t, w0);
+    if (i0 + S - 1 < m) w0[(S - 1) * WS] = t;
     if (a.epi == EPI_SRC && cmask)
-      charged_fixup(cmask, a.epi_coef, [&](int j) { return w0 + j * LB; }, rho_row);
+      charged_fixup(cmask, a.epi_coef, [&](int j) { return w0 + j * WS; }, rho_row);
     __syncthreads();
   }
-store:
-  if (a.ends) {  // slab phase A: only the chunk's end rows leave the block
+  if (a.ends) {  // slab phase A (axis 0): only the chunk's end rows leave the block
     if (tid < 2 * LB) {
       const int l = tid % LB;
       const bool hi = tid >= LB;
-      if (l < ncols) a.ends[base + (hi ? a.ends_off : 0ll) + l] = W[(hi ? m : 1) * LB + l];
+      if (l < ncols) a.ends[lb(l) + (hi ? a.ends_off : 0ll)] = W[sidx(hi ? m : 1, l)];
     }
     return;
   }
   // Phase 5: epilogue + coalesced store of the interior rows.
   {
     bool bad = false;
-    double* gdst = a.dst + base;
     const int epi = a.epi;
-    if ((epi == EPI_STORE || epi == EPI_SRC || epi == EPI_MAOS0) && !a.check) {
+    auto solute = [&](int p, int l) {
+      const int sg = (p - 1) / S;
+      return node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
+    };
+    const bool plain = (epi == EPI_STORE || epi == EPI_SRC || epi == EPI_MAOS0) && !a.check;
+    // per-node epilogue loop (one rolled copy per epilogue kind)
+    auto loop = [&](auto f) {
+      if (RT) {
+        for (int l = 0; l < ncols; ++l) {
+          double* g = a.dst + lb(l);
+          for (int p = 1 + tid; p <= m; p += NT) {
+            const double x = f(sidx(p, l), p, l);
+            g[p] = x;
+            bad |= is_bad(x, a.thr);
+          }
+        }
+      } else {
+        const int l = tid % LB;
+        if (l >= ncols) return;
+        double* g = a.dst + base + l;
+        for (int p = 1 + tid / LB; p <= m; p += NT / LB) {
+          const double x = f(p * LB + l, p, l);
+          g[(long long)p * stride] = x;
+          bad |= is_bad(x, a.thr);
+        }
+      }
+    };
+    if (plain && RT) {  // rows 1..m: 16-byte chunks (1,2), (3,4), ...; an odd last row alone
+      const int nch = m / 2;
+      for (int l = 0; l < ncols; ++l) {
+        double* g = a.dst + lb(l) + 1;
+        const double* w = W + l * RS + 2;
+        for (int c = tid; c < nch; c += NT)
+          *reinterpret_cast<double2*>(g + 2 * c) = *reinterpret_cast<const double2*>(w + 2 * c);
+        if ((m & 1) && tid == 0) g[m - 1] = w[m - 1];
+      }
+    } else if (plain) {
       const int q = (tid % CPR) * 2, p0 = 1 + tid / CPR;  // 16-byte chunks
       const long long gstep = (long long)RPP * stride;
-      double* g = gdst + p0 * (long long)stride + q;
+      double* g = a.dst + base + p0 * (long long)stride + q;
       const double* w = W + p0 * LB + q;
-      if (a.dbg >= 2) {
-        if (W[tid] == 12345.678) gdst[0] = 0.0;  // keep the solve alive
-      } else if (q + 1 < ncols) {
+      if (q + 1 < ncols) {
 #pragma unroll 4
         for (int p = p0; p <= m; p += RPP, g += gstep, w += RPP * LB)
           *reinterpret_cast<double2*>(g) = *reinterpret_cast<const double2*>(w);
@@ -598,30 +681,24 @@ store:
         for (int p = p0; p <= m; p += RPP, g += gstep, w += RPP * LB) *g = *w;
       }
     } else {
-      const int l = tid % LB;
-      auto loop = [&](auto f) {
-        if (l >= ncols) return;
-        for (int p = 1 + tid / LB; p <= m; p += NT / LB) {
-          const int c = p * LB + l;
-          const double x = f(c, p);
-          gdst[(long long)p * stride + l] = x;
-          bad |= is_bad(x, a.thr);
-        }
-      };
-      auto solute = [&](int p) {
-        const int sg = (p - 1) / S;
-        return node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
-      };
       switch (epi) {
-        case EPI_FLOW: loop([&](int c, int p) { return flow_at(a, W[c], solute(p), 1.0); }); break;
+        case EPI_FLOW:
+          loop([&](int c, int p, int l) { return flow_at(a, W[c], solute(p, l), 1.0); });
+          break;
         case EPI_AOS0:
-          loop([&](int c, int p) { return __dadd_rn(flow_at(a, Yt[c], solute(p), a.pm), W[c]); });
+          loop([&](int c, int p, int l) {
+            return __dadd_rn(flow_at(a, Yt[c], solute(p, l), a.pm), W[c]);
+          });
           break;
         case EPI_AOS1:
-        case EPI_MAOS1: loop([&](int c, int) { return __dadd_rn(Yt[c], W[c]); }); break;
-        case EPI_AOS2: loop([&](int c, int) { return __dmul_rn(0.25, __dadd_rn(Yt[c], W[c])); }); break;
-        case EPI_MAOS2: loop([&](int c, int) { return __ddiv_rn(__dadd_rn(Yt[c], W[c]), 3.0); }); break;
-        default: loop([&](int c, int) { return W[c]; }); break;
+        case EPI_MAOS1: loop([&](int c, int, int) { return __dadd_rn(Yt[c], W[c]); }); break;
+        case EPI_AOS2:
+          loop([&](int c, int, int) { return __dmul_rn(0.25, __dadd_rn(Yt[c], W[c])); });
+          break;
+        case EPI_MAOS2:
+          loop([&](int c, int, int) { return __ddiv_rn(__dadd_rn(Yt[c], W[c]), 3.0); });
+          break;
+        default: loop([&](int c, int, int) { return W[c]; }); break;
       }
     }
     if (a.check) {
@@ -867,31 +944,32 @@ __global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const i
 //   word 0: bit j = eps bit (axis) of the node of row i0+j, j = 0..S (zero past node m+1)
 //   word 1: bits 0..S-1 solute bit of the nodes of rows i0..i0+S-1; bits 32.. charged bits
 // Layout: strided axes ((outer-1)*32 + seg)*K + (k-1); contiguous axis line*32 + seg.
-__global__ void k_build_desc(const Layout L, int axis, int S, int P,
+__global__ void k_build_desc(const Layout L, int axis, int S, int P, int rows,
                              const uint8_t* __restrict__ codes,
                              unsigned long long* __restrict__ desc) {
   const int m = (axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2)) - 2;
+  const bool contig = axis == 2 && !rows;
+  const int K = (axis == 2 ? L.n1 : L.n2) - 2;  // lines per outer index (tile layouts)
   long long nseg;
-  if (axis == 2) nseg = (long long)(L.n0 - 2) * (L.n1 - 2) * kSeg;
-  else nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * (L.n2 - 2);
+  if (contig) nseg = (long long)(L.n0 - 2) * (L.n1 - 2) * kSeg;
+  else nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * K;
   const int sh = 1 + axis;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nseg;
        t += (long long)gridDim.x * blockDim.x) {
     long long base, stride;
     int seg;
-    if (axis == 2) {
+    if (contig) {
       const long long line = t / kSeg;
       seg = (int)(t % kSeg);
       base = L.at(1 + (int)(line / (L.n1 - 2)), 1 + (int)(line % (L.n1 - 2)), 0);
       stride = 1;
     } else {
-      const int K = L.n2 - 2;
-      const int k = 1 + (int)(t % K);
+      const int c = 1 + (int)(t % K);
       const long long os = t / K;
       seg = (int)(os % P);
       const int outer = 1 + (int)(os / P);
-      base = axis == 0 ? L.at(0, outer, k) : L.at(outer, 0, k);
-      stride = axis == 0 ? L.s0 : L.pitch;
+      base = axis == 0 ? L.at(0, outer, c) : (axis == 1 ? L.at(outer, 0, c) : L.at(outer, c, 0));
+      stride = axis == 0 ? L.s0 : (axis == 1 ? L.pitch : 1);
     }
     const int i0 = seg * S;
     unsigned long long w0 = 0, w1 = 0;
@@ -915,18 +993,20 @@ __global__ void k_build_desc(const Layout L, int axis, int S, int P,
 // recurrences as the uniform tables, per-row coefficients) and read like a table by the
 // sweeps.  Pass 0 counts, pass 1 assigns slots (atomic; values do not depend on the slot)
 // and writes factors + slot into descriptor word 0.
-__global__ void k_seg_factors(const Layout L, int axis, int S, int P, AxisCoef co, int pass,
-                              unsigned long long* __restrict__ desc, int* __restrict__ counter,
-                              double* __restrict__ gfac) {
+__global__ void k_seg_factors(const Layout L, int axis, int S, int P, int rows, AxisCoef co,
+                              int pass, unsigned long long* __restrict__ desc,
+                              int* __restrict__ counter, double* __restrict__ gfac) {
   const int m = (axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2)) - 2;
+  const bool contig = axis == 2 && !rows;
+  const int K = (axis == 2 ? L.n1 : L.n2) - 2;
   long long nseg;
-  if (axis == 2) nseg = (long long)(L.n0 - 2) * (L.n1 - 2) * P;
-  else nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * (L.n2 - 2);
+  if (contig) nseg = (long long)(L.n0 - 2) * (L.n1 - 2) * P;
+  else nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * K;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nseg;
        t += (long long)gridDim.x * blockDim.x) {
     int seg;
-    if (axis == 2) seg = (int)(t % P);
-    else seg = (int)((t / (L.n2 - 2)) % P);
+    if (contig) seg = (int)(t % P);
+    else seg = (int)((t / K) % P);
     const int i0 = seg * S, first = seg == 0;
     const unsigned long long w0 = desc[2 * t];
     const unsigned long long eb = eps_bits(w0, S);
@@ -976,7 +1056,9 @@ __global__ void k_seg_factors(const Layout L, int axis, int S, int P, AxisCoef c
 // ---------------------------------------------------------------------------------------
 // Host-side launch helpers.
 
-static int seg_S(int m, int P) {
+static int seg_S(int m, int P, bool tile) {
+  if (tile && P == 16) return m <= 256 ? 16 : 0;  // tile launches: S = 16 (and 32) only
+  if (tile && P == 32) return m <= 512 ? 16 : (m <= 1024 ? 32 : 0);
   const int opts[] = {2, 3, 4, 6, 8, 12, 16, 24, 32};
   for (int s : opts)
     if (P * s >= m) return s;
@@ -984,29 +1066,40 @@ static int seg_S(int m, int P) {
 }
 // Strided axes: segments of ~16 rows (registers and occupancy balance, measured); the
 // contiguous axis always uses the 32 lanes of a warp.
+// Axis 2 runs as row tiles of the tile kernel unless PBG_AXIS2=contig (warp-per-row kernel).
+static bool axis2_rows() {
+  static const bool rows = [] {
+    const char* e = getenv("PBG_AXIS2");
+    return !(e && strcmp(e, "contig") == 0);
+  }();
+  return rows;
+}
+
 static int seg_P(int axis, int m) {
-  if (axis == 2) return kSeg;
+  if (axis == 2 && !axis2_rows()) return kSeg;
   return m <= 128 ? 8 : (m <= 256 ? 16 : 32);
 }
 
-template <int S, int P, bool CN, int LB>
+template <int S, int P, bool CN, int LB, bool RT>
 static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
   const int nouter = (axis == 0 ? a.L.n1 : a.L.n0) - 2;
-  dim3 grid((a.L.n2 - 2 + LB - 1) / LB, nouter);
+  const int nlines = (RT ? a.L.n1 : a.L.n2) - 2;
+  dim3 grid((nlines + LB - 1) / LB, nouter);
   dim3 block(LB, P);
-  const size_t smem = strided_smem<LB>(S, P, epi_needs(a.epi) != 0);
+  const size_t smem = strided_smem<LB, RT>(S, P, epi_needs(a.epi) != 0);
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_sweep_strided<S, P, CN, LB>,
+    cudaFuncSetAttribute(k_sweep_strided<S, P, CN, LB, RT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_sweep_strided<S, P, CN, LB><<<grid, block, smem, st>>>(a, axis);
+  k_sweep_strided<S, P, CN, LB, RT><<<grid, block, smem, st>>>(a, axis);
 }
 
 // Axis 0 rows are one field plane apart (MB strides): 128-byte row chunks keep DRAM pages
 // and TLB entries busy (64-byte chunks run at ~55% of copy bandwidth there, measured).
 template <int S, int P, bool CN>
 static void launch_strided_SC(const SweepArgs& a, int axis, cudaStream_t st) {
-  if (axis == 0) launch_strided_SCL<S, P, CN, 16>(a, axis, st);
-  else launch_strided_SCL<S, P, CN, 8>(a, axis, st);
+  if (axis == 0) launch_strided_SCL<S, P, CN, 16, false>(a, axis, st);
+  else if (axis == 1) launch_strided_SCL<S, P, CN, 8, false>(a, axis, st);
+  else launch_strided_SCL<S, P, CN, 8, true>(a, axis, st);
 }
 
 template <int S, int P>
@@ -1049,7 +1142,7 @@ static void launch_contig_S(const SweepArgs& a, cudaStream_t st) {
   }
 
 static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
-  const int P = seg_P(axis, a.m), S = seg_S(a.m, P);
+  const int P = seg_P(axis, a.m), S = seg_S(a.m, P, true);
   if (P == 8) {
 #define PBG_STRIDED8(S) launch_strided_SP<S, 8>(a, axis, st)
     PBG_DISPATCH_S(S, PBG_STRIDED8)
@@ -1069,7 +1162,7 @@ static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
 
 static int launch_contig(const SweepArgs& a, cudaStream_t st) {
 #define PBG_CONTIG(S) launch_contig_S<S>(a, st)
-  PBG_DISPATCH_S(seg_S(a.m, kSeg), PBG_CONTIG)
+  PBG_DISPATCH_S(seg_S(a.m, kSeg, false), PBG_CONTIG)
 #undef PBG_CONTIG
   PBG_LAUNCH_CHECK("k_sweep_contig");
   return PBG_OK;
@@ -1194,7 +1287,7 @@ static SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, 
   a.pro = PRO_NONE;
   a.epi = EPI_STORE;
   a.thr = INFINITY;
-  a.hi_off = (long long)(a.m + 1) * (axis == 0 ? a.L.s0 : a.L.pitch);
+  a.hi_off = (long long)(a.m + 1) * (axis == 0 ? a.L.s0 : (axis == 1 ? a.L.pitch : 1));
   return a;
 }
 
@@ -1206,14 +1299,14 @@ struct AxisAux {
 };
 
 static long long desc_segments(const Layout& L, int axis, int P) {
-  if (axis == 2) return (long long)(L.n0 - 2) * (L.n1 - 2) * kSeg;
-  return (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * (L.n2 - 2);
+  if (axis == 2 && !axis2_rows()) return (long long)(L.n0 - 2) * (L.n1 - 2) * kSeg;
+  return (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * ((axis == 2 ? L.n1 : L.n2) - 2);
 }
 
 static int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
                         cudaStream_t st) {
   const int P = seg_P(axis, a.m);
-  const int S = seg_S(a.m, P);
+  const int S = seg_S(a.m, P, !(axis == 2 && !axis2_rows()));
   if (S < 2) return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 768)");
   std::vector<double> host(kTabDoubles + kSeg * kSeg, 0.0);
   make_tables(a.co, S, host.data());
@@ -1226,12 +1319,14 @@ static int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& a
   const long long nseg = desc_segments(a.L, axis, P);
   // +64 words of slack: tiles past the last interior column read (unused) descriptors
   PBG_CUDA(cudaMallocAsync(&aux.desc, (2 * nseg + 64) * sizeof(unsigned long long), st));
-  k_build_desc<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, codes, aux.desc);
+  k_build_desc<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, axis2_rows() ? 1 : 0, codes,
+                                         aux.desc);
   PBG_LAUNCH_CHECK("k_build_desc");
   int* counter = nullptr;
   PBG_CUDA(cudaMallocAsync(&counter, sizeof(int), st));
   PBG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-  k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, a.co, 0, aux.desc, counter, nullptr);
+  k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, axis2_rows() ? 1 : 0, a.co, 0,
+                                          aux.desc, counter, nullptr);
   PBG_LAUNCH_CHECK("k_seg_factors");
   int ngen = 0;
   PBG_CUDA(cudaMemcpyAsync(&ngen, counter, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1239,8 +1334,8 @@ static int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& a
   PBG_CUDA(cudaMallocAsync(&aux.gfac, ((size_t)ngen + 1) * 5 * kTabRows * sizeof(double), st));
   if (ngen > 0) {
     PBG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-    k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, a.co, 1, aux.desc, counter,
-                                           aux.gfac);
+    k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, axis2_rows() ? 1 : 0, a.co, 1,
+                                           aux.desc, counter, aux.gfac);
     PBG_LAUNCH_CHECK("k_seg_factors");
   }
   PBG_CUDA(cudaFreeAsync(counter, st));
@@ -1261,7 +1356,7 @@ static void release_axis(AxisAux& aux, cudaStream_t st) {
 }
 
 static int launch_sweep(const SweepArgs& a, int axis, cudaStream_t st) {
-  return axis == 2 ? launch_contig(a, st) : launch_strided(a, axis, st);
+  return (axis == 2 && !axis2_rows()) ? launch_contig(a, st) : launch_strided(a, axis, st);
 }
 
 // Variant table (schemes.py:209-262).
