@@ -82,34 +82,35 @@ static __constant__ double kLogPoly[13] = {
     1.0 / 5.0,  1.0 / 3.0,  6.93147180369123816490e-01, 1.90821492927058770002e-10,
     1.4426950408889634, 1.41421356237309504880};
 
-// exp(w) for |w| <= 40: Cody-Waite reduction by ln 2, degree-12 Taylor polynomial on
-// |r| <= ln2/2 (truncation < 2e-16 relative), exponent added directly (no range checks).
+// exp(w) for |w| <= 40: Cody-Waite reduction by ln 2 (k by the 1.5*2^52 rounding trick, no
+// conversion instructions), degree-12 Taylor polynomial on |r| <= ln2/2 (truncation < 2e-16
+// relative), exponent added directly (no range checks).
 __device__ __forceinline__ double exp_small(double w) {
-  const double k = rint(w * kLogPoly[11]);
+  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  const double t = fma(w, kLogPoly[11], kMagic);
+  const double k = t - kMagic;
+  const int ki = __double2loint(t);  // k (two's complement in the low word)
   double r = fma(-k, kLogPoly[9], w);
   r = fma(-k, kLogPoly[10], r);
   double p = kExpPoly[0];
 #pragma unroll
   for (int q = 1; q < 13; ++q) p = fma(p, r, kExpPoly[q]);
-  return __longlong_as_double(__double_as_longlong(p) + ((long long)k << 52));
+  return __hiloint2double(__double2hiint(p) + (ki << 20), __double2loint(p));
 }
 
 // log(N / D) for positive normal N, D with one division: N = 2^eN mN, D = 2^eD mD,
-// mN/mD reduced into [1/sqrt2, sqrt2], log m = 2 atanh(s), s = (mN - mD)/(mN + mD),
-// |s| <= 0.1716, odd series to s^19 (truncation < 3e-17 relative).
+// mN/mD reduced into [1/sqrt2, sqrt2] (selects, no branches), log m = 2 atanh(s),
+// s = (mN - mD)/(mN + mD), |s| <= 0.1716, odd series to s^19 (truncation < 3e-17 relative).
 __device__ __forceinline__ double log_ratio(double N, double D) {
-  const long long bn = __double_as_longlong(N), bd = __double_as_longlong(D);
-  int k = (int)(bn >> 52) - (int)(bd >> 52);
-  const long long mant = 0x000FFFFFFFFFFFFFLL, one = 0x3FF0000000000000LL;
-  double mn = __longlong_as_double((bn & mant) | one);
-  double md = __longlong_as_double((bd & mant) | one);
-  if (mn > kLogPoly[12] * md) {
-    md += md;
-    k += 1;
-  } else if (md > kLogPoly[12] * mn) {
-    mn += mn;
-    k -= 1;
-  }
+  const int hn = __double2hiint(N), hd = __double2hiint(D);
+  int k = (hn >> 20) - (hd >> 20);
+  double mn = __hiloint2double((hn & 0x000FFFFF) | 0x3FF00000, __double2loint(N));
+  double md = __hiloint2double((hd & 0x000FFFFF) | 0x3FF00000, __double2loint(D));
+  const bool up = mn > kLogPoly[12] * md;
+  const bool dn = md > kLogPoly[12] * mn;
+  md = up ? md + md : md;
+  mn = dn ? mn + mn : mn;
+  k += (int)up - (int)dn;
   const double den = mn + md;
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(den));
@@ -128,17 +129,13 @@ __device__ __forceinline__ double log_ratio(double N, double D) {
 }
 
 // Same map as sinh_flow, evaluated as log(((1+d)E + (1-d)) / ((1-d)E + (1+d))), E = exp(w),
-// with the reduced-range exp/log above (~55 instructions instead of ~140 for the libm tanh /
-// atanh pair).  For |w| > 38, tanh(w/2) rounds to +-1 in fp64 and the reference returns
-// +-2*atanh(d) (`sat`, precomputed on the host).  Agrees with sinh_flow to ~1e-16 absolute.
+// with the reduced-range exp/log above.  For |w| > 38, tanh(w/2) rounds to +-1 in fp64 and
+// the reference returns +-2*atanh(d) (`sat`, precomputed on the host); decay >= 1 and NaN
+// pass w through.  Agrees with sinh_flow to ~1e-16 absolute.
 __device__ __forceinline__ double sinh_flow_fast(double w, double d, double sat, double pm) {
   double out;
-  if (d >= 1.0) {
-    out = w;
-  } else if (fabs(w) > 38.0) {
-    out = copysign(sat, w);
-  } else if (w != w) {
-    out = w;
+  if (d >= 1.0 || !(fabs(w) <= 38.0)) {  // rare: identity palette, saturation, NaN
+    out = (d >= 1.0 || w != w) ? w : copysign(sat, w);
   } else {
     const double E = exp_small(w);
     const double opd = 1.0 + d, omd = 1.0 - d;

@@ -149,6 +149,18 @@ __device__ __forceinline__ double flow_at(const SweepArgs& a, double w, uint32_t
   return sinh_flow_fast(w, s ? a.decay1 : a.decay0, s ? a.sat1 : a.sat0, pm);
 }
 
+// Palette constants of the flow held in registers across a loop.
+struct FlowPal {
+  double d0, d1, s0, s1;
+};
+__device__ __forceinline__ FlowPal flow_pal(const SweepArgs& a) {
+  return {a.decay0, a.decay1, a.sat0, a.sat1};
+}
+__device__ __forceinline__ double flow_at(const FlowPal& f, double w, uint32_t c, double pm) {
+  const bool s = (c & 1u) != 0;
+  return sinh_flow_fast(w, s ? f.d1 : f.d0, s ? f.s1 : f.s0, pm);
+}
+
 __device__ __forceinline__ double pro_val(const SweepArgs& a, double v, uint32_t c,
                                           const double* rho_at) {
   if (a.pro == PRO_FLOW) return flow_at(a, v, c, a.pm);
@@ -432,14 +444,17 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
   if (RT) {
     // rows 1..m+1 of each line in 16-byte chunks (row 1 is 256-byte aligned), row 0 alone
     const int nch = (m + 1) / 2;  // full chunks; an odd last row goes alone
-    for (int l = 0; l < ncols; ++l) {
-      const double* g = a.src + lb(l);
-      double* w = W + l * RS + 1;
-      for (int c = tid; c < nch; c += NT) cp_async16(w + 1 + 2 * c, g + 1 + 2 * c);
+    const long long gstep = L.pitch;
+    for (int c = tid; c < nch; c += NT) {
+      const double* g = a.src + base + 1 + 2 * c;
+      unsigned w = (unsigned)__cvta_generic_to_shared(W + 2 + 2 * c);
+      for (int l = 0; l < ncols; ++l, g += gstep, w += RS * 8)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(w), "l"(g));
       if (needY) {
-        const double* gy = gy_all + lb(l);
-        double* y = Yt + l * RS + 1;
-        for (int c = tid; c < nch; c += NT) cp_async16(y + 1 + 2 * c, gy + 1 + 2 * c);
+        const double* gy = gy_all + base + 1 + 2 * c;
+        unsigned y = (unsigned)__cvta_generic_to_shared(Yt + 2 + 2 * c);
+        for (int l = 0; l < ncols; ++l, gy += gstep, y += RS * 8)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(y), "l"(gy));
       }
     }
     if (tid < ncols) {
@@ -492,19 +507,22 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
       const bool hi = tid >= LB;
       if (l < ncols) W[sidx(hi ? nl - 1 : 0, l)] = a.bnd[lb(l) + (hi ? a.hi_off : 0ll)];
     }
+    const FlowPal fp = flow_pal(a);
+    const double pm = a.pm;
     if (RT) {
-      for (int l = 0; l < ncols; ++l)
-        for (int p = 1 + tid; p < nl - 1; p += NT) {
-          const int sg = (p - 1) / S;
-          const uint32_t c = node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
-          W[sidx(p, l)] = flow_at(a, W[sidx(p, l)], c, a.pm);
+      for (int p = 1 + tid; p < nl - 1; p += NT) {
+        const int sg = (p - 1) / S, sb = (p - 1) - sg * S;
+        for (int l = 0; l < ncols; ++l) {
+          const uint32_t c = node_bits(D[2 * (sg * LB + l) + 1], sb);
+          W[l * RS + 1 + p] = flow_at(fp, W[l * RS + 1 + p], c, pm);
         }
+      }
     } else {
       const int l = tid % LB;
       for (int p = 1 + tid / LB; p < nl - 1; p += NT / LB) {
         const int sg = (p - 1) / S;
         const uint32_t c = node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
-        W[p * LB + l] = flow_at(a, W[p * LB + l], c, a.pm);
+        W[p * LB + l] = flow_at(fp, W[p * LB + l], c, pm);
       }
     }
     __syncthreads();
@@ -632,19 +650,16 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
   {
     bool bad = false;
     const int epi = a.epi;
-    auto solute = [&](int p, int l) {
-      const int sg = (p - 1) / S;
-      return node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
-    };
     const bool plain = (epi == EPI_STORE || epi == EPI_SRC || epi == EPI_MAOS0) && !a.check;
     // per-node epilogue loop (one rolled copy per epilogue kind)
     auto loop = [&](auto f) {
       if (RT) {
-        for (int l = 0; l < ncols; ++l) {
-          double* g = a.dst + lb(l);
-          for (int p = 1 + tid; p <= m; p += NT) {
-            const double x = f(sidx(p, l), p, l);
-            g[p] = x;
+        for (int p = 1 + tid; p <= m; p += NT) {
+          double* g = a.dst + base + p;
+          const int sg = (p - 1) / S, sb = (p - 1) - sg * S;
+          for (int l = 0; l < ncols; ++l, g += L.pitch) {
+            const double x = f(l * RS + 1 + p, node_bits(D[2 * (sg * LB + l) + 1], sb));
+            *g = x;
             bad |= is_bad(x, a.thr);
           }
         }
@@ -653,7 +668,8 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
         if (l >= ncols) return;
         double* g = a.dst + base + l;
         for (int p = 1 + tid / LB; p <= m; p += NT / LB) {
-          const double x = f(p * LB + l, p, l);
+          const int sg = (p - 1) / S;
+          const double x = f(p * LB + l, node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S));
           g[(long long)p * stride] = x;
           bad |= is_bad(x, a.thr);
         }
@@ -661,13 +677,13 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
     };
     if (plain && RT) {  // rows 1..m: 16-byte chunks (1,2), (3,4), ...; an odd last row alone
       const int nch = m / 2;
-      for (int l = 0; l < ncols; ++l) {
-        double* g = a.dst + lb(l) + 1;
-        const double* w = W + l * RS + 2;
-        for (int c = tid; c < nch; c += NT)
-          *reinterpret_cast<double2*>(g + 2 * c) = *reinterpret_cast<const double2*>(w + 2 * c);
-        if ((m & 1) && tid == 0) g[m - 1] = w[m - 1];
+      for (int c = tid; c < nch; c += NT) {
+        double* g = a.dst + base + 1 + 2 * c;
+        const double* w = W + 2 + 2 * c;
+        for (int l = 0; l < ncols; ++l, g += L.pitch, w += RS)
+          *reinterpret_cast<double2*>(g) = *reinterpret_cast<const double2*>(w);
       }
+      if ((m & 1) && tid < ncols) a.dst[lb(tid) + m] = W[sidx(m, tid)];
     } else if (plain) {
       const int q = (tid % CPR) * 2, p0 = 1 + tid / CPR;  // 16-byte chunks
       const long long gstep = (long long)RPP * stride;
@@ -681,24 +697,24 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
         for (int p = p0; p <= m; p += RPP, g += gstep, w += RPP * LB) *g = *w;
       }
     } else {
+      const FlowPal fp = flow_pal(a);
+      const double pm = a.pm;
       switch (epi) {
         case EPI_FLOW:
-          loop([&](int c, int p, int l) { return flow_at(a, W[c], solute(p, l), 1.0); });
+          loop([&](int c, uint32_t b) { return flow_at(fp, W[c], b, 1.0); });
           break;
         case EPI_AOS0:
-          loop([&](int c, int p, int l) {
-            return __dadd_rn(flow_at(a, Yt[c], solute(p, l), a.pm), W[c]);
-          });
+          loop([&](int c, uint32_t b) { return __dadd_rn(flow_at(fp, Yt[c], b, pm), W[c]); });
           break;
         case EPI_AOS1:
-        case EPI_MAOS1: loop([&](int c, int, int) { return __dadd_rn(Yt[c], W[c]); }); break;
+        case EPI_MAOS1: loop([&](int c, uint32_t) { return __dadd_rn(Yt[c], W[c]); }); break;
         case EPI_AOS2:
-          loop([&](int c, int, int) { return __dmul_rn(0.25, __dadd_rn(Yt[c], W[c])); });
+          loop([&](int c, uint32_t) { return __dmul_rn(0.25, __dadd_rn(Yt[c], W[c])); });
           break;
         case EPI_MAOS2:
-          loop([&](int c, int, int) { return __ddiv_rn(__dadd_rn(Yt[c], W[c]), 3.0); });
+          loop([&](int c, uint32_t) { return __ddiv_rn(__dadd_rn(Yt[c], W[c]), 3.0); });
           break;
-        default: loop([&](int c, int, int) { return W[c]; }); break;
+        default: loop([&](int c, uint32_t) { return W[c]; }); break;
       }
     }
     if (a.check) {
