@@ -149,16 +149,11 @@ __device__ __forceinline__ double flow_at(const SweepArgs& a, double w, uint32_t
   return sinh_flow_fast(w, s ? a.decay1 : a.decay0, s ? a.sat1 : a.sat0, pm);
 }
 
-// Palette constants of the flow held in registers across a loop.
-struct FlowPal {
-  double d0, d1, s0, s1;
-};
-__device__ __forceinline__ FlowPal flow_pal(const SweepArgs& a) {
-  return {a.decay0, a.decay1, a.sat0, a.sat1};
-}
-__device__ __forceinline__ double flow_at(const FlowPal& f, double w, uint32_t c, double pm) {
-  const bool s = (c & 1u) != 0;
-  return sinh_flow_fast(w, s ? f.d1 : f.d0, s ? f.s1 : f.s0, pm);
+// Flow palette constants staged in shared memory as (decay, sat) pairs indexed by the solute
+// bit: one 16-byte load per node instead of predicated constant-bank selects.
+__device__ __forceinline__ double flow_sm(const double* FP, double w, uint32_t s, double pm) {
+  const double2 v = reinterpret_cast<const double2*>(FP)[s];
+  return sinh_flow_fast(w, v.x, v.y, pm);
 }
 
 __device__ __forceinline__ double pro_val(const SweepArgs& a, double v, uint32_t c,
@@ -362,7 +357,7 @@ template <int LB, bool RT>
 __host__ __device__ constexpr size_t strided_smem(int S, int kSegS, bool needY) {
   return sizeof(double) * (kTabDoubles + kSegS * kSegS + (needY ? 2 : 1) * tile_doubles<LB, RT>(S, kSegS) +
                            4 * LB * kSegS) +
-         sizeof(unsigned long long) * 2 * kSegS * LB;
+         sizeof(unsigned long long) * 2 * kSegS * LB + 4 * sizeof(double);
 }
 
 // High Dirichlet fold of row m-1 (tridiag.py:217): owned by segment (m-1)/S at row (m-1)%S,
@@ -438,7 +433,12 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
   double* Yt = W + TD;
   double* X = Yt + (needY ? TD : 0);
   unsigned long long* D = reinterpret_cast<unsigned long long*>(X + 4 * NT);
+  double* FP = reinterpret_cast<double*>(D + 2 * NT);  // flow palette (decay, sat) x 2
+  const uint32_t* D32 = reinterpret_cast<const uint32_t*>(D);
+  // solute bit of row p of tile line l (low word of descriptor word 1)
+  auto solute = [&](int sg, int sb, int l) { return (D32[4 * (sg * LB + l) + 2] >> sb) & 1u; };
   const double* gy_all = needY == 1 ? a.src : a.acc;
+  if (tid < 4) FP[tid] = tid == 0 ? a.decay0 : (tid == 1 ? a.sat0 : (tid == 2 ? a.decay1 : a.sat1));
 
   // Phase 1: asynchronous staging of the field (+ epilogue operand), descriptors, tables.
   if (RT) {
@@ -507,22 +507,18 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
       const bool hi = tid >= LB;
       if (l < ncols) W[sidx(hi ? nl - 1 : 0, l)] = a.bnd[lb(l) + (hi ? a.hi_off : 0ll)];
     }
-    const FlowPal fp = flow_pal(a);
     const double pm = a.pm;
     if (RT) {
       for (int p = 1 + tid; p < nl - 1; p += NT) {
         const int sg = (p - 1) / S, sb = (p - 1) - sg * S;
-        for (int l = 0; l < ncols; ++l) {
-          const uint32_t c = node_bits(D[2 * (sg * LB + l) + 1], sb);
-          W[l * RS + 1 + p] = flow_at(fp, W[l * RS + 1 + p], c, pm);
-        }
+        for (int l = 0; l < ncols; ++l)
+          W[l * RS + 1 + p] = flow_sm(FP, W[l * RS + 1 + p], solute(sg, sb, l), pm);
       }
     } else {
       const int l = tid % LB;
       for (int p = 1 + tid / LB; p < nl - 1; p += NT / LB) {
         const int sg = (p - 1) / S;
-        const uint32_t c = node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S);
-        W[p * LB + l] = flow_at(fp, W[p * LB + l], c, pm);
+        W[p * LB + l] = flow_sm(FP, W[p * LB + l], solute(sg, (p - 1) - sg * S, l), pm);
       }
     }
     __syncthreads();
@@ -658,7 +654,7 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
           double* g = a.dst + base + p;
           const int sg = (p - 1) / S, sb = (p - 1) - sg * S;
           for (int l = 0; l < ncols; ++l, g += L.pitch) {
-            const double x = f(l * RS + 1 + p, node_bits(D[2 * (sg * LB + l) + 1], sb));
+            const double x = f(l * RS + 1 + p, solute(sg, sb, l));
             *g = x;
             bad |= is_bad(x, a.thr);
           }
@@ -669,7 +665,7 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
         double* g = a.dst + base + l;
         for (int p = 1 + tid / LB; p <= m; p += NT / LB) {
           const int sg = (p - 1) / S;
-          const double x = f(p * LB + l, node_bits(D[2 * (sg * LB + l) + 1], (p - 1) - sg * S));
+          const double x = f(p * LB + l, solute(sg, (p - 1) - sg * S, l));
           g[(long long)p * stride] = x;
           bad |= is_bad(x, a.thr);
         }
@@ -697,14 +693,13 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
         for (int p = p0; p <= m; p += RPP, g += gstep, w += RPP * LB) *g = *w;
       }
     } else {
-      const FlowPal fp = flow_pal(a);
       const double pm = a.pm;
       switch (epi) {
         case EPI_FLOW:
-          loop([&](int c, uint32_t b) { return flow_at(fp, W[c], b, 1.0); });
+          loop([&](int c, uint32_t b) { return flow_sm(FP, W[c], b, 1.0); });
           break;
         case EPI_AOS0:
-          loop([&](int c, uint32_t b) { return __dadd_rn(flow_at(fp, Yt[c], b, pm), W[c]); });
+          loop([&](int c, uint32_t b) { return __dadd_rn(flow_sm(FP, Yt[c], b, pm), W[c]); });
           break;
         case EPI_AOS1:
         case EPI_MAOS1: loop([&](int c, uint32_t) { return __dadd_rn(Yt[c], W[c]); }); break;
