@@ -144,4 +144,69 @@ __device__ __forceinline__ double sinh_flow_fast(double w, double d, double sat,
   return pm != 1.0 ? pm * out : out;
 }
 
+// ---------------------------------------------------------------------------------------
+// Table-driven flow for the sweep kernels (tables staged in shared memory per block):
+//   exp:  w = (64 e + j) ln2/64 + r, |r| <= ln2/128, E = 2^e * T[j] * (1 + expm1_5(r))
+//   log:  x = 2^e m, m = c_i (1 + t) with c_i = 1/invc_i the centre of the i-th of 128
+//         mantissa bins, |t| <= 2^-8, log x = e ln2 - log(invc_i) + log1p_6(t)
+// log(N/D) = log N - log D: no division, absolute error ~3e-16 independent of w.
+constexpr int kExpTab = 64, kLogTab = 128;
+constexpr int kFlowTabDoubles = kExpTab + 2 * kLogTab;  // T[64] | (invc, -log invc)[128]
+
+static __constant__ double kFlowTabC[8] = {
+    92.332482616893656768,             // 64/ln2
+    6.93147180369123816490e-01 / 64.0,  // ln2/64, Cody-Waite high part (exact k*hi)
+    1.90821492927058770002e-10 / 64.0,  // ln2/64, low part
+    1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0,
+    6.93147180369123816490e-01, 1.90821492927058770002e-10};
+
+__device__ __forceinline__ double exp_tab(double w, const double* T) {
+  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  const double t = fma(w, kFlowTabC[0], kMagic);
+  const double kd = t - kMagic;
+  const int kk = __double2loint(t);
+  double r = fma(-kd, kFlowTabC[1], w);
+  r = fma(-kd, kFlowTabC[2], r);
+  double q = fma(r, kFlowTabC[3], kFlowTabC[4]);
+  q = fma(q, r, kFlowTabC[5]);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = q * r;  // expm1(r)
+  const double Tj = T[kk & (kExpTab - 1)];
+  const double E = fma(Tj, q, Tj);
+  return __hiloint2double(__double2hiint(E) + ((kk >> 6) << 20), __double2loint(E));
+}
+
+// log of the mantissa of a positive normal x; adds the unbiased exponent to e.
+__device__ __forceinline__ double log_mant(double x, int& e, const double2* LT) {
+  const int hx = __double2hiint(x);
+  e += (hx >> 20) - 1023;
+  const double m = __hiloint2double((hx & 0x000FFFFF) | 0x3FF00000, __double2loint(x));
+  const double2 c = LT[(hx >> 13) & (kLogTab - 1)];
+  const double t = fma(m, c.x, -1.0);
+  double p = fma(t, -1.0 / 6.0, 0.2);
+  p = fma(p, t, -0.25);
+  p = fma(p, t, 1.0 / 3.0);
+  p = fma(p, t, -0.5);
+  return c.y + fma(t * p, t, t);
+}
+
+__device__ __forceinline__ double sinh_flow_tab(double w, double d, double sat, double pm,
+                                                const double* FT) {
+  double out;
+  if (d >= 1.0 || !(fabs(w) <= 38.0)) {  // rare: identity palette, saturation, NaN
+    out = (d >= 1.0 || w != w) ? w : copysign(sat, w);
+  } else {
+    const double E = exp_tab(w, FT);
+    const double opd = 1.0 + d, omd = 1.0 - d;
+    int en = 0, ed = 0;
+    const double2* LT = reinterpret_cast<const double2*>(FT + kExpTab);
+    const double ln = log_mant(fma(opd, E, omd), en, LT);
+    const double ld = log_mant(fma(omd, E, opd), ed, LT);
+    const double kd = (double)(en - ed);
+    out = fma(kd, kFlowTabC[6], fma(kd, kFlowTabC[7], ln - ld));
+  }
+  return pm != 1.0 ? pm * out : out;
+}
+
 }  // namespace pbg

@@ -41,6 +41,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "pbg_internal.cuh"
@@ -113,6 +114,7 @@ struct SweepArgs {
   double thr;
   int check;
   int dbg;  // experiments only: 1 = stage + store (no solve)
+  const double* ftab;  // flow tables (kFlowTabDoubles), staged into shared memory
   // Strided axes: offset (from the line base) of the high boundary value in bnd; normally
   // plane m+1 of a field, one plane for the two-plane ghost buffers of the slab march.
   long long hi_off;
@@ -153,7 +155,7 @@ __device__ __forceinline__ double flow_at(const SweepArgs& a, double w, uint32_t
 // bit: one 16-byte load per node instead of predicated constant-bank selects.
 __device__ __forceinline__ double flow_sm(const double* FP, double w, uint32_t s, double pm) {
   const double2 v = reinterpret_cast<const double2*>(FP)[s];
-  return sinh_flow_fast(w, v.x, v.y, pm);
+  return sinh_flow_tab(w, v.x, v.y, pm, FP + 4);
 }
 
 __device__ __forceinline__ double pro_val(const SweepArgs& a, double v, uint32_t c,
@@ -357,7 +359,7 @@ template <int LB, bool RT>
 __host__ __device__ constexpr size_t strided_smem(int S, int kSegS, bool needY) {
   return sizeof(double) * (kTabDoubles + kSegS * kSegS + (needY ? 2 : 1) * tile_doubles<LB, RT>(S, kSegS) +
                            4 * LB * kSegS) +
-         sizeof(unsigned long long) * 2 * kSegS * LB + 4 * sizeof(double);
+         sizeof(unsigned long long) * 2 * kSegS * LB + (4 + kFlowTabDoubles) * sizeof(double);
 }
 
 // High Dirichlet fold of row m-1 (tridiag.py:217): owned by segment (m-1)/S at row (m-1)%S,
@@ -488,6 +490,8 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
   for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
   if (a.static_ok)
     for (int c = tid; c < kSegS * kSegS / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
+  if (a.pro == PRO_FLOW || a.epi == EPI_FLOW || a.epi == EPI_AOS0)
+    for (int c = tid; c < kFlowTabDoubles / 2; c += NT) cp_async16(FP + 4 + 2 * c, a.ftab + 2 * c);
   cp_async_wait_all();
   __syncthreads();
   if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
@@ -1287,6 +1291,30 @@ static void set_decays(SweepArgs& a, double d0, double d1) {
   a.sat1 = d1 < 1.0 ? 2.0 * std::atanh(d1) : 0.0;
 }
 
+// Flow tables (pbg_internal.cuh, sinh_flow_tab), one copy per device for the process.
+static const double* flow_tables() {
+  static std::mutex mu;
+  static double* dev[64] = {};
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!dev[d]) {
+    std::vector<double> h(kFlowTabDoubles);
+    for (int j = 0; j < kExpTab; ++j) h[j] = std::exp2((double)j / kExpTab);
+    for (int i = 0; i < kLogTab; ++i) {
+      const double invc = 1.0 / (1.0 + (i + 0.5) / kLogTab);
+      h[kExpTab + 2 * i] = invc;
+      h[kExpTab + 2 * i + 1] = -std::log(invc);
+    }
+    double* p = nullptr;
+    if (cudaMalloc(&p, h.size() * sizeof(double)) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+      return nullptr;
+    dev[d] = p;
+  }
+  return dev[d];
+}
+
 static SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, double factor) {
   SweepArgs a;
   memset(&a, 0, sizeof(a));
@@ -1299,6 +1327,7 @@ static SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, 
   a.epi = EPI_STORE;
   a.thr = INFINITY;
   a.hi_off = (long long)(a.m + 1) * (axis == 0 ? a.L.s0 : (axis == 1 ? a.L.pitch : 1));
+  a.ftab = flow_tables();
   return a;
 }
 
@@ -1367,6 +1396,7 @@ static void release_axis(AxisAux& aux, cudaStream_t st) {
 }
 
 static int launch_sweep(const SweepArgs& a, int axis, cudaStream_t st) {
+  if (!a.ftab) return fail(PBG_E_CUDA, "flow table allocation failed");
   return (axis == 2 && !axis2_rows()) ? launch_contig(a, st) : launch_strided(a, axis, st);
 }
 
