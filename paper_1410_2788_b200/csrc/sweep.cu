@@ -409,7 +409,9 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
   const Layout& L = a.L;
   const int m = a.m, nl = m + 2;
   const int c0 = 1 + blockIdx.x * LB;  // first line of the tile (k for RT=false, j for RT)
-  const int outer = 1 + blockIdx.y;
+  // Row tiles walk the planes in reverse: the axis-1 sweep before them wrote the last planes
+  // last, so those are still in L2 when this launch starts.
+  const int outer = RT ? (int)gridDim.y - (int)blockIdx.y : 1 + (int)blockIdx.y;
   const int K = (RT ? L.n1 : L.n2) - 2;  // lines per outer index
   const int ncols = min(LB, K + 1 - c0);  // active lines in this tile
   // global offset of row p of tile line l: lb(l) + p * gs
