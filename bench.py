@@ -4,7 +4,7 @@ Workload (BASELINE.json metric is quoted at 1/2/4/8 B200 on the sharded config):
 a 10,000-atom synthetic protein on a 513^3 grid (h = 0.3 A, eps 2/80, 0.15 M), LODIE2,
 dt = 0.5.  One bench "step" = one LODIE2 time step over the whole grid (flow + source +
 three implicit line sweeps).  Fields are 1.1 GB each (>> 126 MB L2), so no L2 flush is
-needed between steps.
+needed between steps (`--config c3`: 257^3, 142 MB fields, still larger than L2).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c3] [--impl ours|reference]
 
@@ -319,6 +319,7 @@ def main():
     ms_max = float(t.item())
     value = nint * args.steps * world / (ms_max / 1e3)
 
+    field_mb = p.grid.nx * p.grid.ny * dp.gs.pitch * 8 / 1e6
     per_ms, launches = profiled_kernels(d, min(args.steps, 20))
     dom = int(np.argmax(per_ms))
     peak, peak_kind = peaks()
@@ -359,11 +360,13 @@ def main():
             "config": {"workload": c.name, "grid": [c.n] * 3, "atoms": c.n_atoms, "h": c.h,
                        "variant": c.variant, "dt": c.dt, "interior_nodes": nint,
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "l2": "fields 1.1 GB >> L2, no flush", "assembly_s": round(t_asm, 3)},
+                       "l2": f"field {field_mb:.0f} MB > 126 MB L2 (each sweep streams a whole "
+                             "field), no flush", "assembly_s": round(t_asm, 3)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(c.name, dom),
-                         "kernel": ["sweep_axis0 (strided)", "sweep_axis1 (strided)",
-                                    "sweep_axis2 (contiguous)"][dom],
+                         "kernel": ["k_sweep_strided axis 0 (column tiles, + source)",
+                                    "k_sweep_strided axis 1 (column tiles)",
+                                    "k_sweep_strided axis 2 (row tiles, + flow)"][dom],
                          "kernel_ms": per_ms, "peak_kind": peak_kind,
                          "step_GBps_48B": step_gbs, "step_frac": step_gbs / peak},
             "cpu_baseline": cpu,
