@@ -1114,7 +1114,11 @@ static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
 // and TLB entries busy (64-byte chunks run at ~55% of copy bandwidth there, measured).
 template <int S, int P, bool CN>
 static void launch_strided_SC(const SweepArgs& a, int axis, cudaStream_t st) {
+  // 16-column tiles (128-byte row chunks) unless a second staged tile (AOS/MAOS epilogue
+  // operand) would halve the resident blocks.
+  const bool wide = epi_needs(a.epi) == 0;
   if (axis == 0) launch_strided_SCL<S, P, CN, 16, false>(a, axis, st);
+  else if (axis == 1 && wide) launch_strided_SCL<S, P, CN, 16, false>(a, axis, st);
   else if (axis == 1) launch_strided_SCL<S, P, CN, 8, false>(a, axis, st);
   else launch_strided_SCL<S, P, CN, 8, true>(a, axis, st);
 }
