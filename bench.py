@@ -6,7 +6,7 @@ dt = 0.5.  One bench "step" = one LODIE2 time step over the whole grid (flow + s
 three implicit line sweeps).  Fields are 1.1 GB each (>> 126 MB L2), so no L2 flush is
 needed between steps (`--config c3`: 257^3, 142 MB fields, still larger than L2).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c3] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c3|c2|c5] [--impl ours|reference]
 
 N > 1 (torchrun, one rank per GPU, NCCL): the grid is split into axis-0 slabs, one per
 rank (paper_1410_2788_b200.slab: partitioned axis-0 solve, one all-gather of the chunk end
@@ -297,6 +297,8 @@ def main():
             os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    if args.config == "c5":
+        return c5_main(args, world, rank, local, dist)
     c, p, t_asm = build_problem(args.config)
     nint = (c.n - 2) ** 3
     if dist and mode == "slab":
@@ -373,6 +375,70 @@ def main():
             "e2e": e2e,
             "gpu_launches": 3 * args.steps + 1,
             "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def c5_main(args, world, rank, local, dist):
+    """Config 5: 64 independent 97^3 proteins, AOSIE1 and LODIE2, round-robin over ranks
+    (replicas, weak in proteins per rank), 8 concurrent streams per GPU."""
+    import torch
+
+    import paper_1410_2788_b200 as pb
+    from paper_1410_2788_b200.batch import config5_problem, march_many, rank_indices
+    from paper_1410_2788_b200.configs import batch_sizes
+    from paper_1410_2788_b200.schemes import device_problem
+
+    sizes = batch_sizes()
+    mine = rank_indices(len(sizes), rank, world)
+    t0 = time.perf_counter()
+    probs = {i: config5_problem(i, sizes[i]) for i in mine}
+    for i in mine:
+        device_problem(probs[i][1])
+    torch.cuda.synchronize()
+    t_asm = time.perf_counter() - t0
+    variants = ("AOSIE1", "LODIE2")
+    jobs = [((i, v), probs[i][1], pb.MarchConfig(dt=probs[i][0].dt, T=probs[i][0].dt * args.steps,
+                                                 variant=v)) for i in mine for v in variants]
+    warm = [((k, v), p, pb.MarchConfig(dt=cfg.dt, T=cfg.dt * max(3, args.warmup), variant=v))
+            for (k, v), p, cfg in jobs[:16]]
+    march_many(warm, streams=8)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        reps = march_many(jobs, streams=8)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    bad = [k for k, r in reps.items() if r.diverged or r.steps_taken != args.steps]
+    if bad:
+        raise RuntimeError(f"config 5 marches diverged: {bad[:4]}")
+    t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    wall_max = float(t.item())
+    n = probs[mine[0]][0].n
+    total = len(sizes) * len(variants) * args.steps * (n - 2) ** 3
+    if rank == 0:
+        line = {
+            "metric": "LOD/AOS grid-point updates/s (fp64), config-5 batch",
+            "value": total / wall_max, "unit": "grid-point updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": wall_max / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, configs.py)",
+            "config": {"workload": "c5-batch64-97", "proteins": len(sizes), "grid": [n] * 3,
+                       "variants": list(variants), "dt": 0.5,
+                       "parallelism": f"proteins round-robin over {world} rank(s), 8 streams "
+                                      "per GPU", "assembly_s": round(t_asm, 3),
+                       "timing": "host wall clock around all marches of the rank (incl. per-"
+                                 "march setup), max over ranks"},
+            "roofline": None, "cpu_baseline": None, "e2e": None,
+            "gpu_launches": sum(3 * r.steps_taken for r in reps.values()) * world,
+            "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if dist:

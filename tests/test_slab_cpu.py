@@ -122,3 +122,58 @@ def test_gloo_world2_slab_march(tmp_path, variant):
     assert int(r["taken"]) == max(1, int(round(float(d["T"]) / float(d["dt"]))))
     assert int(r["dstep"]) == -1
     assert _rel(r["full"], d[variant]) <= TOL
+
+
+# ---------------------------------------------------------------------------------------
+# Config 5 batch (replicas): round-robin assignment and the result gather over gloo, with a
+# host stand-in for the march (the device path is covered by tests/test_gpu_batch.py).
+
+def _fake_problem(i, n_atoms):
+    from paper_1410_2788_b200.configs import batch_config
+
+    return batch_config(i, n_atoms), i
+
+
+def _fake_march(prob, cfg):
+    from types import SimpleNamespace
+
+    n = max(1, int(round(cfg.T / cfg.dt)))
+    return SimpleNamespace(steps_taken=n, diverged=False,
+                           final=np.full((2, 2, 2), float(prob) + (0.5 if cfg.variant.value == "LODIE2" else 0.0)),
+                           wall_time=0.0)
+
+
+def test_batch_rank_indices_partition():
+    from paper_1410_2788_b200.batch import rank_indices
+
+    for world in (1, 2, 3, 8):
+        got = sorted(i for r in range(world) for i in rank_indices(64, r, world))
+        assert got == list(range(64))
+    with pytest.raises(ValueError):
+        rank_indices(64, 2, 2)
+
+
+def _batch_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1410_2788_b200.batch import run_config5
+
+        items = run_config5(rank, world, count=10, nsteps=3, march_fn=_fake_march,
+                            problem_fn=_fake_problem)
+        if rank == 0:
+            np.save(os.path.join(out_dir, "items.npy"),
+                    np.array([(it.index, it.variant == "LODIE2", it.steps_taken, it.max_abs)
+                              for it in items]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_batch_gather(tmp_path):
+    mp.spawn(_batch_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    arr = np.load(tmp_path / "items.npy")
+    assert arr.shape == (20, 4)
+    assert list(arr[:, 0]) == [i for i in range(10) for _ in range(2)]
+    assert np.all(arr[:, 2] == 3)
+    assert np.allclose(arr[:, 3], arr[:, 0] + 0.5 * arr[:, 1])
