@@ -240,6 +240,14 @@ PBG_API int pbg_slab_destroy(pbg_slab* h, void* stream);
 PBG_API int pbg_flow_dense(int64_t n, const double* w, const double* kappa2, double coef,
                            double premultiplier, double* out, void* stream);
 
+/* Direct vacuum Poisson solve (vacuum_potential_fast, energy.py:59-85): -eps_m * d2(out) =
+ * rho on the interior with out = bnd on the faces (bnd: pitched field whose faces hold the
+ * Dirichlet data).  Boundary lifting, type-I DST along each axis (cuFFT D2Z of the odd
+ * extension), eigenvalue divide, inverse DST.  Synchronous; scratch ~5 interior-sized
+ * fp64 arrays. */
+PBG_API int pbg_vacuum_dst(const pbg_grid* g, double eps_m, const double* rho,
+                           const double* bnd, double* out, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * Energy (north_star item 5).
  *

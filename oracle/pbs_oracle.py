@@ -462,3 +462,53 @@ def energy_replusv(p: OProblem, variant, dt, T, alpha=None, aos_nonlinear="exact
     div = any(r.diverged for r in (r1, r2, v1, v2))
     dg = float("nan") if div else solvation_energy(p.qfrac, phi_m, phi_0)
     return dg, phi_m, phi_0, div
+
+
+def _const_laplacian_interior(u):
+    """pbsplit/energy.py:46-56 (same accumulation order)."""
+    c = u[INT]
+    out = -6.0 * c
+    out += u[2:, 1:-1, 1:-1]
+    out += u[:-2, 1:-1, 1:-1]
+    out += u[1:-1, 2:, 1:-1]
+    out += u[1:-1, :-2, 1:-1]
+    out += u[1:-1, 1:-1, 2:]
+    out += u[1:-1, 1:-1, :-2]
+    return out
+
+
+def vacuum_potential_fast(rho, g: OGrid, eps_m, bvals):
+    """vacuum_potential_fast (pbsplit/energy.py:59-85): boundary lifting, type-I DST
+    diagonalisation of the 7-point operator, eigenvalue divide, inverse DST."""
+    import scipy.fft
+
+    gg = np.zeros(g.shape)
+    apply_faces(gg, bvals)
+    rhs = rho[INT] + (eps_m / g.h ** 2) * _const_laplacian_interior(gg)
+    lam_1d = []
+    for d in range(3):
+        n = g.shape[d]
+        m = np.arange(1, n - 1)
+        lam_1d.append(4.0 * np.sin(np.pi * m / (2.0 * (n - 1))) ** 2)
+    lam = (eps_m / g.h ** 2) * (lam_1d[0][:, None, None] + lam_1d[1][None, :, None]
+                                + lam_1d[2][None, None, :])
+    psi = scipy.fft.idstn(scipy.fft.dstn(rhs, type=1) / lam, type=1)
+    out = gg
+    out[INT] = psi
+    return out
+
+
+def energy_direct(p: OProblem, variant, dt, T, mode="Plain", alpha=None,
+                  aos_nonlinear="exact"):
+    """energy_pipeline(variant="Plain" | "RE") (pbsplit/energy.py:109-164): solvent march
+    (or its Richardson pair) against the direct vacuum solve."""
+    if mode == "Plain":
+        r = march(p, variant, dt, T, alpha, aos_nonlinear=aos_nonlinear)
+        phi_m, div = r.final, r.diverged
+    else:
+        r1 = march(p, variant, dt, T, alpha, aos_nonlinear=aos_nonlinear)
+        r2 = march(p, variant, 0.5 * dt, T, alpha, aos_nonlinear=aos_nonlinear)
+        phi_m, div = richardson(r1.final, r2.final), r1.diverged or r2.diverged
+    phi_0 = vacuum_potential_fast(p.rho, p.grid, p.eps_m, vacuum_of(p).bvals)
+    dg = float("nan") if div else solvation_energy(p.qfrac, phi_m, phi_0)
+    return dg, phi_m, phi_0, div

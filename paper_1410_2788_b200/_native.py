@@ -98,6 +98,8 @@ _SIGS = {
     "pbg_maxabs": ([_P(PbgGrid), c_void_p, _P(c_double), c_void_p], ctypes.c_int),
     "pbg_set_profiling": ([c_int32], ctypes.c_int),
     "pbg_get_profile": ([_P(c_double), _P(c_int64)], ctypes.c_int),
+    "pbg_vacuum_dst": ([_P(PbgGrid), c_double, c_void_p, c_void_p, c_void_p, c_void_p],
+                       ctypes.c_int),
     "pbg_slab_exchange_elems": ([_P(PbgGrid)], c_int64),
     "pbg_slab_create": ([_P(PbgMarchDesc), c_int32, c_int32, c_void_p, c_void_p,
                          _P(c_void_p), c_void_p], ctypes.c_int),

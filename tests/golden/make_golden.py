@@ -193,11 +193,39 @@ def energy_case():
     save("energy", **out)
 
 
+def vacuum_case():
+    """DST-I vacuum solver and the Plain / RE energies (energy.py:46-85, 109-164)."""
+    from pbsplit.energy import vacuum_potential_fast
+    from pbsplit.problem import make_vacuum_problem
+
+    atoms = synthetic_atoms(12, 3.0, 41)  # the energy_case problem
+    prob = pb.protein_problem(system_of(atoms), h=0.5, padding=4.0, kappa_bar=1.1283,
+                              eps_m=2.0, eps_s=80.0)
+    vac = make_vacuum_problem(prob)
+    out = dict(atoms=np.array(atoms), padding=4.0, kappa_bar=1.1283, eps_m=2.0, eps_s=80.0,
+               **grid_meta(prob.grid))
+    out["phi0_fast"] = vacuum_potential_fast(prob.rho, prob.grid, prob.eps_m,
+                                             vac.boundary).data
+    for v in ("LODIE2", "AOSIE1"):
+        for ev in ("Plain", "RE"):
+            res = pb.energy_pipeline(prob, MarchConfig(dt=0.5, T=5.0, variant=v), ev)
+            out[f"dg_{ev}_{v}"] = res.delta_g
+    # Kirkwood sphere (config 1): Plain energy with the direct vacuum solve
+    sysk = pb.MolecularSystem([pb.Atom((0.0, 0.0, 0.0), 1.0, 2.0)], label="kirkwood")
+    kw = KIRKWOOD
+    pk = pb.protein_problem(sysk, h=kw["h"], padding=kw["padding"], kappa_bar=kw["kappa_bar"],
+                            eps_m=kw["eps_m"], eps_s=kw["eps_s"])
+    res = pb.energy_pipeline(pk, MarchConfig(dt=kw["dt"], T=kw["T"], variant="LODIE2"), "Plain")
+    out["dg_kirkwood_plain"] = res.delta_g
+    out["kirkwood_phi0_plane"] = res.phi_0.data[res.phi_0.data.shape[0] // 2]
+    save("vacuum", **out)
+
+
+CASES = {"assembly": lambda: (assembly_case("a40", 40, 5.0, 11, 0.5, 4.0, 0.0, 1.1283),
+                              assembly_case("a60_probe", 60, 6.0, 12, 0.4, 4.0, 1.4, 0.9212)),
+         "march": march_cases, "small_api": small_api_cases, "sphere": sphere_case,
+         "energy": energy_case, "kirkwood": kirkwood_case, "vacuum": vacuum_case}
+
 if __name__ == "__main__":
-    assembly_case("a40", 40, 5.0, 11, 0.5, 4.0, 0.0, 1.1283)
-    assembly_case("a60_probe", 60, 6.0, 12, 0.4, 4.0, 1.4, 0.9212)
-    march_cases()
-    small_api_cases()
-    sphere_case()
-    energy_case()
-    kirkwood_case()
+    for name in (sys.argv[1:] or list(CASES)):
+        CASES[name]()

@@ -113,3 +113,16 @@ def test_kirkwood_config1():
         assert rel_err(u[32], d[v + "_plane"]) <= 1e-13
         st = np.array([np.max(np.abs(u)), np.sum(u), np.sum(u * u)])
         assert np.allclose(st, d[v + "_stats"], rtol=1e-12, atol=0)
+
+
+def test_vacuum_direct_solver_and_plain_re_energies():
+    """DST-I vacuum solve and Plain / RE energies against the reference (vacuum.npz)."""
+    d = golden("vacuum")
+    p = oracle_protein(d)
+    phi0 = O.vacuum_potential_fast(p.rho, p.grid, p.eps_m, O.vacuum_of(p).bvals)
+    assert rel_err(phi0, d["phi0_fast"]) <= 1e-13
+    for v in ("LODIE2", "AOSIE1"):
+        for mode in ("Plain", "RE"):
+            dg, _, _, div = O.energy_direct(p, v, 0.5, 5.0, mode)
+            want = float(d[f"dg_{mode}_{v}"])
+            assert not div and abs(dg - want) <= 1e-10 * abs(want)
