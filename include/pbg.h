@@ -143,7 +143,7 @@ PBG_API int pbg_coulomb_faces(const pbg_grid* g, const double* atoms, int32_t na
 typedef struct pbg_march_desc {
   pbg_grid grid;
   pbg_palette pal;
-  int32_t variant;          /* PBG_LODIE1 .. PBG_MAOSCN */
+  int32_t variant;          /* PBG_LODIE1 .. PBG_EULER */
   int32_t aos_literal;      /* MarchConfig.aos_nonlinear == "literal" */
   double dt;
   double alpha;             /* already resolved: config.alpha or problem.alpha */

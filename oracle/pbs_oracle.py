@@ -348,12 +348,18 @@ PLANS = {
 }
 
 
+EXTRA_PLANS = {"ADI1": "adi1", "ADI2": "adi2", "ExplicitEuler": "euler"}
+
+
 class OStepper:
     """Stepper (pbsplit/schemes.py:185-380) for the LOD/AOS/MAOS families."""
 
     def __init__(self, p: OProblem, variant, dt, alpha=None, aos_nonlinear="exact"):
         self.p = p
         self.variant = variant
+        if variant in EXTRA_PLANS:  # comparison schemes (schemes.py:240-253)
+            self._init_extra(p, variant, dt, alpha)
+            return
         self.family, mult, self.cn, self.src = PLANS[variant]
         self.alpha = alpha if alpha is not None else p.alpha
         self.dta = dt / self.alpha
@@ -389,8 +395,58 @@ class OStepper:
             rhs = rhs + extra
         return self._faces(self.fac[axis].solve(rhs))
 
+    def _init_extra(self, p, variant, dt, alpha):
+        self.family = EXTRA_PLANS[variant]
+        self.alpha = alpha if alpha is not None else p.alpha
+        self.dta = dt / self.alpha
+        self.h2 = p.grid.h ** 2
+        k2 = p.region.kappa2
+        self.rho_int = p.rho[INT]
+        self.cn = False
+        if variant == "ADI1":
+            self.fac = [LineFactors(p.grid, p.region, p.bvals, a, self.dta) for a in range(3)]
+            self.decay = np.exp(-k2 * self.dta)
+        elif variant == "ADI2":
+            self.fac = [LineFactors(p.grid, p.region, p.bvals, a, 0.5 * self.dta)
+                        for a in range(3)]
+            self.decay = np.exp(-0.5 * k2 * self.dta)
+        else:
+            self.k2_int = k2[INT]
+            self.ion_mask = self.k2_int > 0.0
+
+    def _d2(self, w, axis):
+        return delta2(w, self.p.region.eps_half[axis], axis) / self.h2
+
+    def _step_extra(self, u):
+        fam = self.family
+        if fam == "adi1":  # schemes.py:331-342
+            w = self._nl(u)
+            sy, sz = self._d2(w, 1), self._d2(w, 2)
+            u1 = self._faces(self.fac[0].solve(w[INT] + self.dta * (sy + sz + self.rho_int)))
+            u2 = self._faces(self.fac[1].solve(u1[INT] - self.dta * sy))
+            return self._faces(self.fac[2].solve(u2[INT] - self.dta * sz))
+        if fam == "adi2":  # schemes.py:344-353
+            w = self._nl(u)
+            sx, sy, sz = self._d2(w, 0), self._d2(w, 1), self._d2(w, 2)
+            rhs = w[INT] + self.dta * (0.5 * sx + sy + sz + self.rho_int)
+            v1 = self._faces(self.fac[0].solve(rhs))
+            v2 = self._faces(self.fac[1].solve(v1[INT] - 0.5 * self.dta * sy))
+            v3 = self._faces(self.fac[2].solve(v2[INT] - 0.5 * self.dta * sz))
+            return self._nl(v3)
+        # explicit Euler, schemes.py:355-363
+        r = self.p.region
+        lap = (delta2(u, r.eps_half[0], 0) + delta2(u, r.eps_half[1], 1)
+               + delta2(u, r.eps_half[2], 2)) / self.h2
+        ui = u[INT]
+        react = np.zeros_like(ui)
+        m = self.ion_mask
+        react[m] = self.k2_int[m] * np.sinh(ui[m])
+        return self._faces(ui + self.dta * (lap - react + self.rho_int))
+
     def step(self, u):
         with np.errstate(over="ignore", invalid="ignore", under="ignore"):
+            if self.variant in EXTRA_PLANS:
+                return self._step_extra(u)
             fam = self.family
             if fam in ("lod1", "lod2"):  # schemes.py:301-311
                 if fam == "lod2":

@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 OBJ_DIR = os.path.join(OUT_DIR, "obj")
 LIB = os.path.join(OUT_DIR, "libpbg.so")
-SOURCES = ["sweep.cu", "capi.cu", "assemble.cu", "vacuum.cu"]
+SOURCES = ["sweep.cu", "slab.cu", "schemes_extra.cu", "capi.cu", "assemble.cu", "vacuum.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]

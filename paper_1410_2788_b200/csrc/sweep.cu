@@ -44,85 +44,9 @@
 #include <mutex>
 #include <vector>
 
-#include "pbg_internal.cuh"
+#include "sweep.cuh"
 
 namespace pbg {
-
-enum { PRO_NONE = 0, PRO_FLOW = 1, PRO_SRC = 2 };
-enum {
-  EPI_STORE = 0,
-  EPI_SRC = 1,
-  EPI_FLOW = 2,
-  EPI_AOS0 = 3,
-  EPI_AOS1 = 4,
-  EPI_AOS2 = 5,
-  EPI_MAOS0 = 6,
-  EPI_MAOS1 = 7,
-  EPI_MAOS2 = 8
-};
-
-constexpr int kSeg = 32;   // segments per line, contiguous axis (one warp lane each)
-
-struct AxisCoef {
-  double diag[4];  // [em*2 + ep]  1 + f*(e_plus + e_minus)
-  double sub[2];   // [em]         -f*e_minus
-  double sup[2];   // [ep]         -f*e_plus
-  double flo[2];   // [em]         f*e_minus   (low fold, times the face value)
-  double fhi[2];   // [ep]         f*e_plus    (high fold)
-  double eps[2];   // palette (CN stencil)
-};
-
-// Uniform-segment tables: tab[((type*2 + v)*5 + q)*kTabRows + j], type 0 = interior segment,
-// 1 = first segment of a line (row 0 has no sub-diagonal), 2 = last segment whose separator is
-// the padding row m (its last inner row is row m-1, no super-diagonal); q = inv, g = a*inv,
-// cp, alpha, beta.
-constexpr int kTabRows = 32;
-constexpr int kTabDoubles = 3 * 2 * 5 * kTabRows;
-enum { TQ_INV = 0, TQ_G = 1, TQ_CP = 2, TQ_AL = 3, TQ_BE = 4 };
-
-struct SweepArgs {
-  Layout L;
-  int m;  // interior nodes along the sweep axis
-  const double* src;
-  const double* bnd;
-  const uint8_t* codes;
-  const double* rho;
-  double* dst;
-  const double* acc;
-  const double* tab;   // uniform-segment tables (kTabDoubles)
-  const double* minv;  // 32x32 inverse of the clean-line reduced system
-  const unsigned long long* desc;  // per-segment descriptors (2 words), see k_build_desc
-  const double* gfac;  // precomputed factors of general segments (5 x kTabRows each)
-  int static_ok;       // the clean-line reduced inverse applies to this axis (32*S in {m, m+1})
-  AxisCoef co;
-  // Table of the dominant segment kind (interior, palette 0 = solvent) as kernel parameters:
-  // with unrolled rows the compiler folds these into constant-bank operands (no loads).
-  double tmid[5 * kTabRows];
-  int cn;
-  double cnc;  // cn_f / h^2
-  int pro;
-  double pro_coef;
-  int has_extra;
-  double extra;
-  double decay0, decay1;  // flow decay for solute-bit 0 / 1
-  double sat0, sat1;      // 2*atanh(decay)
-  double pm;
-  int epi;
-  double epi_coef;
-  int* div_step;
-  int step;
-  double thr;
-  int check;
-  int dbg;  // experiments only: 1 = stage + store (no solve)
-  const double* ftab;  // flow tables (kFlowTabDoubles), staged into shared memory
-  // Strided axes: offset (from the line base) of the high boundary value in bnd; normally
-  // plane m+1 of a field, one plane for the two-plane ghost buffers of the slab march.
-  long long hi_off;
-  // Slab march phase A (ends-only mode): store rows 1 and m of every line into ends[base] /
-  // ends[base + ends_off] instead of the field (axis 0 only).
-  double* ends;
-  long long ends_off;
-};
 
 // Asynchronous global->shared copies (LDGSTS): issued back to back, no register round trip.
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -1290,7 +1214,7 @@ static bool make_reduced_inverse(const AxisCoef& co, const double* tab, int S, i
   return true;
 }
 
-static void set_decays(SweepArgs& a, double d0, double d1) {
+void set_decays(SweepArgs& a, double d0, double d1) {
   a.decay0 = d0;
   a.decay1 = d1;
   a.sat0 = d0 < 1.0 ? 2.0 * std::atanh(d0) : 0.0;
@@ -1321,7 +1245,7 @@ static const double* flow_tables() {
   return dev[d];
 }
 
-static SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, double factor) {
+SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, double factor) {
   SweepArgs a;
   memset(&a, 0, sizeof(a));
   a.L = make_layout(g);
@@ -1337,19 +1261,13 @@ static SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, 
   return a;
 }
 
-// Per-launch-sequence device data of one axis: tables, reduced inverse, segment descriptors.
-struct AxisAux {
-  double* buf = nullptr;
-  unsigned long long* desc = nullptr;
-  double* gfac = nullptr;
-};
 
 static long long desc_segments(const Layout& L, int axis, int P) {
   if (axis == 2 && !axis2_rows()) return (long long)(L.n0 - 2) * (L.n1 - 2) * kSeg;
   return (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * ((axis == 2 ? L.n1 : L.n2) - 2);
 }
 
-static int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
+int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
                         cudaStream_t st) {
   const int P = seg_P(axis, a.m);
   const int S = seg_S(a.m, P, !(axis == 2 && !axis2_rows()));
@@ -1392,7 +1310,7 @@ static int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& a
   return PBG_OK;
 }
 
-static void release_axis(AxisAux& aux, cudaStream_t st) {
+void release_axis(AxisAux& aux, cudaStream_t st) {
   if (aux.buf) cudaFreeAsync(aux.buf, st);
   if (aux.desc) cudaFreeAsync(aux.desc, st);
   if (aux.gfac) cudaFreeAsync(aux.gfac, st);
@@ -1401,20 +1319,13 @@ static void release_axis(AxisAux& aux, cudaStream_t st) {
   aux.gfac = nullptr;
 }
 
-static int launch_sweep(const SweepArgs& a, int axis, cudaStream_t st) {
+int launch_sweep(const SweepArgs& a, int axis, cudaStream_t st) {
   if (!a.ftab) return fail(PBG_E_CUDA, "flow table allocation failed");
   return (axis == 2 && !axis2_rows()) ? launch_contig(a, st) : launch_strided(a, axis, st);
 }
 
-// Variant table (schemes.py:209-262).
-struct Plan {
-  int family;  // 0: LOD flow-first (IE1/CN1), 1: LOD source-first (IE2/CN2), 2: AOS, 3: MAOS
-  double mult;  // sweep factor = mult * dta
-  int cn;
-  double src[3];
-};
 
-static bool plan_for(int v, Plan& p) {
+bool plan_for(int v, Plan& p) {
   p.src[0] = p.src[1] = p.src[2] = 0.0;
   switch (v) {
     case PBG_LODIE1: p = {0, 1.0, 0, {0, 0, 0}}; return true;
@@ -1432,7 +1343,7 @@ static bool plan_for(int v, Plan& p) {
 }
 
 __global__ void k_faces_bad(const Layout L, const double* x, double thr, int* flag,
-                            int skip_lo = 0, int skip_hi = 0) {
+                            int skip_lo, int skip_hi) {
   // One thread per node of the six faces.  Faces equal the Dirichlet data after step 1, so a
   // bad face means march() stops at step 1 (max|u| includes faces, schemes.py:417-421).
   const long long n01 = (long long)L.n0 * L.n1, n02 = (long long)L.n0 * L.n2,
@@ -1466,7 +1377,7 @@ __global__ void k_faces_bad(const Layout L, const double* x, double thr, int* fl
 }
 
 // Per-axis launch arguments of one march (variant plan, flow decays, fusions).
-static void march_axes(const pbg_march_desc* d, const Plan& plan, SweepArgs ax[3]) {
+void march_axes(const pbg_march_desc* d, const Plan& plan, SweepArgs ax[3]) {
   const pbg_grid* g = &d->grid;
   const double dta = d->dt / d->alpha;
   const double factor = plan.mult * dta;
@@ -1568,13 +1479,16 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
   if (!d) return fail(PBG_E_INVALID, "null descriptor");
   int rc = validate_grid(&d->grid);
   if (rc) return rc;
-  Plan plan;
-  if (!plan_for(d->variant, plan))
-    return fail(PBG_E_UNSUPPORTED, "variant not supported by the device march");
   if (!(d->dt > 0) || !(d->alpha > 0) || d->nsteps < 1)
     return fail(PBG_E_INVALID, "dt, alpha must be positive and nsteps >= 1");
   if (!d->codes || !d->rho || !d->initial || !d->work[0] || !d->work[1])
     return fail(PBG_E_INVALID, "null device buffer");
+  if (d->variant == PBG_ADI1 || d->variant == PBG_ADI2 || d->variant == PBG_EULER)
+    return march_extra(d, steps_taken, diverged_step, result_slot, device_ms,
+                       (cudaStream_t)stream);
+  Plan plan;
+  if (!plan_for(d->variant, plan))
+    return fail(PBG_E_UNSUPPORTED, "variant not supported by the device march");
   cudaStream_t st = (cudaStream_t)stream;
   SweepArgs ax[3];
   march_axes(d, plan, ax);
@@ -1706,385 +1620,3 @@ extern "C" PBG_API int pbg_sweep(const pbg_grid* g, const pbg_palette* pal,
   return rc;
 }
 
-// ---------------------------------------------------------------------------------------
-// Slab-decomposed march: the grid is split along axis 0 into contiguous
-// slabs of interior planes, one per rank.  A rank's local grid carries one extra plane on
-// each side: the global face on the first / last rank, otherwise a ghost plane.  Axes 1 and
-// 2, the flow and the source are rank-local.  The axis-0 sweep couples the ranks; it is
-// solved exactly by a two-level partitioned (SPIKE-style) scheme:
-//
-//   phase A   each rank solves its chunk of every axis-0 line with zero values in the
-//             internal ghost planes (true faces kept) and keeps only the chunk's first and
-//             last rows g_f, g_l (ends-only mode of k_sweep_strided: 8 B/node read);
-//   exchange  all ranks all-gather (g_f, g_l) planes + their divergence flag;
-//   interface every rank solves, per line, the 2N-unknown system of chunk end values
-//               F_r = g_f + p_f L_{r-1} + q_f F_{r+1},  L_r = g_l + p_l L_{r-1} + q_l F_{r+1}
-//             whose responses p, q (the chunk's end rows for a unit ghost value) are static
-//             and gathered once at setup; the neighbours' end values become the rank's
-//             ghost (Dirichlet) values;
-//   phase B   the ordinary axis-0 sweep of the chunk with those ghost values, then the
-//             rank-local axis-1 and axis-2 sweeps.
-//
-// The chunk system with the exact neighbour values is the global system restricted to the
-// chunk, so the result equals the single-device march up to reassociation.  CN variants
-// also exchange the state's end planes before phase A (the explicit half reads the ghost
-// planes).  The caller moves the exchange buffers (NCCL all-gather, or a device copy when
-// all partitions live on one GPU).
-
-namespace pbg {
-
-constexpr int kMaxRanks = 16;
-constexpr long long kExchTail = 32;  // flag + padding, keeps rank blocks 256-byte aligned
-
-static long long slab_plane(const Layout& L) { return L.s0; }
-
-// x += c*rho on n elements (LODCN2 halo: the ghost planes carry w = u + dta*rho).
-__global__ void k_slab_add_source(double* x, const double* rho, double c, long long n) {
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
-       t += (long long)gridDim.x * blockDim.x) {
-    const double r = rho[t];
-    if (r != 0.0) x[t] = __dadd_rn(x[t], __dmul_rn(c, r));
-  }
-}
-static long long slab_elems(const Layout& L) { return 4 * slab_plane(L) + kExchTail; }
-
-// Per line (j, k): block Thomas over the ranks' chunk end values.  recv/coef hold one
-// exchange block of E doubles per rank: planes [g_f | g_l | .. ] and [p_f | p_l | q_f | q_l].
-__global__ void k_slab_interface(const Layout L, int rank, int nranks, const double* recv,
-                                 const double* coef, long long E, double* gb, int* dflag) {
-  const long long plane = L.s0;
-  if (blockIdx.x == 0 && (int)threadIdx.x < nranks) {
-    const int f = *reinterpret_cast<const int*>(recv + threadIdx.x * E + 4 * plane);
-    if (f != INT_MAX) atomicMin(dflag, f);
-  }
-  const int nj = L.n1 - 2, nk = L.n2 - 2;
-  const long long nl = (long long)nj * nk;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nl;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int j = 1 + (int)(t / nk), k = 1 + (int)(t % nk);
-    const long long o = L.at(0, j, k);
-    double e[kMaxRanks], hh[kMaxRanks], cc[kMaxRanks], dd[kMaxRanks];
-    double c = 0.0, d = 0.0;
-    for (int r = 0; r < nranks; ++r) {
-      const double* G = recv + r * E;
-      const double* Q = coef + r * E;
-      const double gf = G[o], gl = G[plane + o];
-      const double pf = r > 0 ? Q[o] : 0.0, pl = r > 0 ? Q[plane + o] : 0.0;
-      const double qf = r + 1 < nranks ? Q[2 * plane + o] : 0.0;
-      const double ql = r + 1 < nranks ? Q[3 * plane + o] : 0.0;
-      const double inv = 1.0 / (1.0 - pf * d);
-      e[r] = (gf + pf * c) * inv;
-      hh[r] = qf * inv;
-      const double cn = gl + pl * c + pl * d * e[r];
-      const double dn = pl * d * hh[r] + ql;
-      cc[r] = c = cn;
-      dd[r] = d = dn;
-    }
-    double F = 0.0, Lprev = 0.0, Fnext = 0.0;
-    for (int r = nranks - 1; r >= 0; --r) {
-      const double Fr = e[r] + hh[r] * F;
-      if (r == rank + 1) Fnext = Fr;
-      if (r == rank - 1) Lprev = cc[r] + dd[r] * F;
-      F = Fr;
-    }
-    if (rank > 0) gb[o] = Lprev;
-    if (rank + 1 < nranks) gb[plane + o] = Fnext;
-  }
-}
-
-}  // namespace pbg
-
-struct pbg_slab {
-  pbg_march_desc d;
-  int rank, nranks;
-  Plan plan;
-  SweepArgs ax[3];
-  AxisAux aux[3];
-  double* send;
-  double* recv;
-  double* coef = nullptr;  // nranks exchange blocks: the gathered responses
-  double* gbA = nullptr;   // ghost values of phase A: zeros (faces on the outer ranks)
-  double* gbB = nullptr;   // ghost values of phase B: the neighbours' chunk end values
-  int* dflag = nullptr;
-  int st_idx, st0, step;
-  long long plane, E;
-};
-
-static int slab_state(const pbg_slab* h, const double** X, double** A, double** Bf) {
-  const pbg_march_desc* d = &h->d;
-  *X = h->st_idx < 0 ? d->initial : d->work[h->st_idx];
-  const int other = h->st_idx < 0 ? 0 : 1 - h->st_idx;
-  *A = d->work[other];
-  *Bf = h->st_idx < 0 ? d->work[1] : d->work[h->st_idx];
-  return other;
-}
-
-extern "C" PBG_API int64_t pbg_slab_exchange_elems(const pbg_grid* local) {
-  if (!local) return -1;
-  return slab_elems(make_layout(local));
-}
-
-extern "C" PBG_API int pbg_slab_destroy(pbg_slab* h, void* stream) {
-  if (!h) return PBG_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  for (int q = 0; q < 3; ++q) release_axis(h->aux[q], st);
-  if (h->coef) cudaFreeAsync(h->coef, st);
-  if (h->gbA) cudaFreeAsync(h->gbA, st);
-  if (h->gbB) cudaFreeAsync(h->gbB, st);
-  if (h->dflag) cudaFreeAsync(h->dflag, st);
-  cudaStreamSynchronize(st);
-  delete h;
-  return PBG_OK;
-}
-
-extern "C" PBG_API int pbg_slab_create(const pbg_march_desc* d, int32_t rank, int32_t nranks,
-                                       double* send, double* recv, pbg_slab** out,
-                                       void* stream) {
-  if (!d || !out) return fail(PBG_E_INVALID, "null descriptor");
-  *out = nullptr;
-  int rc = validate_grid(&d->grid);
-  if (rc) return rc;
-  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
-    return fail(PBG_E_INVALID, "rank / nranks out of range (1 <= nranks <= 16)");
-  if (!send || !recv) return fail(PBG_E_INVALID, "null exchange buffer");
-  Plan plan;
-  if (!plan_for(d->variant, plan))
-    return fail(PBG_E_UNSUPPORTED, "variant not supported by the device march");
-  if (plan.family > 1 || d->variant == PBG_LODCN1)
-    return fail(PBG_E_UNSUPPORTED,
-                "slab march supports LODIE1, LODIE2 and LODCN2 (AOS/MAOS/LODCN1: single device)");
-  if (!(d->dt > 0) || !(d->alpha > 0) || d->nsteps < 1)
-    return fail(PBG_E_INVALID, "dt, alpha must be positive and nsteps >= 1");
-  if (!d->codes || !d->rho || !d->initial || !d->work[0] || !d->work[1])
-    return fail(PBG_E_INVALID, "null device buffer");
-  cudaStream_t st = (cudaStream_t)stream;
-  pbg_slab* h = new pbg_slab();
-  h->d = *d;
-  h->rank = rank;
-  h->nranks = nranks;
-  h->plan = plan;
-  h->send = send;
-  h->recv = recv;
-  march_axes(d, plan, h->ax);
-  for (int axis = 0; axis < 3; ++axis) {
-    rc = prepare_axis(h->ax[axis], axis, d->codes, h->aux[axis], st);
-    if (rc) {
-      pbg_slab_destroy(h, stream);
-      return rc;
-    }
-  }
-  const Layout L = make_layout(&d->grid);
-  h->plane = slab_plane(L);
-  h->E = slab_elems(L);
-  const size_t pb = h->plane * sizeof(double);
-  const bool first = rank == 0, last = rank == nranks - 1;
-  auto cu = [&](cudaError_t e) {
-    if (e != cudaSuccess) {
-      fail(PBG_E_CUDA, cudaGetErrorString(e));
-      return false;
-    }
-    return true;
-  };
-  double* zeros = nullptr;
-  double* unit = nullptr;
-  const long long nelem = (long long)L.n0 * L.s0 + 64;
-  bool ok = cu(cudaMallocAsync(&h->coef, nranks * h->E * sizeof(double), st)) &&
-            cu(cudaMallocAsync(&h->gbA, 2 * pb, st)) && cu(cudaMallocAsync(&h->gbB, 2 * pb, st)) &&
-            cu(cudaMallocAsync(&h->dflag, sizeof(int), st)) &&
-            cu(cudaMallocAsync(&zeros, nelem * sizeof(double), st)) &&
-            cu(cudaMallocAsync(&unit, 2 * pb, st)) &&
-            cu(cudaMemsetAsync(zeros, 0, nelem * sizeof(double), st)) &&
-            cu(cudaMemsetAsync(h->gbA, 0, 2 * pb, st));
-  if (ok) {  // outer ranks keep the true faces as their fixed Dirichlet values
-    const double* w = d->work[0];
-    if (first) ok = cu(cudaMemcpyAsync(h->gbA, w, pb, cudaMemcpyDeviceToDevice, st));
-    if (ok && last)
-      ok = cu(cudaMemcpyAsync(h->gbA + h->plane, w + (L.n0 - 1) * h->plane, pb,
-                              cudaMemcpyDeviceToDevice, st));
-    if (ok) ok = cu(cudaMemcpyAsync(h->gbB, h->gbA, 2 * pb, cudaMemcpyDeviceToDevice, st));
-  }
-  if (ok) {
-    const int init = INT_MAX;
-    ok = cu(cudaMemcpyAsync(h->dflag, &init, sizeof(init), cudaMemcpyHostToDevice, st));
-  }
-  // Static responses of the chunk's end rows to a unit low / high ghost value: the same
-  // kernel on a zero field without prologue, so the arithmetic matches phase A.
-  for (int side = 0; ok && side < 2; ++side) {
-    std::vector<double> hv(2 * h->plane, 0.0);
-    for (long long q = 0; q < h->plane; ++q) hv[side * h->plane + q] = 1.0;
-    ok = cu(cudaMemcpyAsync(unit, hv.data(), 2 * pb, cudaMemcpyHostToDevice, st)) &&
-         cu(cudaStreamSynchronize(st));
-    if (!ok) break;
-    SweepArgs a = h->ax[0];
-    a.pro = PRO_NONE;
-    a.has_extra = 0;
-    a.epi = EPI_STORE;
-    a.check = 0;
-    a.src = zeros;
-    a.rho = zeros;
-    a.dst = zeros;
-    a.bnd = unit;
-    a.hi_off = h->plane;
-    a.ends = send + 2 * side * h->plane;
-    a.ends_off = h->plane;
-    a.step = 1;
-    a.div_step = nullptr;
-    if (launch_sweep(a, 0, st)) ok = false;
-  }
-  if (ok) {
-    const int init = INT_MAX;
-    ok = cu(cudaMemcpyAsync(send + 4 * h->plane, &init, sizeof(init), cudaMemcpyHostToDevice,
-                            st));
-  }
-  if (ok && d->check_divergence) {
-    k_faces_bad<<<148, 256, 0, st>>>(L, d->work[0], d->divergence_threshold, h->dflag,
-                                     first ? 0 : 1, last ? 0 : 1);
-    ok = cudaGetLastError() == cudaSuccess || (fail(PBG_E_CUDA, "k_faces_bad"), false);
-  }
-  if (zeros) cudaFreeAsync(zeros, st);
-  if (unit) cudaFreeAsync(unit, st);
-  if (ok) ok = cu(cudaStreamSynchronize(st));
-  if (!ok) {
-    pbg_slab_destroy(h, stream);
-    return PBG_E_CUDA;
-  }
-  h->st_idx = -1;
-  if (d->initial == d->work[0]) h->st_idx = 0;
-  else if (d->initial == d->work[1]) h->st_idx = 1;
-  h->st0 = h->st_idx;
-  h->step = 0;
-  *out = h;
-  return PBG_OK;
-}
-
-extern "C" PBG_API int pbg_slab_setup(pbg_slab* h, void* stream) {
-  if (!h) return fail(PBG_E_INVALID, "null slab");
-  cudaStream_t st = (cudaStream_t)stream;
-  PBG_CUDA(cudaMemcpyAsync(h->coef, h->recv, h->nranks * h->E * sizeof(double),
-                           cudaMemcpyDeviceToDevice, st));
-  return PBG_OK;
-}
-
-extern "C" PBG_API int pbg_slab_halo_pack(pbg_slab* h, void* stream) {
-  if (!h) return fail(PBG_E_INVALID, "null slab");
-  cudaStream_t st = (cudaStream_t)stream;
-  const double *X;
-  double *A, *Bf;
-  slab_state(h, &X, &A, &Bf);
-  const int n0 = h->d.grid.n[0];
-  const size_t pb = h->plane * sizeof(double);
-  PBG_CUDA(cudaMemcpyAsync(h->send, X + h->plane, pb, cudaMemcpyDeviceToDevice, st));
-  PBG_CUDA(cudaMemcpyAsync(h->send + h->plane, X + (n0 - 2) * h->plane, pb,
-                           cudaMemcpyDeviceToDevice, st));
-  if (h->ax[0].pro == PRO_SRC) {  // the CN stencil of the first sweep reads w = u + dta*rho
-    const double* rho = h->d.rho;
-    k_slab_add_source<<<148, 256, 0, st>>>(h->send, rho + h->plane, h->ax[0].pro_coef,
-                                           h->plane);
-    k_slab_add_source<<<148, 256, 0, st>>>(h->send + h->plane, rho + (n0 - 2) * h->plane,
-                                           h->ax[0].pro_coef, h->plane);
-    PBG_LAUNCH_CHECK("k_slab_add_source");
-  }
-  return PBG_OK;
-}
-
-extern "C" PBG_API int pbg_slab_halo_unpack(pbg_slab* h, void* stream) {
-  if (!h) return fail(PBG_E_INVALID, "null slab");
-  cudaStream_t st = (cudaStream_t)stream;
-  const double *X;
-  double *A, *Bf;
-  slab_state(h, &X, &A, &Bf);
-  double* Xw = const_cast<double*>(X);  // ghost planes only; never the owned planes
-  const int n0 = h->d.grid.n[0];
-  const size_t pb = h->plane * sizeof(double);
-  if (h->rank > 0)
-    PBG_CUDA(cudaMemcpyAsync(Xw, h->recv + (h->rank - 1) * h->E + h->plane, pb,
-                             cudaMemcpyDeviceToDevice, st));
-  if (h->rank + 1 < h->nranks)
-    PBG_CUDA(cudaMemcpyAsync(Xw + (n0 - 1) * h->plane, h->recv + (h->rank + 1) * h->E, pb,
-                             cudaMemcpyDeviceToDevice, st));
-  return PBG_OK;
-}
-
-extern "C" PBG_API int pbg_slab_step_a(pbg_slab* h, void* stream) {
-  if (!h) return fail(PBG_E_INVALID, "null slab");
-  cudaStream_t st = (cudaStream_t)stream;
-  const double *X;
-  double *A, *Bf;
-  slab_state(h, &X, &A, &Bf);
-  SweepArgs a = h->ax[0];
-  a.step = h->step + 1;
-  a.div_step = h->d.check_divergence ? h->dflag : nullptr;
-  a.src = X;
-  a.dst = A;  // not written in ends-only mode
-  a.bnd = h->gbA;
-  a.hi_off = h->plane;
-  a.ends = h->send;
-  a.ends_off = h->plane;
-  int rc = launch_sweep(a, 0, st);
-  if (rc) return rc;
-  PBG_CUDA(cudaMemcpyAsync(h->send + 4 * h->plane, h->dflag, sizeof(int),
-                           cudaMemcpyDeviceToDevice, st));
-  return PBG_OK;
-}
-
-extern "C" PBG_API int pbg_slab_step_b(pbg_slab* h, void* stream) {
-  if (!h) return fail(PBG_E_INVALID, "null slab");
-  cudaStream_t st = (cudaStream_t)stream;
-  const double *X;
-  double *A, *Bf;
-  const int other = slab_state(h, &X, &A, &Bf);
-  const Layout L = make_layout(&h->d.grid);
-  k_slab_interface<<<148 * 4, 256, 0, st>>>(L, h->rank, h->nranks, h->recv, h->coef, h->E,
-                                            h->gbB, h->dflag);
-  PBG_LAUNCH_CHECK("k_slab_interface");
-  const int s = h->step + 1;
-  for (int axis = 0; axis < 3; ++axis) {
-    SweepArgs a = h->ax[axis];
-    a.step = s;
-    a.div_step = h->d.check_divergence ? h->dflag : nullptr;
-    a.src = axis == 0 ? X : (axis == 1 ? A : Bf);
-    a.dst = axis == 0 ? A : (axis == 1 ? Bf : A);
-    if (axis == 0) {
-      a.bnd = h->gbB;
-      a.hi_off = h->plane;
-    }
-    int rc = launch_sweep(a, axis, st);
-    if (rc) return rc;
-  }
-  h->st_idx = other;
-  h->step = s;
-  return PBG_OK;
-}
-
-extern "C" PBG_API int pbg_slab_flag_pack(pbg_slab* h, void* stream) {
-  if (!h) return fail(PBG_E_INVALID, "null slab");
-  PBG_CUDA(cudaMemcpyAsync(h->send + 4 * h->plane, h->dflag, sizeof(int),
-                           cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
-  return PBG_OK;
-}
-
-extern "C" PBG_API int pbg_slab_finish(pbg_slab* h, int32_t* steps_taken,
-                                       int32_t* diverged_step, int32_t* result_slot,
-                                       void* stream) {
-  if (!h) return fail(PBG_E_INVALID, "null slab");
-  cudaStream_t st = (cudaStream_t)stream;
-  std::vector<int> flags(h->nranks);
-  for (int r = 0; r < h->nranks; ++r)
-    PBG_CUDA(cudaMemcpyAsync(&flags[r], h->recv + r * h->E + 4 * h->plane, sizeof(int),
-                             cudaMemcpyDeviceToHost, st));
-  int local = INT_MAX;
-  PBG_CUDA(cudaMemcpyAsync(&local, h->dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  PBG_CUDA(cudaStreamSynchronize(st));
-  int dstep = local;
-  for (int f : flags) dstep = std::min(dstep, f);
-  const int nsteps = h->step;
-  int taken = nsteps;
-  if (h->d.check_divergence && dstep != INT_MAX) taken = std::min(dstep, nsteps);
-  if (diverged_step) *diverged_step = (h->d.check_divergence && dstep != INT_MAX) ? taken : 0;
-  int slot;
-  if (h->st0 < 0) slot = (taken - 1) % 2;
-  else slot = (h->st0 + taken) % 2;
-  if (steps_taken) *steps_taken = taken;
-  if (result_slot) *result_slot = slot;
-  return PBG_OK;
-}

@@ -2,8 +2,8 @@
 
 API mirror of pbsplit/schemes.py.  `march`, `step`, `Stepper.step`, `ie_sweep`, `cn_sweep`,
 `nonlinear_step` and `source_step` run the hand-written sm_100a kernels of libpbg.so
-(north_star items 2-4); there is no CPU fallback.  ADI1/ADI2/ExplicitEuler are comparison
-schemes outside the LOD/AOS hot path and are not on the device yet.
+(north_star items 2-4); there is no CPU fallback.  The comparison schemes ADI1/ADI2/
+ExplicitEuler use the same device march (schemes_extra.cu).
 """
 
 from __future__ import annotations
@@ -39,7 +39,7 @@ class SchemeVariant(str, enum.Enum):
 
 SCHEME_NAMES = tuple(v.value for v in SchemeVariant)
 SPLITTING_SCHEMES = tuple(n for n in SCHEME_NAMES if n.startswith(("LOD", "AOS", "MAOS")))
-DEVICE_SCHEMES = SPLITTING_SCHEMES
+DEVICE_SCHEMES = SCHEME_NAMES
 
 
 def parse_variant(name) -> SchemeVariant:
@@ -130,9 +130,6 @@ def device_problem(problem) -> DeviceProblem:
 def _run_march(problem, variant, dt, alpha, nsteps, threshold, aos_literal, check_div,
                initial_dev=None):
     v = parse_variant(variant)
-    if v.value not in DEVICE_SCHEMES:
-        raise NotImplementedError(f"{v.value} is a comparison scheme outside the LOD/AOS "
-                                  "device path (SURVEY.md §8f)")
     dp = device_problem(problem)
     w0, w1 = dp.work_pair()
     init = initial_dev if initial_dev is not None else problem.initial._device()

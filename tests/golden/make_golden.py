@@ -221,10 +221,35 @@ def vacuum_case():
     save("vacuum", **out)
 
 
+def comparison_cases():
+    """ADI1 / ADI2 / ExplicitEuler (schemes.py:240-253, 331-363) on the march_variants
+    problem: ADI at the splitting step size, Euler at a stable step, plus an Euler run that
+    diverges (threshold stop)."""
+    atoms = synthetic_atoms(8, 2.5, 21)
+    prob = pb.protein_problem(system_of(atoms), h=0.5, padding=3.0, kappa_bar=1.0,
+                              eps_m=2.0, eps_s=80.0)
+    out = dict(atoms=np.array(atoms), padding=3.0, kappa_bar=1.0, eps_m=2.0, eps_s=80.0,
+               **grid_meta(prob.grid))
+    for v in ("ADI1", "ADI2"):
+        rep = march(prob, MarchConfig(dt=0.3, T=1.5, variant=v))
+        out[v] = rep.final.data
+        out[v + "_steps"] = rep.steps_taken
+    rep = march(prob, MarchConfig(dt=2e-4, T=2e-2, variant="ExplicitEuler"))
+    out["Euler"] = rep.final.data
+    out["Euler_steps"] = rep.steps_taken
+    rep = march(prob, MarchConfig(dt=0.01, T=1.0, variant="ExplicitEuler",
+                                  divergence_threshold=1e6))
+    out["Euler_div_final"] = rep.final.data
+    out["Euler_div_steps"] = rep.steps_taken
+    out["Euler_div_step"] = -1 if rep.diverged_step is None else rep.diverged_step
+    save("comparison", **out)
+
+
 CASES = {"assembly": lambda: (assembly_case("a40", 40, 5.0, 11, 0.5, 4.0, 0.0, 1.1283),
                               assembly_case("a60_probe", 60, 6.0, 12, 0.4, 4.0, 1.4, 0.9212)),
          "march": march_cases, "small_api": small_api_cases, "sphere": sphere_case,
-         "energy": energy_case, "kirkwood": kirkwood_case, "vacuum": vacuum_case}
+         "energy": energy_case, "kirkwood": kirkwood_case, "vacuum": vacuum_case,
+         "comparison": comparison_cases}
 
 if __name__ == "__main__":
     for name in (sys.argv[1:] or list(CASES)):

@@ -126,3 +126,20 @@ def test_vacuum_direct_solver_and_plain_re_energies():
             dg, _, _, div = O.energy_direct(p, v, 0.5, 5.0, mode)
             want = float(d[f"dg_{mode}_{v}"])
             assert not div and abs(dg - want) <= 1e-10 * abs(want)
+
+
+def test_comparison_schemes_vs_reference():
+    """ADI1 / ADI2 / ExplicitEuler (schemes.py:240-253, 331-363) against comparison.npz."""
+    d = golden("comparison")
+    p = oracle_protein(d)
+    for v in ("ADI1", "ADI2"):
+        rep = O.march(p, v, 0.3, 1.5)
+        assert rep.steps_taken == int(d[v + "_steps"])
+        assert rel_err(rep.final, d[v]) <= 1e-13
+    rep = O.march(p, "ExplicitEuler", 2e-4, 2e-2)
+    assert rep.steps_taken == int(d["Euler_steps"]) and not rep.diverged
+    assert rel_err(rep.final, d["Euler"]) <= 1e-13
+    rep = O.march(p, "ExplicitEuler", 0.01, 1.0, threshold=1e6)
+    assert rep.diverged and rep.diverged_step == int(d["Euler_div_step"])
+    assert rep.steps_taken == int(d["Euler_div_steps"])
+    assert rel_err(rep.final, d["Euler_div_final"]) <= 1e-13
