@@ -251,6 +251,28 @@ CASES = {"assembly": lambda: (assembly_case("a40", 40, 5.0, 11, 0.5, 4.0, 0.0, 1
          "energy": energy_case, "kirkwood": kirkwood_case, "vacuum": vacuum_case,
          "comparison": comparison_cases}
 
+
+
+sys.path.insert(0, HERE)
+from make_golden_cases import CLI_CASES  # noqa: E402
+
+
+def cli_cases():
+    """CSV reports of the reference CLI (cli.py) for small ladders -> tests/golden/cli/."""
+    from pbsplit.cli import main as ref_main
+
+    d = os.path.join(HERE, "cli")
+    sysf = os.path.join(d, "mini.sys")
+    for name, argv in CLI_CASES.items():
+        argv = [sysf if a == "SYS" else a for a in argv]
+        out = os.path.join(d, name + ".csv")
+        rc = ref_main(argv + ["--out", out])
+        print(name, "rc", rc, os.path.getsize(out))
+
+
+CASES["cli"] = cli_cases
+
+
 if __name__ == "__main__":
     for name in (sys.argv[1:] or list(CASES)):
         CASES[name]()
