@@ -193,14 +193,19 @@ __device__ __forceinline__ void uni_finish(const double (&r)[S], Tab tab, double
   for (int j = 0; j < S - 1; ++j) w0[j * WS] = fma(tab(TQ_BE, j), t, fma(tab(TQ_AL, j), tm, r[j]));
 }
 
-// Table type of a segment whose S nodes carry the same eps bit: 0 interior, 1 first, 2 last
-// (separator is the padding row m); -1 if the segment must be eliminated on the fly.
+// Table type of a segment whose S nodes carry the same eps bit; -1 if it must use its own
+// precomputed factors.  The first segment and a last segment whose separator is the padding
+// row m both use the interior tables (type 0): the first segment's missing left separator is
+// zero, which makes the interior table's extra sub-diagonal term vanish exactly, and the
+// padding separator's right-hand side is zeroed (seg_eliminate) so its coupling to row m-1
+// multiplies zero.  Results are bit-identical to the dedicated first / last tables, and
+// warps made only of solvent segments take the parameter-table path wherever they sit.
 template <int S>
 __device__ __forceinline__ int seg_type(unsigned long long amask, int i0, int m, int first) {
   const unsigned long long allm = (1ull << S) - 1ull, bits = amask & allm;
   if (bits != 0ull && bits != allm) return -1;
-  if (i0 + S <= m) return first ? 1 : 0;
-  if (i0 + S - 1 == m && !first) return 2;
+  if (i0 + S <= m) return 0;
+  if (i0 + S - 1 == m && !first) return 0;
   return -1;
 }
 
@@ -222,7 +227,7 @@ __device__ __forceinline__ const double* seg_eliminate(const SweepArgs& a, doubl
                                                        int first, const double* T, SegOut& o) {
   const int m = a.m;
   const int ttype = seg_type<S>(amask, i0, m, first);
-  o.rs = r[S - 1];
+  o.rs = i0 + S - 1 < m ? r[S - 1] : 0.0;  // a padding separator carries zero
   row_coefs(a.co, i0 + S - 1, m, (uint32_t)(amask >> (S - 1)) & 1u,
             (uint32_t)(amask >> S) & 1u, o.as, o.bs, o.cs);
   if (__all_sync(0xffffffffu, ttype == 0 && !(amask & 1ull))) {
