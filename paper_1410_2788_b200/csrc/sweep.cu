@@ -373,7 +373,10 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
   const double* gy_all = needY == 1 ? a.src : a.acc;
   if (tid < 4) FP[tid] = tid == 0 ? a.decay0 : (tid == 1 ? a.sat0 : (tid == 2 ? a.decay1 : a.sat1));
 
-  // Phase 1: asynchronous staging of the field (+ epilogue operand), descriptors, tables.
+  // Phase 1: asynchronous staging of the own descriptor (first group), then of the field
+  // (+ epilogue operand) and tables.
+  cp_async16(D + 2 * tid, a.desc + 2 * (((long long)(outer - 1) * kSegS + seg) * K + (c0 - 1 + lane)));
+  asm volatile("cp.async.commit_group;\n" ::);
   if (RT) {
     // rows 1..m+1 of each line in 16-byte chunks (row 1 is 256-byte aligned), row 0 alone
     const int nch = (m + 1) / 2;  // full chunks; an odd last row goes alone
@@ -417,12 +420,34 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
     }
     for (int c = nl * LB + tid; c < NR * LB; c += NT) W[c] = 0.0;  // rows past the far face
   }
-  cp_async16(D + 2 * tid, a.desc + 2 * (((long long)(outer - 1) * kSegS + seg) * K + (c0 - 1 + lane)));
   for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
   if (a.static_ok)
     for (int c = tid; c < kSegS * kSegS / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
   if (a.pro == PRO_FLOW || a.epi == EPI_FLOW || a.epi == EPI_AOS0)
     for (int c = tid; c < kFlowTabDoubles / 2; c += NT) cp_async16(FP + 4 + 2 * c, a.ftab + 2 * c);
+  asm volatile("cp.async.commit_group;\n" ::);
+  // A general segment reads its precomputed factors from global memory: bring the five rows
+  // of its table towards L1 while the tile is still in flight.
+  // Same for the Dirichlet values of the line ends and the source at charged nodes.
+  asm volatile("cp.async.wait_group 1;\n" ::);
+  double bfold = 0.0;
+  if (lane < ncols) {
+    const unsigned long long slot = D[2 * tid] >> kSlotShift;
+    if (slot) {
+      const double* f = a.gfac + (long long)(slot - 1) * 5 * kTabRows;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) asm volatile("prefetch.global.L1 [%0];" ::"l"(f + q * kTabRows));
+    }
+    unsigned cm = (unsigned)(D[2 * tid + 1] >> 32);
+    const double* rr = a.rho + lb(lane) + (long long)(seg * S + 1) * stride;
+    while (cm) {
+      const int j = __ffs(cm) - 1;
+      cm &= cm - 1;
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(rr + (long long)j * stride));
+    }
+    if (seg == 0) bfold = a.bnd[lb(lane)];
+    else if (seg == (m - 1) / S) bfold = a.bnd[lb(lane) + a.hi_off];
+  }
   cp_async_wait_all();
   __syncthreads();
   if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
@@ -482,8 +507,9 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
         if ((cmask >> j) & 1u) r[j] = __dadd_rn(r[j], __dmul_rn(a.extra, *rho_row(j)));
     }
     if (seg == 0 && active)
-      r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], a.bnd[gl]));
-    if (seg == (m - 1) / S && active) fold_high<S>(a, r, amask, a.bnd[gl + a.hi_off]);
+      r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], bfold));
+    if (seg == (m - 1) / S && active)
+      fold_high<S>(a, r, amask, seg == 0 ? a.bnd[gl + a.hi_off] : bfold);
     // clean tile: every line of the tile is one dielectric (palette 0) end to end
     const bool clean = __syncthreads_and(!active || eps_bits(amask, S) == 0ull) && a.static_ok;
 
