@@ -1,0 +1,87 @@
+"""Dev tool: turn gpurun_out captures into the committed profile summaries.
+
+    python scripts/summarize_profiles.py TAG   (reads gpurun_out/{launches_TAG.csv,
+    c4_full_TAG.ncu-rep, bench_*.json}; writes profiles/*_TAG*)
+"""
+import collections, csv, io, json, os, subprocess, sys
+
+tag = sys.argv[1]
+root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+out = os.path.join(root, "profiles")
+go = os.path.join(root, "gpurun_out")
+NODES = 133432831
+
+# bench lines
+lines = []
+for name in ("bench_c4.json", "bench_c3.json", "bench_ref.json", "bench_c5.json", "bench_slab1.json"):
+    p = os.path.join(go, name)
+    if os.path.exists(p):
+        lines += [ln for ln in open(p).read().splitlines() if ln.startswith("{")]
+open(os.path.join(out, f"bench_{tag}.jsonl"), "w").write("\n".join(lines) + "\n")
+
+# launch list
+rows = [r for r in csv.reader(open(os.path.join(go, f"launches_{tag}.csv"))) if len(r) > 5]
+hdr = rows[0]
+ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+agg = collections.OrderedDict()
+for r in rows[1:]:
+    a = agg.setdefault(r[ki], [0, 0.0])
+    a[0] += 1
+    a[1] += float(r[vi].replace(",", "")) * scale[r[ui]]
+sweeps = {k: v for k, v in agg.items() if "k_sweep" in k}
+tot, tsw = sum(a[1] for a in agg.values()), sum(a[1] for a in sweeps.values())
+md = [f"# ncu launch list, {tag}", "",
+      "Command: `ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python "
+      "bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e` (config c4, 513^3, LODIE2).",
+      "Per-launch times are cold-cache and serialised; compare shares with `roofline.kernel_ms` "
+      f"in `bench_{tag}.jsonl`.", "",
+      "| kernel | launches | total us | mean us | share of all kernel time | share of sweep time |",
+      "|---|---|---|---|---|---|"]
+for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    sh = f"{t / tsw * 100:.1f}%" if k in sweeps else "-"
+    md.append(f"| `{k[:80]}` | {n} | {t:.1f} | {t / n:.1f} | {t / tot * 100:.1f}% | {sh} |")
+md += ["", "Setup kernels (`k_coulomb_faces`, `k_classify_*`, `k_build_desc`, `k_seg_factors`) run "
+       "once per problem / march, outside the timed step loop."]
+open(os.path.join(out, f"launches_{tag}_summary.md"), "w").write("\n".join(md) + "\n")
+os.replace(os.path.join(go, f"launches_{tag}.csv"), os.path.join(out, f"launches_{tag}.csv"))
+
+# full capture
+raw = subprocess.run(["ncu", "-i", os.path.join(go, f"c4_full_{tag}.ncu-rep"), "--page", "raw",
+                      "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units = rows[0], rows[1]
+g = lambda r, k: r[hdr.index(k)]
+md = [f"# ncu --set full, {tag}", "",
+      "Command: `ncu --set full --clock-control none --import-source on -k regex:k_sweep -s 9 -c 3 "
+      "python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e` (c4, LODIE2; one launch "
+      "per sweep axis; cold-cache serialised replays).", "",
+      "| kernel | duration us | DRAM read GB | DRAM write GB | DRAM busy % | SM busy % | warps "
+      "active % | regs | thread-instr / node | fp64 pipe % | top stalls (cycles/issue) |",
+      "|---|---|---|---|---|---|---|---|---|---|---|"]
+traffic = {}
+stall = [i for i, h in enumerate(hdr) if h.startswith("smsp__average_warps_issue_stalled_")
+         and h.endswith("_per_issue_active.ratio")]
+for ax, r in enumerate(rows[2:5]):  # the capture holds K0, K1, K2 of one step, in order
+    name = g(r, "Kernel Name")
+    rd, wr = float(g(r, "dram__bytes_read.sum")), float(g(r, "dram__bytes_write.sum"))
+    mult = 1e9 if units[hdr.index("dram__bytes_read.sum")] == "Gbyte" else 1e6
+    traffic[str(ax)] = (rd + wr) * mult
+    st = sorted([(float(r[i]) if r[i] else 0.0, hdr[i]) for i in stall], reverse=True)[:3]
+    sts = ", ".join(f"{h.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')} {v:.1f}" for v, h in st)
+    md.append(f"| `{name}` | {float(g(r, 'gpu__time_duration.sum')):.0f} | {rd * mult / 1e9:.3f} | "
+              f"{wr * mult / 1e9:.3f} | {float(g(r, 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed')):.1f} | "
+              f"{float(g(r, 'sm__throughput.avg.pct_of_peak_sustained_elapsed')):.1f} | "
+              f"{float(g(r, 'sm__warps_active.avg.pct_of_peak_sustained_active')):.1f} | "
+              f"{g(r, 'launch__registers_per_thread')} | "
+              f"{float(g(r, 'smsp__inst_executed.sum')) * 32 / NODES:.1f} | "
+              f"{float(g(r, 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active')):.1f} | {sts} |")
+md += ["", "Template arguments: `<S, P, CN, LB, RT>` = rows per segment, segments per line, "
+       "Crank-Nicolson, lines per tile, row tiles.  Algorithmic bytes per sweep launch: 16 B x "
+       "133,432,831 interior nodes = 2.135 GB."]
+open(os.path.join(out, f"ncu_{tag}_summary.md"), "w").write("\n".join(md) + "\n")
+tr = json.load(open(os.path.join(out, "ncu_traffic.json")))
+tr["c4-protein10000-513"] = traffic
+tr["_note"] = f"dram read+write bytes per launch by sweep axis, ncu --set full capture {tag}"
+json.dump(tr, open(os.path.join(out, "ncu_traffic.json"), "w"), indent=1)
+print("\n".join(md))
