@@ -1071,8 +1071,12 @@ template <int S, int P, bool CN>
 static void launch_strided_SC(const SweepArgs& a, int axis, cudaStream_t st) {
   // 16-column tiles (128-byte row chunks) unless a second staged tile (AOS/MAOS epilogue
   // operand) would halve the resident blocks.
-  const bool wide = epi_needs(a.epi) == 0;
-  if (axis == 0) launch_strided_SCL<S, P, CN, 16, false>(a, axis, st);
+  // Tiles must also fit the 227 KB of shared memory per block (long lines with AOS/MAOS).
+  const bool needY = epi_needs(a.epi) != 0;
+  const bool wide = !needY;
+  const bool fits16 = strided_smem<16, false>(S, P, needY) <= 232448;
+  if (axis == 0 && fits16) launch_strided_SCL<S, P, CN, 16, false>(a, axis, st);
+  else if (axis == 0) launch_strided_SCL<S, P, CN, 8, false>(a, axis, st);
   else if (axis == 1 && wide) launch_strided_SCL<S, P, CN, 16, false>(a, axis, st);
   else if (axis == 1) launch_strided_SCL<S, P, CN, 8, false>(a, axis, st);
   else launch_strided_SCL<S, P, CN, 8, true>(a, axis, st);

@@ -1,0 +1,62 @@
+"""Ragged and extreme line lengths: every tile geometry (P = 8/16/32 segments, S from 2 to
+32, padding segments, row tiles, the longest supported line m = 1024, the single-node grid)
+against the CPU oracle on an off-centre dielectric sphere with a random sparse source and
+random Dirichlet faces; lines longer than 1024 interior nodes are refused loudly."""
+
+import numpy as np
+import pytest
+
+import paper_1410_2788_b200 as pb
+from oracle import pbs_oracle as O
+from tests.helpers import rel_err
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(3, 3, 3), (4, 5, 6), (18, 19, 20), (131, 10, 9), (9, 260, 11), (7, 8, 600),
+          (6, 390, 5), (1026, 5, 5)]
+VARIANTS = ["LODIE1", "LODCN2", "AOSCN1", "MAOSIE", "ADI2"]
+
+
+def problems(shape, seed=0):
+    h = 0.25
+    lo = (-0.35 * (shape[0] - 1) * h, -0.6 * (shape[1] - 1) * h, -0.45 * (shape[2] - 1) * h)
+    hi = tuple(lo[a] + (shape[a] - 1) * h for a in range(3))
+    g = pb.make_grid(lo, hi, h)
+    assert g.shape == shape
+    R = 0.3 * min(hi[a] - lo[a] for a in range(3)) + 0.3
+    rng = np.random.default_rng(seed)
+    bvals = rng.standard_normal(shape)
+    rho = np.zeros(shape)
+    idx = tuple(rng.integers(1, max(2, s - 1), size=7) for s in shape)
+    rho[idx] = rng.standard_normal(7) * 5.0
+    region = pb.build_region_maps(g, pb.AnalyticSphere(R), 2.0, 80.0, 1.3)
+    init = np.zeros(shape)
+    bspec = pb.BoundarySpec(g, bvals)
+    bspec.apply(init)
+    p = pb.NPBProblem(grid=g, region=region, rho=pb.ScalarField(g, rho),
+                      qfrac=pb.ScalarField.zeros(g), boundary=bspec, alpha=1.0,
+                      initial=pb.ScalarField(g, init), eps_m=2.0, eps_s=80.0, kappa_bar=1.14)
+    og = O.OGrid(g.lo, g.h, shape)
+    op = O.OProblem(og, O.sphere_region(og, R, 2.0, 80.0, 1.3), rho, np.zeros(shape), bvals,
+                    1.0, init.copy(), 2.0, 80.0, 1.14)
+    return p, op
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_ragged_shapes_vs_oracle(shape):
+    p, op = problems(shape)
+    for v in VARIANTS:
+        rep = pb.march(p, pb.MarchConfig(dt=0.2, T=0.6, variant=v))
+        orep = O.march(op, v, 0.2, 0.6)
+        assert rep.steps_taken == orep.steps_taken == 3, v
+        assert rel_err(rep.final.data, orep.final) <= 1e-12, (shape, v)
+
+
+def test_line_longer_than_supported_is_refused():
+    g = pb.make_grid((0, 0, 0), (0.25 * 1026, 0.75, 0.75), 0.25)  # m = 1025 along x
+    p = pb.NPBProblem(grid=g, region=pb.uniform_region(g, 1.0, 0.0),
+                      rho=pb.ScalarField.zeros(g), qfrac=pb.ScalarField.zeros(g),
+                      boundary=pb.BoundarySpec(g, np.zeros(g.shape)), alpha=1.0,
+                      initial=pb.ScalarField.zeros(g), eps_m=1.0, eps_s=1.0)
+    with pytest.raises(NotImplementedError):
+        pb.march(p, pb.MarchConfig(dt=0.1, T=0.1, variant="LODIE2"))
