@@ -7,27 +7,24 @@
 // the tridiagonal rows are  sub = -f*e_minus, diag = 1 + f*(e_plus + e_minus),
 // sup = -f*e_plus  (tridiag.py:165, 179-181), with the static Dirichlet fold-ins on the
 // first/last row (tridiag.py:193-202).  The reference runs one serial Thomas per line with
-// stored LU factors (3 x 8 B/node of coefficient traffic per sweep).  Here each line is split
-// into 32 segments of S rows (S = ceil(m/32)), one thread per segment:
+// stored LU factors.  Here each line is split into P segments of S rows (S = 16, P = 8/16/32;
+// S = 32 for lines longer than 512), one thread per segment:
 //
 //   * rows j < S-1 of a segment are "inner", row S-1 is a separator t_k; inner unknowns are
 //     x_j = y_j + alpha_j * t_{k-1} + beta_j * t_k  (one elimination, three right-hand sides);
-//   * the 32 separators of a line satisfy a diagonally dominant tridiagonal "reduced" system,
-//     solved by parallel cyclic reduction (5 steps: warp shuffles on the contiguous axis,
-//     shared memory on the strided axes);
-//   * alpha/beta and the LU factors of a segment depend only on the coefficient codes, so a
-//     segment whose S nodes all carry the same dielectric ("uniform", >90% of segments in the
-//     protein configs) reads them from a per-axis table built once per launch: 5 fp64 ops per
-//     node and no reciprocal.  Other segments ("general") eliminate on the fly with their
-//     per-row state in shared memory and L1-resident local arrays.
+//   * the P separators of a line satisfy a diagonally dominant tridiagonal "reduced" system,
+//     solved with a precomputed dense inverse on lines of one dielectric ("clean"), by
+//     parallel cyclic reduction in shared memory otherwise;
+//   * alpha/beta and the LU factors of a segment depend only on the coefficient codes: a
+//     segment whose nodes carry one dielectric ("uniform", >90% in the protein configs) reads
+//     them from per-axis tables (the dominant kind from kernel parameters = constant bank),
+//     other segments from factors precomputed once per march (k_seg_factors).
 //
-// Data movement: every block stages its lines through shared memory with asynchronous copies
-// (LDGSTS, the whole tile in flight at once): strided axes stage a tile of 8 adjacent k
-// columns x the whole line (each row segment 64 contiguous bytes), the contiguous axis one row
-// per warp.  The prologue is applied in the staging pass, the line is solved from shared
-// memory, and the epilogue runs in the coalesced store pass.  Geometry (S, 32 segments, 8
-// columns) is compile time, offsets are 32-bit; the transcendental prologue / epilogue live in
-// rolled loops so the unrolled solver stays small.
+// Data movement: every block stages a tile of LB lines x the whole line through shared memory
+// with asynchronous copies (LDGSTS).  Axes 0/1 ("column tiles"): LB adjacent k columns, each
+// row of the tile one 64/128-byte run.  Axis 2 ("row tiles"): LB adjacent (i, j) lines, each
+// a contiguous row.  The prologue is applied in the staging pass, the line is solved from
+// shared memory / registers, and the epilogue runs in the coalesced store pass.
 //
 // Prologue / epilogue fusions:
 //   PRO_FLOW  w = pm*flow(u)         LODIE1/LODCN1 first sweep, MAOS branches
@@ -68,25 +65,11 @@ __host__ __device__ __forceinline__ int epi_needs(int epi) {
                                 : 0);
 }
 
-// One inlined flow evaluation: select the palette constants first (a ternary over two calls
-// is if-converted by the compiler into two full evaluations).
-__device__ __forceinline__ double flow_at(const SweepArgs& a, double w, uint32_t c, double pm) {
-  const bool s = (c & 1u) != 0;
-  return sinh_flow_fast(w, s ? a.decay1 : a.decay0, s ? a.sat1 : a.sat0, pm);
-}
-
 // Flow palette constants staged in shared memory as (decay, sat) pairs indexed by the solute
 // bit: one 16-byte load per node instead of predicated constant-bank selects.
 __device__ __forceinline__ double flow_sm(const double* FP, double w, uint32_t s, double pm) {
   const double2 v = reinterpret_cast<const double2*>(FP)[s];
   return sinh_flow_tab(w, v.x, v.y, pm, FP + 4);
-}
-
-__device__ __forceinline__ double pro_val(const SweepArgs& a, double v, uint32_t c,
-                                          const double* rho_at) {
-  if (a.pro == PRO_FLOW) return flow_at(a, v, c, a.pm);
-  if (a.pro == PRO_SRC && (c & 16u)) return __dadd_rn(v, __dmul_rn(a.pro_coef, *rho_at));
-  return v;
 }
 
 __device__ __forceinline__ void row_coefs(const AxisCoef& co, int i, int m, uint32_t em,
@@ -100,29 +83,6 @@ __device__ __forceinline__ void row_coefs(const AxisCoef& co, int i, int m, uint
   av = (i == 0) ? 0.0 : (em ? co.sub[1] : co.sub[0]);
   cv = (i == m - 1) ? 0.0 : (ep ? co.sup[1] : co.sup[0]);
   bv = em ? (ep ? co.diag[3] : co.diag[2]) : (ep ? co.diag[1] : co.diag[0]);
-}
-
-// Epilogue for the final value x at a node (schemes.py:309-311, 322, 329); y is the
-// prefetched raw field (AOS0) or accumulator (AOS1/2, MAOS1/2) at the node.
-__device__ __forceinline__ double epi_val(const SweepArgs& a, double x, double y, uint32_t c,
-                                          const double* rho_at) {
-  switch (a.epi) {
-    case EPI_SRC:
-      return (c & 16u) ? __dadd_rn(x, __dmul_rn(a.epi_coef, *rho_at)) : x;
-    case EPI_FLOW:
-      return flow_at(a, x, c, 1.0);
-    case EPI_AOS0:
-      return __dadd_rn(flow_at(a, y, c, a.pm), x);
-    case EPI_AOS1:
-    case EPI_MAOS1:
-      return __dadd_rn(y, x);
-    case EPI_AOS2:
-      return __dmul_rn(0.25, __dadd_rn(y, x));
-    case EPI_MAOS2:
-      return __ddiv_rn(__dadd_rn(y, x), 3.0);
-    default:
-      return x;
-  }
 }
 
 // Reciprocal of a well-conditioned positive pivot: MUFU seed + two Newton steps (~1 ulp,
@@ -680,269 +640,26 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
 }
 
 // ---------------------------------------------------------------------------------------
-// Contiguous axis (2): one warp per (i, j) line, lane = segment of S rows.  The row lives in
-// shared memory with one pad slot per S nodes (S even) so lanes read their rows without bank
-// conflicts.
-template <int S>
-__host__ __device__ constexpr int cpos(int p) {
-  return (S % 2 == 0) ? p + p / S : p;
-}
-
-template <int S>
-__host__ __device__ constexpr int contig_buf_doubles() {
-  return ((cpos<S>(32 * S + 2) + 2) + 1) & ~1;
-}
-
-constexpr int kContigWarps = 8;
-
-// Stage one row into a warp's buffers: field (+ epilogue operand) by cp.async, zero past the
-// far face.  Returns nothing; the caller commits the cp.async group.
-template <int S>
-__device__ __forceinline__ void contig_stage(const SweepArgs& a, int line, int needY, int lane,
-                                             double* buf, double* ybuf) {
-  const Layout& L = a.L;
-  const int n2 = L.n2;
-  const long long rb = L.at(1 + line / (L.n1 - 2), 1 + line % (L.n1 - 2), 0);
-  const double* gsrc = a.src + rb;
-#pragma unroll 4
-  for (int e = lane; e < n2; e += 32) cp_async8(buf + cpos<S>(e), gsrc + e);
-  if (needY) {
-    const double* gy = (needY == 1 ? a.src : a.acc) + rb;
-#pragma unroll 4
-    for (int e = lane; e < n2; e += 32) cp_async8(ybuf + e, gy + e);
-  }
-  for (int e = n2 + lane; e <= 32 * S + 1; e += 32) buf[cpos<S>(e)] = 0.0;
-}
-
-// Solve one staged row (warp-wide) and store it.  Returns the lane's divergence flag.
-template <int S, bool CN>
-__device__ __forceinline__ bool contig_solve(const SweepArgs& a, int line, int lane,
-                                             const double* T, const double* Mi, double* buf,
-                                             const double* ybuf, double* sR,
-                                             unsigned long long dw0, unsigned long long dw1,
-                                             int needY) {
-  const Layout& L = a.L;
-  const int m = a.m, n2 = L.n2;
-  const long long rb = L.at(1 + line / (L.n1 - 2), 1 + line % (L.n1 - 2), 0);
-  const double* grho = a.rho + rb;
-  const int i0 = lane * S;
-  const unsigned long long amask = dw0;
-  const unsigned cmask = (unsigned)(dw1 >> 32);
-  double* w0 = buf + cpos<S>(i0 + 1);
-  auto rho_row = [&](int j) { return grho + i0 + j + 1; };
-  if (a.pro == PRO_FLOW) {
-    if (lane < 2) {  // flow stages see the Dirichlet faces
-      const int e = lane ? n2 - 1 : 0;
-      buf[cpos<S>(e)] = a.bnd[rb + e];
-    }
-    for (int e0 = 1; e0 < n2 - 1; e0 += 32) {  // warp-uniform trip count (shuffles inside)
-      const int e = e0 + lane;
-      const int sg = min((e - 1) / S, kSeg - 1);
-      const uint32_t c = node_bits(__shfl_sync(0xffffffffu, dw1, sg), (e - 1) - sg * S);
-      if (e < n2 - 1) buf[cpos<S>(e)] = flow_at(a, buf[cpos<S>(e)], c, a.pm);
-    }
-    __syncwarp();
-  } else if (a.pro == PRO_SRC) {
-    if (cmask)
-      charged_fixup(cmask, a.pro_coef, [&](int j) { return buf + cpos<S>(i0 + 1 + j); }, rho_row);
-    __syncwarp();
-  }
-
-  double r[S];
-#pragma unroll
-  for (int j = 0; j < S; ++j) {
-    const int p = i0 + j + 1;
-    const double wc = buf[cpos<S>(p)];
-    r[j] = CN ? cn_term(a, (uint32_t)(amask >> j) & 1u, (uint32_t)(amask >> (j + 1)) & 1u,
-                        buf[cpos<S>(p - 1)], wc, buf[cpos<S>(p + 1)])
-              : wc;
-  }
-  if (a.has_extra && cmask) {
-#pragma unroll
-    for (int j = 0; j < S; ++j)
-      if ((cmask >> j) & 1u) r[j] = __dadd_rn(r[j], __dmul_rn(a.extra, *rho_row(j)));
-  }
-  if (lane == 0) r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], a.bnd[rb]));
-  if (lane == (m - 1) / S) fold_high<S>(a, r, amask, a.bnd[rb + m + 1]);
-  const bool clean = __all_sync(0xffffffffu, eps_bits(amask, S) == 0ull) && a.static_ok;
-  __syncwarp();
-
-  SegOut o;
-  const double* Tv = seg_eliminate<S>(a, r, amask, i0, lane == 0, T, o);
-
-  const double yFn0 = __shfl_down_sync(0xffffffffu, o.yF, 1);
-  double t, tm;
-  if (clean) {  // static inverse of the clean-line reduced system
-    sR[lane] = o.rs - o.as * o.yL - o.cs * (lane == 31 ? 0.0 : yFn0);
-    __syncwarp();
-    const int k1 = lane > 0 ? lane - 1 : 0;  // transposed inverse: column q at Mi[q*32]
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll 8
-    for (int q = 0; q < kSeg; ++q) {
-      const double Rq = sR[q];  // broadcast
-      s0 = fma(Mi[q * kSeg + lane], Rq, s0);
-      s1 = fma(Mi[q * kSeg + k1], Rq, s1);
-    }
-    t = s0;
-    tm = lane > 0 ? s1 : 0.0;
-  } else {
-    double yFn = yFn0;
-    double aFn = __shfl_down_sync(0xffffffffu, o.aF, 1);
-    double bFn = __shfl_down_sync(0xffffffffu, o.bF, 1);
-    if (lane == 31) yFn = aFn = bFn = 0.0;
-    double A, B, Cc, R;
-    reduced_row(o, yFn, aFn, bFn, A, B, Cc, R);
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const double iB = fast_rcp(B);
-      double Am = __shfl_up_sync(0xffffffffu, A, d);
-      double iBm = __shfl_up_sync(0xffffffffu, iB, d);
-      double Cm = __shfl_up_sync(0xffffffffu, Cc, d);
-      double Rm = __shfl_up_sync(0xffffffffu, R, d);
-      double Ap = __shfl_down_sync(0xffffffffu, A, d);
-      double iBp = __shfl_down_sync(0xffffffffu, iB, d);
-      double Cp = __shfl_down_sync(0xffffffffu, Cc, d);
-      double Rp = __shfl_down_sync(0xffffffffu, R, d);
-      if (lane < d) {
-        Am = 0.0;
-        iBm = 1.0;
-        Cm = 0.0;
-        Rm = 0.0;
-      }
-      if (lane + d >= 32) {
-        Ap = 0.0;
-        iBp = 1.0;
-        Cp = 0.0;
-        Rp = 0.0;
-      }
-      const double k1 = -A * iBm, k2 = -Cc * iBp;
-      A = k1 * Am;
-      Cc = k2 * Cp;
-      B = B + k1 * Cm + k2 * Ap;
-      R = R + k1 * Rm + k2 * Rp;
-    }
-    t = R * fast_rcp(B);
-    tm = __shfl_up_sync(0xffffffffu, t, 1);
-    if (lane == 0) tm = 0.0;
-  }
-
-  seg_finish<S, 1>(a, Tv, r, tm, t, w0);
-  if (i0 + S - 1 < m) buf[cpos<S>(i0 + S)] = t;
-  if (a.epi == EPI_SRC && cmask)
-    charged_fixup(cmask, a.epi_coef, [&](int j) { return buf + cpos<S>(i0 + 1 + j); }, rho_row);
-  __syncwarp();
-
-  bool bad = false;
-  double* gdst = a.dst + rb;
-  const int epi = a.epi;
-  if (epi == EPI_STORE || epi == EPI_SRC || epi == EPI_MAOS0) {
-    if (a.check) {
-      for (int p = lane + 1; p <= m; p += 32) {
-        const double x = buf[cpos<S>(p)];
-        gdst[p] = x;
-        bad |= is_bad(x, a.thr);
-      }
-    } else {
-      for (int p = lane + 1; p <= m; p += 32) gdst[p] = buf[cpos<S>(p)];
-    }
-  } else if (epi == EPI_FLOW || epi == EPI_AOS0) {
-    const bool aos0 = epi == EPI_AOS0;
-    const double pm = aos0 ? a.pm : 1.0;
-    for (int p0 = 1; p0 <= m; p0 += 32) {  // warp-uniform trip count (shuffles inside)
-      const int p = p0 + lane;
-      const int sg = min((p - 1) / S, kSeg - 1);
-      const uint32_t bits = node_bits(__shfl_sync(0xffffffffu, dw1, sg), (p - 1) - sg * S);
-      if (p <= m) {
-        const double xs = buf[cpos<S>(p)];
-        const double f = flow_at(a, aos0 ? ybuf[p] : xs, bits, pm);
-        const double x = aos0 ? __dadd_rn(f, xs) : f;
-        gdst[p] = x;
-        bad |= is_bad(x, a.thr);
-      }
-    }
-  } else {
-    for (int p = lane + 1; p <= m; p += 32) {
-      const double y = ybuf[p], x0 = buf[cpos<S>(p)];
-      double x;
-      if (epi == EPI_AOS2) x = __dmul_rn(0.25, __dadd_rn(y, x0));
-      else if (epi == EPI_MAOS2) x = __ddiv_rn(__dadd_rn(y, x0), 3.0);
-      else x = __dadd_rn(y, x0);  // AOS1 / MAOS1
-      gdst[p] = x;
-      bad |= is_bad(x, a.thr);
-    }
-  }
-  return bad;
-}
-
-// One warp per row; blocks of kContigWarps rows share the staged tables.
-template <int S, bool CN>
-__global__ void __launch_bounds__(256) k_sweep_contig(const SweepArgs a, const int nlines) {
-  extern __shared__ double sm[];
-  constexpr int BUF = contig_buf_doubles<S>();
-  constexpr int W = kContigWarps;
-  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int needY = epi_needs(a.epi);
-  const int YB = needY ? 32 * S + 2 : 0;
-  double* T = sm;
-  double* Mi = T + kTabDoubles;
-  double* buf = Mi + kSeg * kSeg + warp * (BUF + YB + kSeg);
-  double* ybuf = buf + BUF;
-  double* sR = ybuf + YB;
-
-  for (int c = threadIdx.x; c < kTabDoubles / 2; c += 32 * W) cp_async16(T + 2 * c, a.tab + 2 * c);
-  if (a.static_ok)
-    for (int c = threadIdx.x; c < kSeg * kSeg / 2; c += 32 * W) cp_async16(Mi + 2 * c, a.minv + 2 * c);
-  const int line = blockIdx.x * W + warp;
-  const bool live = line < nlines;
-  unsigned long long dw0 = 0, dw1 = 0;
-  if (live) {
-    contig_stage<S>(a, line, needY, lane, buf, ybuf);
-    const unsigned long long* dp = a.desc + 2 * ((long long)line * kSeg + lane);
-    dw0 = dp[0];
-    dw1 = dp[1];
-  }
-  cp_async_wait_all();
-  __syncthreads();  // tables are shared by the block
-  if (!live || dstep < a.step) return;
-  const bool bad = contig_solve<S, CN>(a, line, lane, T, Mi, buf, ybuf, sR, dw0, dw1, needY);
-  if (a.check) {
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(a.div_step, a.step);
-  }
-}
-
-// ---------------------------------------------------------------------------------------
 // Segment descriptors, built once per march and axis from the 1-byte node codes:
 //   word 0: bit j = eps bit (axis) of the node of row i0+j, j = 0..S (zero past node m+1)
 //   word 1: bits 0..S-1 solute bit of the nodes of rows i0..i0+S-1; bits 32.. charged bits
 // Layout: strided axes ((outer-1)*32 + seg)*K + (k-1); contiguous axis line*32 + seg.
-__global__ void k_build_desc(const Layout L, int axis, int S, int P, int rows,
+__global__ void k_build_desc(const Layout L, int axis, int S, int P,
                              const uint8_t* __restrict__ codes,
                              unsigned long long* __restrict__ desc) {
   const int m = (axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2)) - 2;
-  const bool contig = axis == 2 && !rows;
-  const int K = (axis == 2 ? L.n1 : L.n2) - 2;  // lines per outer index (tile layouts)
-  long long nseg;
-  if (contig) nseg = (long long)(L.n0 - 2) * (L.n1 - 2) * kSeg;
-  else nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * K;
+  const int K = (axis == 2 ? L.n1 : L.n2) - 2;  // lines per outer index
+  const long long nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * K;
   const int sh = 1 + axis;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nseg;
        t += (long long)gridDim.x * blockDim.x) {
-    long long base, stride;
-    int seg;
-    if (contig) {
-      const long long line = t / kSeg;
-      seg = (int)(t % kSeg);
-      base = L.at(1 + (int)(line / (L.n1 - 2)), 1 + (int)(line % (L.n1 - 2)), 0);
-      stride = 1;
-    } else {
-      const int c = 1 + (int)(t % K);
-      const long long os = t / K;
-      seg = (int)(os % P);
-      const int outer = 1 + (int)(os / P);
-      base = axis == 0 ? L.at(0, outer, c) : (axis == 1 ? L.at(outer, 0, c) : L.at(outer, c, 0));
-      stride = axis == 0 ? L.s0 : (axis == 1 ? L.pitch : 1);
-    }
+    const int c = 1 + (int)(t % K);
+    const long long os = t / K;
+    const int seg = (int)(os % P);
+    const int outer = 1 + (int)(os / P);
+    const long long base =
+        axis == 0 ? L.at(0, outer, c) : (axis == 1 ? L.at(outer, 0, c) : L.at(outer, c, 0));
+    const long long stride = axis == 0 ? L.s0 : (axis == 1 ? L.pitch : 1);
     const int i0 = seg * S;
     unsigned long long w0 = 0, w1 = 0;
     for (int j = 0; j <= S; ++j) {
@@ -965,20 +682,15 @@ __global__ void k_build_desc(const Layout L, int axis, int S, int P, int rows,
 // recurrences as the uniform tables, per-row coefficients) and read like a table by the
 // sweeps.  Pass 0 counts, pass 1 assigns slots (atomic; values do not depend on the slot)
 // and writes factors + slot into descriptor word 0.
-__global__ void k_seg_factors(const Layout L, int axis, int S, int P, int rows, AxisCoef co,
-                              int pass, unsigned long long* __restrict__ desc,
-                              int* __restrict__ counter, double* __restrict__ gfac) {
+__global__ void k_seg_factors(const Layout L, int axis, int S, int P, AxisCoef co, int pass,
+                              unsigned long long* __restrict__ desc, int* __restrict__ counter,
+                              double* __restrict__ gfac) {
   const int m = (axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2)) - 2;
-  const bool contig = axis == 2 && !rows;
   const int K = (axis == 2 ? L.n1 : L.n2) - 2;
-  long long nseg;
-  if (contig) nseg = (long long)(L.n0 - 2) * (L.n1 - 2) * P;
-  else nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * K;
+  const long long nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * K;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nseg;
        t += (long long)gridDim.x * blockDim.x) {
-    int seg;
-    if (contig) seg = (int)(t % P);
-    else seg = (int)((t / K) % P);
+    const int seg = (int)((t / K) % P);
     const int i0 = seg * S, first = seg == 0;
     const unsigned long long w0 = desc[2 * t];
     const unsigned long long eb = eps_bits(w0, S);
@@ -1028,9 +740,9 @@ __global__ void k_seg_factors(const Layout L, int axis, int S, int P, int rows, 
 // ---------------------------------------------------------------------------------------
 // Host-side launch helpers.
 
-static int seg_S(int m, int P, bool tile) {
-  if (tile && P == 16) return m <= 256 ? 16 : 0;  // tile launches: S = 16 (and 32) only
-  if (tile && P == 32) return m <= 512 ? 16 : (m <= 1024 ? 32 : 0);
+static int seg_S(int m, int P) {
+  if (P == 16) return m <= 256 ? 16 : 0;  // instantiated: P = 8 with any S, 16/32 with 16/32
+  if (P == 32) return m <= 512 ? 16 : (m <= 1024 ? 32 : 0);
   const int opts[] = {2, 3, 4, 6, 8, 12, 16, 24, 32};
   for (int s : opts)
     if (P * s >= m) return s;
@@ -1038,17 +750,7 @@ static int seg_S(int m, int P, bool tile) {
 }
 // Strided axes: segments of ~16 rows (registers and occupancy balance, measured); the
 // contiguous axis always uses the 32 lanes of a warp.
-// Axis 2 runs as row tiles of the tile kernel unless PBG_AXIS2=contig (warp-per-row kernel).
-static bool axis2_rows() {
-  static const bool rows = [] {
-    const char* e = getenv("PBG_AXIS2");
-    return !(e && strcmp(e, "contig") == 0);
-  }();
-  return rows;
-}
-
 static int seg_P(int axis, int m) {
-  if (axis == 2 && !axis2_rows()) return kSeg;
   return m <= 128 ? 8 : (m <= 256 ? 16 : 32);
 }
 
@@ -1088,25 +790,6 @@ static void launch_strided_SP(const SweepArgs& a, int axis, cudaStream_t st) {
   else launch_strided_SC<S, P, false>(a, axis, st);
 }
 
-template <int S, bool CN>
-static void launch_contig_SC(const SweepArgs& a, cudaStream_t st) {
-  const int W = kContigWarps;
-  const int nlines = (a.L.n0 - 2) * (a.L.n1 - 2);
-  const size_t yb = epi_needs(a.epi) ? 32 * S + 2 : 0;
-  const size_t smem = sizeof(double) * (kTabDoubles + kSeg * kSeg) +
-                      (size_t)W * (contig_buf_doubles<S>() + yb + kSeg) * sizeof(double);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_sweep_contig<S, CN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-  k_sweep_contig<S, CN><<<(nlines + W - 1) / W, 32 * W, smem, st>>>(a, nlines);
-}
-
-template <int S>
-static void launch_contig_S(const SweepArgs& a, cudaStream_t st) {
-  if (a.cn) launch_contig_SC<S, true>(a, st);
-  else launch_contig_SC<S, false>(a, st);
-}
-
 #define PBG_DISPATCH_S(S_, CALL)                                                        \
   switch (S_) {                                                                         \
     case 2: CALL(2); break;                                                             \
@@ -1122,7 +805,7 @@ static void launch_contig_S(const SweepArgs& a, cudaStream_t st) {
   }
 
 static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
-  const int P = seg_P(axis, a.m), S = seg_S(a.m, P, true);
+  const int P = seg_P(axis, a.m), S = seg_S(a.m, P);
   if (P == 8) {
 #define PBG_STRIDED8(S) launch_strided_SP<S, 8>(a, axis, st)
     PBG_DISPATCH_S(S, PBG_STRIDED8)
@@ -1140,13 +823,6 @@ static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
   return PBG_OK;
 }
 
-static int launch_contig(const SweepArgs& a, cudaStream_t st) {
-#define PBG_CONTIG(S) launch_contig_S<S>(a, st)
-  PBG_DISPATCH_S(seg_S(a.m, kSeg, false), PBG_CONTIG)
-#undef PBG_CONTIG
-  PBG_LAUNCH_CHECK("k_sweep_contig");
-  return PBG_OK;
-}
 
 // Tridiagonal row tables for one axis: f = factor / h^2 (tridiag.py:165, 179-181, 199-202).
 static AxisCoef make_axis_coef(const double eps[2], double factor, double h) {
@@ -1298,14 +974,13 @@ SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, double 
 
 
 static long long desc_segments(const Layout& L, int axis, int P) {
-  if (axis == 2 && !axis2_rows()) return (long long)(L.n0 - 2) * (L.n1 - 2) * kSeg;
   return (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * ((axis == 2 ? L.n1 : L.n2) - 2);
 }
 
 int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
                         cudaStream_t st) {
   const int P = seg_P(axis, a.m);
-  const int S = seg_S(a.m, P, !(axis == 2 && !axis2_rows()));
+  const int S = seg_S(a.m, P);
   if (S < 2) return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 768)");
   std::vector<double> host(kTabDoubles + kSeg * kSeg, 0.0);
   make_tables(a.co, S, host.data());
@@ -1318,13 +993,13 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
   const long long nseg = desc_segments(a.L, axis, P);
   // +64 words of slack: tiles past the last interior column read (unused) descriptors
   PBG_CUDA(cudaMallocAsync(&aux.desc, (2 * nseg + 64) * sizeof(unsigned long long), st));
-  k_build_desc<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, axis2_rows() ? 1 : 0, codes,
+  k_build_desc<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, codes,
                                          aux.desc);
   PBG_LAUNCH_CHECK("k_build_desc");
   int* counter = nullptr;
   PBG_CUDA(cudaMallocAsync(&counter, sizeof(int), st));
   PBG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-  k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, axis2_rows() ? 1 : 0, a.co, 0,
+  k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, a.co, 0,
                                           aux.desc, counter, nullptr);
   PBG_LAUNCH_CHECK("k_seg_factors");
   int ngen = 0;
@@ -1333,7 +1008,7 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
   PBG_CUDA(cudaMallocAsync(&aux.gfac, ((size_t)ngen + 1) * 5 * kTabRows * sizeof(double), st));
   if (ngen > 0) {
     PBG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-    k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, axis2_rows() ? 1 : 0, a.co, 1,
+    k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, a.co, 1,
                                            aux.desc, counter, aux.gfac);
     PBG_LAUNCH_CHECK("k_seg_factors");
   }
@@ -1356,7 +1031,7 @@ void release_axis(AxisAux& aux, cudaStream_t st) {
 
 int launch_sweep(const SweepArgs& a, int axis, cudaStream_t st) {
   if (!a.ftab) return fail(PBG_E_CUDA, "flow table allocation failed");
-  return (axis == 2 && !axis2_rows()) ? launch_contig(a, st) : launch_strided(a, axis, st);
+  return launch_strided(a, axis, st);
 }
 
 
@@ -1475,10 +1150,6 @@ void march_axes(const pbg_march_desc* d, const Plan& plan, SweepArgs ax[3]) {
         break;
     }
     a.check = (axis == 2) && d->check_divergence;
-    {
-      const char* dbg = getenv("PBG_DEBUG_SKELETON");
-      a.dbg = dbg ? atoi(dbg) : 0;
-    }
     ax[axis] = a;
   }
 }

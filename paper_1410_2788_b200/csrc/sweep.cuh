@@ -73,7 +73,6 @@ struct SweepArgs {
   int step;
   double thr;
   int check;
-  int dbg;  // experiments only: 1 = stage + store (no solve)
   const double* ftab;  // flow tables (kFlowTabDoubles), staged into shared memory
   // Strided axes: offset (from the line base) of the high boundary value in bnd; normally
   // plane m+1 of a field, one plane for the two-plane ghost buffers of the slab march.
