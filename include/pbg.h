@@ -240,6 +240,14 @@ PBG_API int pbg_slab_destroy(pbg_slab* h, void* stream);
 PBG_API int pbg_flow_dense(int64_t n, const double* w, const double* kappa2, double coef,
                            double premultiplier, double* out, void* stream);
 
+/* Host only (no device needed): the interval table the sweep kernels evaluate the flow
+ * 2*artanh(decay*tanh(w/2)) with (|w| <= 38, 0 <= decay < 1): PBG_FLOW_TABLE_DOUBLES
+ * doubles, 84 intervals of 12 [centre, a0..a9, 0], interval index = (hi word of |w|+1 >> 16)
+ * - 0x3FF0, value = sum a_q (|w| - centre)^q with the sign of w.  Replaces the per-node
+ * tanh/atanh of _apply_flow (schemes.py:88-103) on the hot path; exported for testing. */
+#define PBG_FLOW_TABLE_DOUBLES 1008
+PBG_API int pbg_flow_table(double decay, double* out);
+
 /* Direct vacuum Poisson solve (vacuum_potential_fast, energy.py:59-85): -eps_m * d2(out) =
  * rho on the interior with out = bnd on the faces (bnd: pitched field whose faces hold the
  * Dirichlet data).  Boundary lifting, type-I DST along each axis (cuFFT D2Z of the odd

@@ -38,7 +38,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "sweep.cuh"
@@ -65,11 +67,17 @@ __host__ __device__ __forceinline__ int epi_needs(int epi) {
                                 : 0);
 }
 
-// Flow palette constants staged in shared memory as (decay, sat) pairs indexed by the solute
-// bit: one 16-byte load per node instead of predicated constant-bank selects.
+// Flow palette constants staged in shared memory: (decay, sat) pairs indexed by the solute
+// bit, the two table offsets, then the interval tables (FP + kFlowHdr).
+constexpr int kFlowHdr = 6;
 __device__ __forceinline__ double flow_sm(const double* FP, double w, uint32_t s, double pm) {
   const double2 v = reinterpret_cast<const double2*>(FP)[s];
-  return sinh_flow_tab(w, v.x, v.y, pm, FP + 4);
+  const int off = reinterpret_cast<const int*>(FP + 4)[s];
+  return sinh_flow_poly(w, v.x, v.y, pm, FP + kFlowHdr + off);
+}
+
+__host__ __device__ __forceinline__ bool uses_flow(int pro, int epi) {
+  return pro == PRO_FLOW || epi == EPI_FLOW || epi == EPI_AOS0;
 }
 
 __device__ __forceinline__ void row_coefs(const AxisCoef& co, int i, int m, uint32_t em,
@@ -245,10 +253,15 @@ __host__ __device__ constexpr size_t tile_doubles(int S, int kSegS) {
 }
 
 template <int LB, bool RT>
-__host__ __device__ constexpr size_t strided_smem(int S, int kSegS, bool needY) {
-  return sizeof(double) * (kTabDoubles + kSegS * kSegS + (needY ? 2 : 1) * tile_doubles<LB, RT>(S, kSegS) +
+__host__ __device__ constexpr size_t strided_smem(int S, int kSegS, bool needY, int fpoly_n) {
+  return sizeof(double) * (kTabDoubles + kSegS * (kSegS + 2) + (needY ? 2 : 1) * tile_doubles<LB, RT>(S, kSegS) +
                            4 * LB * kSegS) +
-         sizeof(unsigned long long) * 2 * kSegS * LB + (4 + kFlowTabDoubles) * sizeof(double);
+         sizeof(unsigned long long) * 2 * kSegS * LB + (kFlowHdr + fpoly_n) * sizeof(double);
+}
+
+// Shared-memory flow doubles of a launch: the interval tables only where the flow runs.
+__host__ __forceinline__ int flow_stage_n(const SweepArgs& a) {
+  return uses_flow(a.pro, a.epi) ? a.fpoly_n : 0;
 }
 
 // High Dirichlet fold of row m-1 (tridiag.py:217): owned by segment (m-1)/S at row (m-1)%S,
@@ -276,122 +289,124 @@ __device__ __forceinline__ void charged_fixup(unsigned cmask, double coef, Slot 
   }
 }
 
-// One block = LB lines x kSegS segments (thread (lane, seg) = segment seg of line lane).
+// One tile = LB lines x kSegS segments (thread (lane, seg) = segment seg of line lane).
 //   RT = false (axes 0, 1): the LB lines are adjacent k columns; the tile is stored row-major
 //        W[p][l] and staged / stored in 16-byte chunks of adjacent columns;
 //   RT = true  (axis 2, "row tiles"): the LB lines are adjacent j rows, each contiguous in
 //        global memory; the tile is stored line-major W[l][p] (stride rt_stride) and staged /
 //        stored as contiguous rows.
-// Block (x = column / row group, y = outer index).
-template <int S, int kSegS, bool CN, int LB, bool RT>
-__global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSegS <= 256 ? 3 : 2))
-    k_sweep_strided(const SweepArgs a, const int axis) {
-  extern __shared__ double sm[];
-  constexpr int NT = LB * kSegS, NR = strided_rows<S, kSegS>();
-  constexpr int RS = rt_stride<S, kSegS>();
-  constexpr int WS = RT ? 1 : LB;  // shared-memory step between consecutive rows of a line
-  constexpr int CPR = LB / 2, RPP = NT / CPR;  // 16-byte chunks per row, rows per pass
-  // divergence flag: issue the load now, decide after staging
-  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
-  const int lane = threadIdx.x, seg = threadIdx.y;
-  const int tid = seg * LB + lane;
+template <int S, int kSegS, int LB, bool RT>
+struct TileShape {
+  static constexpr int NT = LB * kSegS, NR = strided_rows<S, kSegS>();
+  static constexpr int RS = rt_stride<S, kSegS>();
+  static constexpr int WS = RT ? 1 : LB;  // shared-memory step between consecutive rows
+  static constexpr int CPR = LB / 2, RPP = NT / CPR;  // 16-byte chunks per row, rows per pass
+  static constexpr int TD = RT ? LB * RS : NR * LB;   // doubles of one staged tile
+};
+
+// Where a tile sits: tile (tx, ty) of a launch with nty outer indices.
+struct TileGeo {
+  int c0;       // first line of the tile (k for column tiles, j for row tiles)
+  int outer;    // outer index (j for axis 0, i for axes 1 and 2)
+  int ncols;    // active lines
+  int stride;   // global step between consecutive rows of a line
+  long long base;  // global offset of row 0 of tile line 0
+};
+
+template <int LB, bool RT>
+__device__ __forceinline__ TileGeo tile_geo(const SweepArgs& a, int axis, int tx, int ty,
+                                            int nty) {
   const Layout& L = a.L;
-  const int m = a.m, nl = m + 2;
-  const int c0 = 1 + blockIdx.x * LB;  // first line of the tile (k for RT=false, j for RT)
+  TileGeo g;
+  g.c0 = 1 + tx * LB;
   // Row tiles walk the planes in reverse: the axis-1 sweep before them wrote the last planes
   // last, so those are still in L2 when this launch starts.
-  const int outer = RT ? (int)gridDim.y - (int)blockIdx.y : 1 + (int)blockIdx.y;
+  g.outer = RT ? nty - ty : 1 + ty;
   const int K = (RT ? L.n1 : L.n2) - 2;  // lines per outer index
-  const int ncols = min(LB, K + 1 - c0);  // active lines in this tile
-  // global offset of row p of tile line l: lb(l) + p * gs
-  long long base;
-  int stride;
+  g.ncols = min(LB, K + 1 - g.c0);
   if (RT) {
-    base = L.at(outer, c0, 0);
-    stride = 1;
+    g.base = L.at(g.outer, g.c0, 0);
+    g.stride = 1;
   } else if (axis == 0) {
-    base = L.at(0, outer, c0);
-    stride = (int)L.s0;
+    g.base = L.at(0, g.outer, g.c0);
+    g.stride = (int)L.s0;
   } else {
-    base = L.at(outer, 0, c0);
-    stride = (int)L.pitch;
+    g.base = L.at(g.outer, 0, g.c0);
+    g.stride = (int)L.pitch;
   }
-  auto lb = [&](int l) { return base + (RT ? (long long)l * L.pitch : (long long)l); };
-  auto sidx = [&](int p, int l) { return RT ? l * RS + 1 + p : p * LB + l; };
-  const int needY = epi_needs(a.epi);
-  constexpr int TD = RT ? LB * RS : NR * LB;
-  double* T = sm;
-  double* Mi = T + kTabDoubles;
-  double* W = Mi + kSegS * kSegS;
-  double* Yt = W + TD;
-  double* X = Yt + (needY ? TD : 0);
-  unsigned long long* D = reinterpret_cast<unsigned long long*>(X + 4 * NT);
-  double* FP = reinterpret_cast<double*>(D + 2 * NT);  // flow palette (decay, sat) x 2
-  const uint32_t* D32 = reinterpret_cast<const uint32_t*>(D);
-  // solute bit of row p of tile line l (low word of descriptor word 1)
-  auto solute = [&](int sg, int sb, int l) { return (D32[4 * (sg * LB + l) + 2] >> sb) & 1u; };
-  const double* gy_all = needY == 1 ? a.src : a.acc;
-  if (tid < 4) FP[tid] = tid == 0 ? a.decay0 : (tid == 1 ? a.sat0 : (tid == 2 ? a.decay1 : a.sat1));
+  return g;
+}
 
-  // Phase 1: asynchronous staging of the own descriptor (first group), then of the field
-  // (+ epilogue operand) and tables.
-  cp_async16(D + 2 * tid, a.desc + 2 * (((long long)(outer - 1) * kSegS + seg) * K + (c0 - 1 + lane)));
-  asm volatile("cp.async.commit_group;\n" ::);
+// Asynchronous staging of one tile (own descriptor, field rows, epilogue operand); rows past
+// the far face are zeroed.  The caller commits the group.
+template <int S, int kSegS, int LB, bool RT>
+__device__ __forceinline__ void stage_tile(const SweepArgs& a, const TileGeo& g, double* W,
+                                           double* Yt, unsigned long long* D, int needY) {
+  using TS = TileShape<S, kSegS, LB, RT>;
+  constexpr int NT = TS::NT, NR = TS::NR, RS = TS::RS, CPR = TS::CPR, RPP = TS::RPP;
+  const int lane = threadIdx.x, seg = threadIdx.y, tid = seg * LB + lane;
+  const Layout& L = a.L;
+  const int m = a.m, nl = m + 2;
+  const int K = (RT ? L.n1 : L.n2) - 2;
+  const double* gy_all = needY == 1 ? a.src : a.acc;
+  cp_async16(D + 2 * tid,
+             a.desc + 2 * (((long long)(g.outer - 1) * kSegS + seg) * K + (g.c0 - 1 + lane)));
   if (RT) {
     // rows 1..m+1 of each line in 16-byte chunks (row 1 is 256-byte aligned), row 0 alone
     const int nch = (m + 1) / 2;  // full chunks; an odd last row goes alone
     const long long gstep = L.pitch;
     for (int c = tid; c < nch; c += NT) {
-      const double* g = a.src + base + 1 + 2 * c;
+      const double* gp = a.src + g.base + 1 + 2 * c;
       unsigned w = (unsigned)__cvta_generic_to_shared(W + 2 + 2 * c);
-      for (int l = 0; l < ncols; ++l, g += gstep, w += RS * 8)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(w), "l"(g));
+      for (int l = 0; l < g.ncols; ++l, gp += gstep, w += RS * 8)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(w), "l"(gp));
       if (needY) {
-        const double* gy = gy_all + base + 1 + 2 * c;
+        const double* gy = gy_all + g.base + 1 + 2 * c;
         unsigned y = (unsigned)__cvta_generic_to_shared(Yt + 2 + 2 * c);
-        for (int l = 0; l < ncols; ++l, gy += gstep, y += RS * 8)
+        for (int l = 0; l < g.ncols; ++l, gy += gstep, y += RS * 8)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(y), "l"(gy));
       }
     }
-    if (tid < ncols) {
-      cp_async8(W + tid * RS + 1, a.src + lb(tid));
-      if ((m + 1) & 1) cp_async8(W + tid * RS + 1 + m + 1, a.src + lb(tid) + m + 1);
+    if (tid < g.ncols) {
+      const long long lbt = g.base + (long long)tid * L.pitch;
+      cp_async8(W + tid * RS + 1, a.src + lbt);
+      if ((m + 1) & 1) cp_async8(W + tid * RS + 1 + m + 1, a.src + lbt + m + 1);
       if (needY) {
-        cp_async8(Yt + tid * RS + 1, gy_all + lb(tid));
-        if ((m + 1) & 1) cp_async8(Yt + tid * RS + 1 + m + 1, gy_all + lb(tid) + m + 1);
+        cp_async8(Yt + tid * RS + 1, gy_all + lbt);
+        if ((m + 1) & 1) cp_async8(Yt + tid * RS + 1 + m + 1, gy_all + lbt + m + 1);
       }
     }
     for (int c = tid; c < LB * (NR - nl); c += NT) {  // rows past the far face
       const int l = c / (NR - nl), p = nl + c % (NR - nl);
-      W[sidx(p, l)] = 0.0;
+      W[l * RS + 1 + p] = 0.0;
     }
   } else {
     const int q = (tid % CPR) * 2, p0 = tid / CPR;
-    const long long gstep = (long long)RPP * stride;
-    const double* g = a.src + base + p0 * (long long)stride + q;
+    const long long gstep = (long long)RPP * g.stride;
+    const double* gp = a.src + g.base + p0 * (long long)g.stride + q;
     double* w = W + p0 * LB + q;
 #pragma unroll 4
-    for (int p = p0; p < nl; p += RPP, g += gstep, w += RPP * LB) cp_async16(w, g);
+    for (int p = p0; p < nl; p += RPP, gp += gstep, w += RPP * LB) cp_async16(w, gp);
     if (needY) {
-      const double* gyp = gy_all + base + p0 * (long long)stride + q;
+      const double* gyp = gy_all + g.base + p0 * (long long)g.stride + q;
       double* yp = Yt + p0 * LB + q;
 #pragma unroll 4
       for (int p = p0; p < nl; p += RPP, gyp += gstep, yp += RPP * LB) cp_async16(yp, gyp);
     }
     for (int c = nl * LB + tid; c < NR * LB; c += NT) W[c] = 0.0;  // rows past the far face
   }
-  for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
-  if (a.static_ok)
-    for (int c = tid; c < kSegS * kSegS / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
-  if (a.pro == PRO_FLOW || a.epi == EPI_FLOW || a.epi == EPI_AOS0)
-    for (int c = tid; c < kFlowTabDoubles / 2; c += NT) cp_async16(FP + 4 + 2 * c, a.ftab + 2 * c);
-  asm volatile("cp.async.commit_group;\n" ::);
-  // A general segment reads its precomputed factors from global memory: bring the five rows
-  // of its table towards L1 while the tile is still in flight.
-  // Same for the Dirichlet values of the line ends and the source at charged nodes.
-  asm volatile("cp.async.wait_group 1;\n" ::);
+}
+
+// Once the own descriptor has landed: a general segment reads its precomputed factors from
+// global memory, so bring the five rows of its table towards L1; same for the source at
+// charged nodes.  Returns the Dirichlet value the thread folds into its first / last row.
+template <int S, int kSegS, int LB, bool RT>
+__device__ __forceinline__ double tile_prefetch(const SweepArgs& a, const TileGeo& g,
+                                                const unsigned long long* D) {
+  const int lane = threadIdx.x, seg = threadIdx.y, tid = seg * LB + lane;
   double bfold = 0.0;
-  if (lane < ncols) {
+  if (lane < g.ncols) {
+    const long long gl = g.base + (RT ? (long long)lane * a.L.pitch : (long long)lane);
     const unsigned long long slot = D[2 * tid] >> kSlotShift;
     if (slot) {
       const double* f = a.gfac + (long long)(slot - 1) * 5 * kTabRows;
@@ -399,18 +414,38 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
       for (int q = 0; q < 5; ++q) asm volatile("prefetch.global.L1 [%0];" ::"l"(f + q * kTabRows));
     }
     unsigned cm = (unsigned)(D[2 * tid + 1] >> 32);
-    const double* rr = a.rho + lb(lane) + (long long)(seg * S + 1) * stride;
+    const double* rr = a.rho + gl + (long long)(seg * S + 1) * g.stride;
     while (cm) {
       const int j = __ffs(cm) - 1;
       cm &= cm - 1;
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(rr + (long long)j * stride));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(rr + (long long)j * g.stride));
     }
-    if (seg == 0) bfold = a.bnd[lb(lane)];
-    else if (seg == (m - 1) / S) bfold = a.bnd[lb(lane) + a.hi_off];
+    if (seg == 0) bfold = a.bnd[gl];
+    else if (seg == (a.m - 1) / S) bfold = a.bnd[gl + a.hi_off];
   }
-  cp_async_wait_all();
-  __syncthreads();
-  if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
+  return bfold;
+}
+
+// Everything after staging: prologue, local elimination, reduced system, reconstruction,
+// epilogue and coalesced store of one tile.  Block-uniform control flow (all barriers are
+// reached by every thread).
+template <int S, int kSegS, bool CN, int LB, bool RT>
+__device__ __forceinline__ void tile_body(const SweepArgs& a, const TileGeo& g, const double* T,
+                                          const double* Mi, double* W, const double* Yt,
+                                          double* X, const unsigned long long* D,
+                                          const double* FP, double bfold) {
+  using TS = TileShape<S, kSegS, LB, RT>;
+  constexpr int NT = TS::NT, RS = TS::RS, WS = TS::WS, CPR = TS::CPR, RPP = TS::RPP;
+  const int lane = threadIdx.x, seg = threadIdx.y, tid = seg * LB + lane;
+  const Layout& L = a.L;
+  const int m = a.m, nl = m + 2;
+  const int ncols = g.ncols, stride = g.stride;
+  const long long base = g.base;
+  auto lb = [&](int l) { return base + (RT ? (long long)l * L.pitch : (long long)l); };
+  auto sidx = [&](int p, int l) { return RT ? l * RS + 1 + p : p * LB + l; };
+  const uint32_t* D32 = reinterpret_cast<const uint32_t*>(D);
+  // solute bit of row p of tile line l (low word of descriptor word 1)
+  auto solute = [&](int sg, int sb, int l) { return (D32[4 * (sg * LB + l) + 2] >> sb) & 1u; };
 
   const int i0 = seg * S;
   // lines past the last interior one read unrelated descriptor words: neutralise them
@@ -470,9 +505,6 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
       r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], bfold));
     if (seg == (m - 1) / S && active)
       fold_high<S>(a, r, amask, seg == 0 ? a.bnd[gl + a.hi_off] : bfold);
-    // clean tile: every line of the tile is one dielectric (palette 0) end to end
-    const bool clean = __syncthreads_and(!active || eps_bits(amask, S) == 0ull) && a.static_ok;
-
     SegOut o;
     const double* Tv = seg_eliminate<S>(a, r, amask, i0, seg == 0, T, o);
 
@@ -481,28 +513,34 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
     double* sB = X + NT;
     double* sC = X + 2 * NT;
     double* sR = X + 3 * NT;
+    sA[tid] = o.yF;
+    sB[tid] = o.aF;
+    sC[tid] = o.bF;
+    // clean tile: every line of the tile is one dielectric (palette 0) end to end
+    const bool clean = __syncthreads_and(!active || eps_bits(amask, S) == 0ull) && a.static_ok;
     double t, tm;
-    if (clean) {  // static inverse: one exchange of y_F, one of R, then two dot products
-      sA[tid] = o.yF;
-      __syncthreads();
+    if (clean) {  // static inverse: separator rhs per line, one dot product, one exchange
+      constexpr int RP = kSegS + 2;  // padded rows: conflict-free 16-byte loads
+      double* sRl = X + 2 * NT;      // [line][separator] (spans sC, sR; sC unused here)
       const double yFn = (seg + 1 < kSegS) ? sA[tid + LB] : 0.0;
-      sR[tid] = o.rs - o.as * o.yL - o.cs * yFn;
+      sRl[lane * RP + seg] = o.rs - o.as * o.yL - o.cs * yFn;
       __syncthreads();
-      const int k1 = seg > 0 ? seg - 1 : 0;  // transposed inverse: column q at Mi[q*P]
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll 8
-      for (int q = 0; q < kSegS; ++q) {
-        const double Rq = sR[q * LB + lane];
-        s0 = fma(Mi[q * kSegS + seg], Rq, s0);
-        s1 = fma(Mi[q * kSegS + k1], Rq, s1);
+      const double2* Rr = reinterpret_cast<const double2*>(sRl + lane * RP);
+      const double2* Mr = reinterpret_cast<const double2*>(Mi + seg * RP);  // row seg
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int q = 0; q < kSegS / 2; q += 2) {
+        const double2 r0 = Rr[q], m0 = Mr[q], r1 = Rr[q + 1], m1 = Mr[q + 1];
+        s0 = fma(m0.x, r0.x, s0);
+        s1 = fma(m0.y, r0.y, s1);
+        s2 = fma(m1.x, r1.x, s2);
+        s3 = fma(m1.y, r1.y, s3);
       }
-      t = s0;
-      tm = seg > 0 ? s1 : 0.0;
-    } else {  // parallel cyclic reduction
-      sA[tid] = o.yF;
-      sB[tid] = o.aF;
-      sC[tid] = o.bF;
+      t = (s0 + s1) + (s2 + s3);
+      sB[tid] = t;
       __syncthreads();
+      tm = (seg > 0) ? sB[tid - LB] : 0.0;
+    } else {  // parallel cyclic reduction
       double yFn = 0.0, aFn = 0.0, bFn = 0.0;
       if (seg + 1 < kSegS) {
         yFn = sA[tid + LB];
@@ -639,6 +677,103 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
   }
 }
 
+
+// Single-tile kernel: block (x = column / row group, y = outer index).  Used when a second
+// staged operand (AOS/MAOS), the slab ends-only mode or a short launch rules out the
+// pipelined kernel below.
+template <int S, int kSegS, bool CN, int LB, bool RT>
+__global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSegS <= 256 ? 3 : 2))
+    k_sweep_strided(const SweepArgs a, const int axis) {
+  extern __shared__ double sm[];
+  using TS = TileShape<S, kSegS, LB, RT>;
+  constexpr int NT = TS::NT, TD = TS::TD;
+  // divergence flag: issue the load now, decide after staging
+  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
+  const int tid = threadIdx.y * LB + threadIdx.x;
+  const TileGeo g = tile_geo<LB, RT>(a, axis, blockIdx.x, blockIdx.y, gridDim.y);
+  const int needY = epi_needs(a.epi);
+  double* T = sm;
+  double* Mi = T + kTabDoubles;
+  double* W = Mi + kSegS * (kSegS + 2);
+  double* Yt = W + TD;
+  double* X = Yt + (needY ? TD : 0);
+  unsigned long long* D = reinterpret_cast<unsigned long long*>(X + 4 * NT);
+  double* FP = reinterpret_cast<double*>(D + 2 * NT);  // flow palette and tables
+  if (tid < 4) FP[tid] = tid == 0 ? a.decay0 : (tid == 1 ? a.sat0 : (tid == 2 ? a.decay1 : a.sat1));
+  if (tid < 2) reinterpret_cast<int*>(FP + 4)[tid] = a.foff[tid];
+
+  // Phase 1: asynchronous staging of the tile (own descriptor first), then the tables.
+  stage_tile<S, kSegS, LB, RT>(a, g, W, Yt, D, needY);
+  asm volatile("cp.async.commit_group;\n" ::);
+  for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
+  if (a.static_ok)
+    for (int c = tid; c < kSegS * (kSegS + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
+  if (uses_flow(a.pro, a.epi))
+    for (int c = tid; c < a.fpoly_n / 2; c += NT) cp_async16(FP + kFlowHdr + 2 * c, a.fpoly + 2 * c);
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 1;\n" ::);
+  const double bfold = tile_prefetch<S, kSegS, LB, RT>(a, g, D);
+  cp_async_wait_all();
+  __syncthreads();
+  if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
+  tile_body<S, kSegS, CN, LB, RT>(a, g, T, Mi, W, Yt, X, D, FP, bfold);
+}
+
+// Persistent, double-buffered kernel (plain launches: no second staged operand, no ends-only
+// mode): one block per SM walks tiles blockIdx.x, blockIdx.x + gridDim.x, ...; the next tile
+// is staged into the other buffer while the current one is solved and stored, so the memory
+// traffic of tile k+1 overlaps the compute of tile k.
+template <int S, int kSegS, bool CN, int LB, bool RT>
+__global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 256 ? 2 : 1)
+    k_sweep_pipe(const SweepArgs a, const int axis, const int ntx, const int nty) {
+  extern __shared__ double sm[];
+  using TS = TileShape<S, kSegS, LB, RT>;
+  constexpr int NT = TS::NT, TD = TS::TD;
+  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
+  const int tid = threadIdx.y * LB + threadIdx.x;
+  double* T = sm;
+  double* Mi = T + kTabDoubles;
+  double* X = Mi + kSegS * (kSegS + 2);
+  double* Wb[2];
+  Wb[0] = X + 4 * NT;
+  Wb[1] = Wb[0] + TD;
+  unsigned long long* Db[2];
+  Db[0] = reinterpret_cast<unsigned long long*>(Wb[1] + TD);
+  Db[1] = Db[0] + 2 * NT;
+  double* FP = reinterpret_cast<double*>(Db[1] + 2 * NT);
+  if (tid < 4) FP[tid] = tid == 0 ? a.decay0 : (tid == 1 ? a.sat0 : (tid == 2 ? a.decay1 : a.sat1));
+  if (tid < 2) reinterpret_cast<int*>(FP + 4)[tid] = a.foff[tid];
+  const int ntiles = ntx * nty;
+  int tile = blockIdx.x;
+  if (tile < ntiles)
+    stage_tile<S, kSegS, LB, RT>(a, tile_geo<LB, RT>(a, axis, tile % ntx, tile / ntx, nty), Wb[0],
+                                 nullptr, Db[0], 0);
+  for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
+  if (a.static_ok)
+    for (int c = tid; c < kSegS * (kSegS + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
+  if (uses_flow(a.pro, a.epi))
+    for (int c = tid; c < a.fpoly_n / 2; c += NT) cp_async16(FP + kFlowHdr + 2 * c, a.fpoly + 2 * c);
+  asm volatile("cp.async.commit_group;\n" ::);
+  if (dstep < a.step) {  // an earlier step diverged: nothing more to compute
+    cp_async_wait_all();
+    return;
+  }
+  for (int b = 0; tile < ntiles; tile += gridDim.x, b ^= 1) {
+    const int next = tile + gridDim.x;
+    if (next < ntiles)
+      stage_tile<S, kSegS, LB, RT>(a, tile_geo<LB, RT>(a, axis, next % ntx, next / ntx, nty),
+                                   Wb[b ^ 1], nullptr, Db[b ^ 1], 0);
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);  // the current tile (and the tables) landed
+    const TileGeo g = tile_geo<LB, RT>(a, axis, tile % ntx, tile / ntx, nty);
+    const double bfold = tile_prefetch<S, kSegS, LB, RT>(a, g, Db[b]);
+    __syncthreads();
+    tile_body<S, kSegS, CN, LB, RT>(a, g, T, Mi, Wb[b], nullptr, X, Db[b], FP, bfold);
+    __syncthreads();  // buffer b is restaged two tiles later
+  }
+  cp_async_wait_all();
+}
+
 // ---------------------------------------------------------------------------------------
 // Segment descriptors, built once per march and axis from the 1-byte node codes:
 //   word 0: bit j = eps bit (axis) of the node of row i0+j, j = 0..S (zero past node m+1)
@@ -754,13 +889,47 @@ static int seg_P(int axis, int m) {
   return m <= 128 ? 8 : (m <= 256 ? 16 : 32);
 }
 
+template <int LB, bool RT>
+static size_t pipe_smem(int S, int kSegS, int fpoly_n) {
+  return sizeof(double) * (kTabDoubles + kSegS * (kSegS + 2) + 4 * LB * kSegS +
+                           2 * tile_doubles<LB, RT>(S, kSegS) + 2 * 2 * LB * kSegS + kFlowHdr +
+                           fpoly_n);
+}
+
+// The persistent double-buffered kernel serves every launch without a second staged operand
+// or the slab ends-only mode (PBG_PIPE=0 selects the single-tile kernel, for comparison).
+static bool pipe_enabled(const SweepArgs& a) {
+  static const bool on = [] {
+    const char* e = getenv("PBG_PIPE");
+    return !(e && e[0] == '0');
+  }();
+  return on && epi_needs(a.epi) == 0 && a.ends == nullptr;
+}
+
 template <int S, int P, bool CN, int LB, bool RT>
 static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
   const int nouter = (axis == 0 ? a.L.n1 : a.L.n0) - 2;
   const int nlines = (RT ? a.L.n1 : a.L.n2) - 2;
-  dim3 grid((nlines + LB - 1) / LB, nouter);
+  const int ntx = (nlines + LB - 1) / LB;
   dim3 block(LB, P);
-  const size_t smem = strided_smem<LB, RT>(S, P, epi_needs(a.epi) != 0);
+  if (pipe_enabled(a)) {
+    const size_t smem = pipe_smem<LB, RT>(S, P, flow_stage_n(a));
+    if (smem <= 232448) {
+      auto kern = k_sweep_pipe<S, P, CN, LB, RT>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int dev = 0, nsm = 148, bps = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, LB * P, smem);
+      if (bps > 0) {
+        const int grid = std::min(ntx * nouter, nsm * bps);
+        kern<<<grid, block, smem, st>>>(a, axis, ntx, nouter);
+        return;
+      }
+    }
+  }
+  dim3 grid(ntx, nouter);
+  const size_t smem = strided_smem<LB, RT>(S, P, epi_needs(a.epi) != 0, flow_stage_n(a));
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_sweep_strided<S, P, CN, LB, RT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -776,7 +945,7 @@ static void launch_strided_SC(const SweepArgs& a, int axis, cudaStream_t st) {
   // Tiles must also fit the 227 KB of shared memory per block (long lines with AOS/MAOS).
   const bool needY = epi_needs(a.epi) != 0;
   const bool wide = !needY;
-  const bool fits16 = strided_smem<16, false>(S, P, needY) <= 232448;
+  const bool fits16 = strided_smem<16, false>(S, P, needY, flow_stage_n(a)) <= 232448;
   if (axis == 0 && fits16) launch_strided_SCL<S, P, CN, 16, false>(a, axis, st);
   else if (axis == 0) launch_strided_SCL<S, P, CN, 8, false>(a, axis, st);
   else if (axis == 1 && wide) launch_strided_SCL<S, P, CN, 16, false>(a, axis, st);
@@ -920,9 +1089,86 @@ static bool make_reduced_inverse(const AxisCoef& co, const double* tab, int S, i
       for (int q = 0; q < 2 * P; ++q) M[r][q] -= f * M[c][q];
     }
   }
-  for (int r = 0; r < P; ++r)  // stored transposed: minv[q*32 + k] = inverse[k][q]
-    for (int c = 0; c < P; ++c) minv[c * P + r] = M[r][P + c];
+  for (int r = 0; r < P; ++r)  // row-major, rows padded to P + 2 (conflict-free loads)
+    for (int c = 0; c < P; ++c) minv[r * (P + 2) + c] = M[r][P + c];
   return true;
+}
+
+// Flow interval table of decay d (pbg_internal.cuh, flow_poly): on interval [lo, hi] the
+// map F(x) = 2 artanh(d tanh(x/2)) is interpolated at the 10 Chebyshev nodes in extended
+// precision, and the Chebyshev series is re-expanded in powers of t = x - c.
+static void build_flow_poly(double d, double* out) {
+  constexpr int n = 10;
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int iv = 0; iv < kFPolyIv; ++iv) {
+    const int e = iv / 16, s = iv % 16;
+    const double lo = std::ldexp(1.0 + s / 16.0, e) - 1.0;
+    const double hi = std::ldexp(1.0 + (s + 1) / 16.0, e) - 1.0;
+    const double c = 0.5 * (lo + hi);
+    const long double r = 0.5L * ((long double)hi - (long double)lo);
+    long double y[n], g[n];
+    for (int k = 0; k < n; ++k) {
+      const long double x = (long double)c + r * std::cos(pi * (k + 0.5L) / n);
+      y[k] = 2.0L * std::atanh((long double)d * std::tanh(0.5L * x));
+    }
+    for (int j = 0; j < n; ++j) {
+      long double acc = 0.0L;
+      for (int k = 0; k < n; ++k) acc += y[k] * std::cos(pi * j * (k + 0.5L) / n);
+      g[j] = (j == 0 ? 1.0L : 2.0L) * acc / n;
+    }
+    // sum_j g_j T_j(u), u = t / r, in powers of u (T_{j+1} = 2u T_j - T_{j-1})
+    long double Tp[n] = {0}, Tc[n] = {0}, b[n] = {0};
+    Tp[0] = 1.0L;
+    Tc[1] = 1.0L;
+    b[0] = g[0];
+    b[1] = g[1];
+    for (int j = 2; j < n; ++j) {
+      long double Tn[n] = {0};
+      for (int q = 0; q + 1 < n; ++q) Tn[q + 1] = 2.0L * Tc[q];
+      for (int q = 0; q < n; ++q) {
+        Tn[q] -= Tp[q];
+        b[q] += g[j] * Tn[q];
+        Tp[q] = Tc[q];
+        Tc[q] = Tn[q];
+      }
+    }
+    double* o = out + iv * kFPolyStride;
+    o[0] = c;
+    long double rp = 1.0L;
+    for (int q = 0; q < n; ++q, rp *= r) o[1 + q] = (double)(b[q] / rp);
+    o[kFPolyStride - 1] = 0.0;
+  }
+}
+
+// Device copy of the interval tables of a decay pair, [palette slot][kFPolyDoubles], cached
+// per device for the process (a march uses at most two pairs).
+static const double* flow_poly_table(double d0, double d1, int& ntab) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, double, double>, std::pair<double*, int>> cache;
+  int dev = 0;
+  ntab = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(dev, d0, d1);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    ntab = it->second.second;
+    return it->second.first;
+  }
+  std::vector<double> h;
+  for (double d : {d0, d1}) {
+    if (!(d < 1.0) || (ntab == 1 && d == d0)) continue;
+    h.resize((size_t)(ntab + 1) * kFPolyDoubles);
+    build_flow_poly(d, h.data() + (size_t)ntab * kFPolyDoubles);
+    ++ntab;
+  }
+  if (h.empty()) h.assign(2, 0.0);
+  double* p = nullptr;
+  if (cudaMalloc(&p, h.size() * sizeof(double)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+    return nullptr;
+  cache[key] = {p, ntab};
+  return p;
 }
 
 void set_decays(SweepArgs& a, double d0, double d1) {
@@ -930,30 +1176,11 @@ void set_decays(SweepArgs& a, double d0, double d1) {
   a.decay1 = d1;
   a.sat0 = d0 < 1.0 ? 2.0 * std::atanh(d0) : 0.0;
   a.sat1 = d1 < 1.0 ? 2.0 * std::atanh(d1) : 0.0;
-}
-
-// Flow tables (pbg_internal.cuh, sinh_flow_tab), one copy per device for the process.
-static const double* flow_tables() {
-  static std::mutex mu;
-  static double* dev[64] = {};
-  int d = 0;
-  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  if (!dev[d]) {
-    std::vector<double> h(kFlowTabDoubles);
-    for (int j = 0; j < kExpTab; ++j) h[j] = std::exp2((double)j / kExpTab);
-    for (int i = 0; i < kLogTab; ++i) {
-      const double invc = 1.0 / (1.0 + (i + 0.5) / kLogTab);
-      h[kExpTab + 2 * i] = invc;
-      h[kExpTab + 2 * i + 1] = -std::log(invc);
-    }
-    double* p = nullptr;
-    if (cudaMalloc(&p, h.size() * sizeof(double)) != cudaSuccess) return nullptr;
-    if (cudaMemcpy(p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
-      return nullptr;
-    dev[d] = p;
-  }
-  return dev[d];
+  int ntab = 0;
+  a.fpoly = flow_poly_table(d0, d1, ntab);
+  a.fpoly_n = ntab * kFPolyDoubles;
+  a.foff[0] = 0;  // palette 0 has slot 0 when it needs one
+  a.foff[1] = (d0 < 1.0 && d1 < 1.0 && d1 != d0) ? kFPolyDoubles : 0;
 }
 
 SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, double factor) {
@@ -968,7 +1195,6 @@ SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, double 
   a.epi = EPI_STORE;
   a.thr = INFINITY;
   a.hi_off = (long long)(a.m + 1) * (axis == 0 ? a.L.s0 : (axis == 1 ? a.L.pitch : 1));
-  a.ftab = flow_tables();
   return a;
 }
 
@@ -982,7 +1208,7 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
   const int P = seg_P(axis, a.m);
   const int S = seg_S(a.m, P);
   if (S < 2) return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 768)");
-  std::vector<double> host(kTabDoubles + kSeg * kSeg, 0.0);
+  std::vector<double> host(kTabDoubles + kSeg * (kSeg + 2), 0.0);
   make_tables(a.co, S, host.data());
   memcpy(a.tmid, host.data(), sizeof(a.tmid));  // type 0 (interior), palette 0
   a.static_ok =
@@ -1030,7 +1256,7 @@ void release_axis(AxisAux& aux, cudaStream_t st) {
 }
 
 int launch_sweep(const SweepArgs& a, int axis, cudaStream_t st) {
-  if (!a.ftab) return fail(PBG_E_CUDA, "flow table allocation failed");
+  if (!a.fpoly) return fail(PBG_E_CUDA, "flow table allocation failed");
   return launch_strided(a, axis, st);
 }
 
@@ -1161,6 +1387,14 @@ static long long g_prof_n[3] = {0, 0, 0};
 }  // namespace pbg
 
 using namespace pbg;
+
+extern "C" PBG_API int pbg_flow_table(double decay, double* out) {
+  static_assert(kFPolyDoubles == PBG_FLOW_TABLE_DOUBLES, "flow table size");
+  if (!out) return fail(PBG_E_INVALID, "null pointer");
+  if (!(decay >= 0.0 && decay < 1.0)) return fail(PBG_E_INVALID, "decay must be in [0, 1)");
+  build_flow_poly(decay, out);
+  return PBG_OK;
+}
 
 extern "C" PBG_API int pbg_set_profiling(int32_t on) {
   g_profile = on != 0;

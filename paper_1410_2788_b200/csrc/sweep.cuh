@@ -73,7 +73,12 @@ struct SweepArgs {
   int step;
   double thr;
   int check;
-  const double* ftab;  // flow tables (kFlowTabDoubles), staged into shared memory
+  // Flow interval tables (kFPolyDoubles per palette with decay < 1, sweep.cu flow_poly_table),
+  // staged into shared memory by launches that apply the flow; foff[b] = offset of palette
+  // b's table, fpoly_n = doubles to stage.
+  const double* fpoly;
+  int foff[2];
+  int fpoly_n;
   // Strided axes: offset (from the line base) of the high boundary value in bnd; normally
   // plane m+1 of a field, one plane for the two-plane ghost buffers of the slab march.
   long long hi_off;
