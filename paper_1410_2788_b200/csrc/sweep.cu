@@ -264,6 +264,92 @@ __host__ __forceinline__ int flow_stage_n(const SweepArgs& a) {
   return uses_flow(a.pro, a.epi) ? a.fpoly_n : 0;
 }
 
+// Reduced system over the P separators of each line of a tile (block-wide, all threads):
+// a precomputed dense inverse when every line of the tile is one dielectric end to end
+// ("clean"), parallel cyclic reduction otherwise.  Returns the thread's separator t and its
+// left neighbour's tm.  Scratch X: 4 * LB * kSegS doubles.
+template <int S, int kSegS, int LB>
+__device__ __forceinline__ void reduced_solve(const SweepArgs& a, const SegOut& o,
+                                              const double* Mi, double* X, bool active,
+                                              unsigned long long amask, double& t, double& tm) {
+  constexpr int NT = LB * kSegS;
+  const int lane = threadIdx.x, seg = threadIdx.y, tid = seg * LB + lane;
+  double* sA = X;
+  double* sB = X + NT;
+  double* sC = X + 2 * NT;
+  double* sR = X + 3 * NT;
+  sA[tid] = o.yF;
+  sB[tid] = o.aF;
+  sC[tid] = o.bF;
+  // clean tile: every line of the tile is one dielectric (palette 0) end to end
+  const bool clean = __syncthreads_and(!active || eps_bits(amask, S) == 0ull) && a.static_ok;
+  if (clean) {  // static inverse: separator rhs per line, one dot product, one exchange
+    constexpr int RP = kSegS + 2;  // padded rows: conflict-free 16-byte loads
+    double* sRl = X + 2 * NT;      // [line][separator] (spans sC, sR; sC unused here)
+    const double yFn = (seg + 1 < kSegS) ? sA[tid + LB] : 0.0;
+    sRl[lane * RP + seg] = o.rs - o.as * o.yL - o.cs * yFn;
+    __syncthreads();
+    const double2* Rr = reinterpret_cast<const double2*>(sRl + lane * RP);
+    const double2* Mr = reinterpret_cast<const double2*>(Mi + seg * RP);  // row seg
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int q = 0; q < kSegS / 2; q += 2) {
+      const double2 r0 = Rr[q], m0 = Mr[q], r1 = Rr[q + 1], m1 = Mr[q + 1];
+      s0 = fma(m0.x, r0.x, s0);
+      s1 = fma(m0.y, r0.y, s1);
+      s2 = fma(m1.x, r1.x, s2);
+      s3 = fma(m1.y, r1.y, s3);
+    }
+    t = (s0 + s1) + (s2 + s3);
+    sB[tid] = t;
+    __syncthreads();
+    tm = (seg > 0) ? sB[tid - LB] : 0.0;
+  } else {  // parallel cyclic reduction
+    double yFn = 0.0, aFn = 0.0, bFn = 0.0;
+    if (seg + 1 < kSegS) {
+      yFn = sA[tid + LB];
+      aFn = sB[tid + LB];
+      bFn = sC[tid + LB];
+    }
+    __syncthreads();
+    double A, B, Cc, R;
+    reduced_row(o, yFn, aFn, bFn, A, B, Cc, R);
+#pragma unroll
+    for (int d = 1; d < kSegS; d <<= 1) {
+      sA[tid] = A;
+      sB[tid] = fast_rcp(B);
+      sC[tid] = Cc;
+      sR[tid] = R;
+      __syncthreads();
+      double Am = 0.0, iBm = 1.0, Cm = 0.0, Rm = 0.0, Ap = 0.0, iBp = 1.0, Cp = 0.0, Rp = 0.0;
+      if (seg >= d) {
+        const int q = tid - d * LB;
+        Am = sA[q];
+        iBm = sB[q];
+        Cm = sC[q];
+        Rm = sR[q];
+      }
+      if (seg + d < kSegS) {
+        const int q = tid + d * LB;
+        Ap = sA[q];
+        iBp = sB[q];
+        Cp = sC[q];
+        Rp = sR[q];
+      }
+      __syncthreads();
+      const double k1 = -A * iBm, k2 = -Cc * iBp;
+      A = k1 * Am;
+      Cc = k2 * Cp;
+      B = B + k1 * Cm + k2 * Ap;
+      R = R + k1 * Rm + k2 * Rp;
+    }
+    t = R * fast_rcp(B);
+    sA[tid] = t;
+    __syncthreads();
+    tm = (seg > 0) ? sA[tid - LB] : 0.0;
+  }
+}
+
 // High Dirichlet fold of row m-1 (tridiag.py:217): owned by segment (m-1)/S at row (m-1)%S,
 // both launch-uniform, so the static-index select below runs in one thread per line.
 template <int S>
@@ -509,81 +595,8 @@ __device__ __forceinline__ void tile_body(const SweepArgs& a, const TileGeo& g, 
     const double* Tv = seg_eliminate<S>(a, r, amask, i0, seg == 0, T, o);
 
     // Phase 3: reduced system over the separators of each line.
-    double* sA = X;
-    double* sB = X + NT;
-    double* sC = X + 2 * NT;
-    double* sR = X + 3 * NT;
-    sA[tid] = o.yF;
-    sB[tid] = o.aF;
-    sC[tid] = o.bF;
-    // clean tile: every line of the tile is one dielectric (palette 0) end to end
-    const bool clean = __syncthreads_and(!active || eps_bits(amask, S) == 0ull) && a.static_ok;
     double t, tm;
-    if (clean) {  // static inverse: separator rhs per line, one dot product, one exchange
-      constexpr int RP = kSegS + 2;  // padded rows: conflict-free 16-byte loads
-      double* sRl = X + 2 * NT;      // [line][separator] (spans sC, sR; sC unused here)
-      const double yFn = (seg + 1 < kSegS) ? sA[tid + LB] : 0.0;
-      sRl[lane * RP + seg] = o.rs - o.as * o.yL - o.cs * yFn;
-      __syncthreads();
-      const double2* Rr = reinterpret_cast<const double2*>(sRl + lane * RP);
-      const double2* Mr = reinterpret_cast<const double2*>(Mi + seg * RP);  // row seg
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-      for (int q = 0; q < kSegS / 2; q += 2) {
-        const double2 r0 = Rr[q], m0 = Mr[q], r1 = Rr[q + 1], m1 = Mr[q + 1];
-        s0 = fma(m0.x, r0.x, s0);
-        s1 = fma(m0.y, r0.y, s1);
-        s2 = fma(m1.x, r1.x, s2);
-        s3 = fma(m1.y, r1.y, s3);
-      }
-      t = (s0 + s1) + (s2 + s3);
-      sB[tid] = t;
-      __syncthreads();
-      tm = (seg > 0) ? sB[tid - LB] : 0.0;
-    } else {  // parallel cyclic reduction
-      double yFn = 0.0, aFn = 0.0, bFn = 0.0;
-      if (seg + 1 < kSegS) {
-        yFn = sA[tid + LB];
-        aFn = sB[tid + LB];
-        bFn = sC[tid + LB];
-      }
-      __syncthreads();
-      double A, B, Cc, R;
-      reduced_row(o, yFn, aFn, bFn, A, B, Cc, R);
-#pragma unroll
-      for (int d = 1; d < kSegS; d <<= 1) {
-        sA[tid] = A;
-        sB[tid] = fast_rcp(B);
-        sC[tid] = Cc;
-        sR[tid] = R;
-        __syncthreads();
-        double Am = 0.0, iBm = 1.0, Cm = 0.0, Rm = 0.0, Ap = 0.0, iBp = 1.0, Cp = 0.0, Rp = 0.0;
-        if (seg >= d) {
-          const int q = tid - d * LB;
-          Am = sA[q];
-          iBm = sB[q];
-          Cm = sC[q];
-          Rm = sR[q];
-        }
-        if (seg + d < kSegS) {
-          const int q = tid + d * LB;
-          Ap = sA[q];
-          iBp = sB[q];
-          Cp = sC[q];
-          Rp = sR[q];
-        }
-        __syncthreads();
-        const double k1 = -A * iBm, k2 = -Cc * iBp;
-        A = k1 * Am;
-        Cc = k2 * Cp;
-        B = B + k1 * Cm + k2 * Ap;
-        R = R + k1 * Rm + k2 * Rp;
-      }
-      t = R * fast_rcp(B);
-      sA[tid] = t;
-      __syncthreads();
-      tm = (seg > 0) ? sA[tid - LB] : 0.0;
-    }
+    reduced_solve<S, kSegS, LB>(a, o, Mi, X, active, amask, t, tm);
 
     // Phase 4: reconstruct the inner rows, separator = t; sparse source epilogue (LODIE1).
     if (!a.ends || seg == 0 || seg == (m - 1) / S)  // ends-only: rows 1 and m
@@ -678,6 +691,185 @@ __device__ __forceinline__ void tile_body(const SweepArgs& a, const TileGeo& g, 
 }
 
 
+// r[j] += v for a runtime j (unrolled selects keep r in registers).
+template <int S>
+__device__ __forceinline__ void add_at(double (&r)[S], int j, double v) {
+#pragma unroll
+  for (int k = 0; k < S; ++k)
+    if (k == j) r[k] = __dadd_rn(r[k], v);
+}
+
+// Sparse charged-node fix-up on register rows: r[j] += coef * rr[j * st] for the set bits of
+// cmask (a rolled loop, so the rare source loads are not hoisted into registers).
+template <int S>
+__device__ __forceinline__ void fix_regs(double (&r)[S], unsigned cmask, double coef,
+                                         const double* rr, long long st) {
+  while (cmask) {
+    const int j = __ffs(cmask) - 1;
+    cmask &= cmask - 1;
+    add_at<S>(r, j, __dmul_rn(coef, rr[j * st]));
+  }
+}
+
+// Column sweeps without a staged tile (axes 0 and 1).  Thread (lane, seg) loads the S rows
+// of its segment straight into registers -- one warp-wide load covers two 128-byte row
+// chunks of 16 adjacent columns -- eliminates, joins the block-wide reduced system, and
+// stores its rows back from registers.  Shared memory holds only the tables and the
+// reduced-system scratch: no block-wide wait for a staged tile, no shared-memory round trip
+// of the field.  Block (LB columns, kSegS segments), grid (column groups, outer index).
+template <int S, int kSegS, bool CN, int LB>
+__global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
+    k_sweep_col(const SweepArgs a, const int axis) {
+  extern __shared__ double sm[];
+  constexpr int NT = LB * kSegS;
+  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
+  const int lane = threadIdx.x, seg = threadIdx.y, tid = seg * LB + lane;
+  const TileGeo g = tile_geo<LB, false>(a, axis, blockIdx.x, blockIdx.y, gridDim.y);
+  const int m = a.m, i0 = seg * S;
+  const bool act = lane < g.ncols;
+  const long long st = g.stride, gl = g.base + lane;  // this thread's line
+  const int K = a.L.n2 - 2;                            // lines per outer index
+
+  // The own descriptor and rows first (registers), then the tables (shared memory).
+  unsigned long long amask = 0ull, w1 = 0ull;
+  if (act) {
+    const ulonglong2 dd = *reinterpret_cast<const ulonglong2*>(
+        a.desc + 2 * (((long long)(g.outer - 1) * kSegS + seg) * K + (g.c0 - 1 + lane)));
+    amask = dd.x;
+    w1 = dd.y;
+  }
+  const uint32_t sbits = (uint32_t)w1, cmask = (uint32_t)(w1 >> 32);
+  double r[S];
+  const double* srow = a.src + gl + (long long)(i0 + 1) * st;
+#pragma unroll
+  for (int j = 0; j < S; ++j) r[j] = (act && i0 + 1 + j <= m + 1) ? srow[j * st] : 0.0;
+  double bfold = 0.0;
+  if (act) {
+    if (seg == 0) bfold = a.bnd[gl];
+    else if (seg == (m - 1) / S) bfold = a.bnd[gl + a.hi_off];
+  }
+  double* T = sm;
+  double* Mi = T + kTabDoubles;
+  double* X = Mi + kSegS * (kSegS + 2);
+  double* FP = X + 4 * NT;
+  if (tid < 4) FP[tid] = tid == 0 ? a.decay0 : (tid == 1 ? a.sat0 : (tid == 2 ? a.decay1 : a.sat1));
+  if (tid < 2) reinterpret_cast<int*>(FP + 4)[tid] = a.foff[tid];
+  for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
+  if (a.static_ok)
+    for (int c = tid; c < kSegS * (kSegS + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
+  const bool flow = uses_flow(a.pro, a.epi);
+  if (flow)
+    for (int c = tid; c < a.fpoly_n / 2; c += NT) cp_async16(FP + kFlowHdr + 2 * c, a.fpoly + 2 * c);
+  cp_async_wait_all();
+  __syncthreads();
+  if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
+
+  const double* rr = a.rho + gl + (long long)(i0 + 1) * st;  // source of row j: rr[j * st]
+  // Prologue on the own rows: w = pm*flow(u) or w = u + dta*rho (charged nodes).
+  if (a.pro == PRO_FLOW) {
+    const double pm = a.pm;
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if (i0 + 1 + j <= m) r[j] = flow_sm(FP, r[j], (sbits >> j) & 1u, pm);
+    const int jf = m - i0;  // the far face row m+1, if inside this segment: Dirichlet data
+    if (CN && act && jf >= 0 && jf < S) {
+      const double bh = a.bnd[gl + a.hi_off];
+#pragma unroll
+      for (int j = 0; j < S; ++j)
+        if (j == jf) r[j] = bh;
+    }
+  } else if (a.pro == PRO_SRC && cmask) {
+    fix_regs<S>(r, cmask, a.pro_coef, rr, st);
+  }
+  if (CN) {  // explicit half along the axis; the rows just outside the segment, prologue applied
+    auto outside = [&](int p) {  // w at row p (0..m+1) of this line
+      if (p > m + 1 || !act) return 0.0;
+      if (p == 0 || p == m + 1) return a.pro == PRO_FLOW ? a.bnd[gl + (p ? a.hi_off : 0ll)]
+                                                          : a.src[gl + (long long)p * st];
+      double w = a.src[gl + (long long)p * st];
+      const uint32_t c = a.codes[gl + (long long)p * st];
+      if (a.pro == PRO_FLOW) w = flow_sm(FP, w, c & 1u, a.pm);
+      else if (a.pro == PRO_SRC && ((c >> 4) & 1u))
+        w = __dadd_rn(w, __dmul_rn(a.pro_coef, a.rho[gl + (long long)p * st]));
+      return w;
+    };
+    double wl = outside(i0);
+    const double wr = outside(i0 + S + 1);
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const double wc = r[j], wn = j + 1 < S ? r[j + 1] : wr;
+      r[j] = cn_term(a, (uint32_t)(amask >> j) & 1u, (uint32_t)(amask >> (j + 1)) & 1u, wl, wc,
+                     wn);
+      wl = wc;
+    }
+  }
+  if (a.has_extra && cmask) fix_regs<S>(r, cmask, a.extra, rr, st);
+  if (seg == 0 && act)
+    r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], bfold));
+  if (seg == (m - 1) / S && act)
+    fold_high<S>(a, r, amask, seg == 0 ? a.bnd[gl + a.hi_off] : bfold);
+
+  SegOut o;
+  const double* Tv = seg_eliminate<S>(a, r, amask, i0, seg == 0, T, o);
+  double t, tm;
+  reduced_solve<S, kSegS, LB>(a, o, Mi, X, act, amask, t, tm);
+  // Reconstruction in registers: x_j = y_j + alpha_j tm + beta_j t, separator = t.
+  if (Tv == nullptr) {
+#pragma unroll
+    for (int j = 0; j < S - 1; ++j)
+      r[j] = fma(a.tmid[TQ_BE * kTabRows + j], t, fma(a.tmid[TQ_AL * kTabRows + j], tm, r[j]));
+  } else {
+#pragma unroll
+    for (int j = 0; j < S - 1; ++j)
+      r[j] = fma(Tv[TQ_BE * kTabRows + j], t, fma(Tv[TQ_AL * kTabRows + j], tm, r[j]));
+  }
+  r[S - 1] = t;
+  if (a.epi == EPI_SRC && cmask) fix_regs<S>(r, cmask, a.epi_coef, rr, st);
+  if (!act) return;
+  if (a.ends) {  // slab phase A (axis 0): only the chunk's end rows 1 and m leave the block
+    if (seg == 0) a.ends[gl] = r[0];
+    const int jl = (m - 1) - i0;
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if (j == jl) a.ends[gl + a.ends_off] = r[j];
+    return;
+  }
+  // Epilogue and store of the own rows 1..m.
+  double* drow = a.dst + gl + (long long)(i0 + 1) * st;
+  const int epi = a.epi;
+  bool bad = false;
+  if ((epi == EPI_STORE || epi == EPI_SRC || epi == EPI_MAOS0) && !a.check) {
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if (i0 + 1 + j <= m) drow[j * st] = r[j];
+  } else {
+    const double* yrow = (epi == EPI_AOS0 ? a.src : a.acc) + gl + (long long)(i0 + 1) * st;
+    const bool needY = epi_needs(epi) != 0;
+    const double pm = a.pm;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      if (i0 + 1 + j > m) continue;
+      const uint32_t sb = (sbits >> j) & 1u;
+      const double yv = needY ? yrow[j * st] : 0.0;
+      double x;
+      switch (epi) {
+        case EPI_FLOW: x = flow_sm(FP, r[j], sb, 1.0); break;
+        case EPI_AOS0: x = __dadd_rn(flow_sm(FP, yv, sb, pm), r[j]); break;
+        case EPI_AOS1:
+        case EPI_MAOS1: x = __dadd_rn(yv, r[j]); break;
+        case EPI_AOS2: x = __dmul_rn(0.25, __dadd_rn(yv, r[j])); break;
+        case EPI_MAOS2: x = __ddiv_rn(__dadd_rn(yv, r[j]), 3.0); break;
+        default: x = r[j]; break;
+      }
+      drow[j * st] = x;
+      bad |= is_bad(x, a.thr);
+    }
+  }
+  if (a.check) {
+    if (__any_sync(__activemask(), bad) && bad) atomicMin(a.div_step, a.step);
+  }
+}
+
 // Single-tile kernel: block (x = column / row group, y = outer index).  Used when a second
 // staged operand (AOS/MAOS), the slab ends-only mode or a short launch rules out the
 // pipelined kernel below.
@@ -734,20 +926,16 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 256 ? 2 : 1)
   double* T = sm;
   double* Mi = T + kTabDoubles;
   double* X = Mi + kSegS * (kSegS + 2);
-  double* Wb[2];
-  Wb[0] = X + 4 * NT;
-  Wb[1] = Wb[0] + TD;
-  unsigned long long* Db[2];
-  Db[0] = reinterpret_cast<unsigned long long*>(Wb[1] + TD);
-  Db[1] = Db[0] + 2 * NT;
-  double* FP = reinterpret_cast<double*>(Db[1] + 2 * NT);
+  double* const W0 = X + 4 * NT;  // buffer b: W0 + b * TD, D0 + b * 2 * NT
+  unsigned long long* const D0 = reinterpret_cast<unsigned long long*>(W0 + 2 * TD);
+  double* FP = reinterpret_cast<double*>(D0 + 4 * NT);
   if (tid < 4) FP[tid] = tid == 0 ? a.decay0 : (tid == 1 ? a.sat0 : (tid == 2 ? a.decay1 : a.sat1));
   if (tid < 2) reinterpret_cast<int*>(FP + 4)[tid] = a.foff[tid];
   const int ntiles = ntx * nty;
   int tile = blockIdx.x;
   if (tile < ntiles)
-    stage_tile<S, kSegS, LB, RT>(a, tile_geo<LB, RT>(a, axis, tile % ntx, tile / ntx, nty), Wb[0],
-                                 nullptr, Db[0], 0);
+    stage_tile<S, kSegS, LB, RT>(a, tile_geo<LB, RT>(a, axis, tile % ntx, tile / ntx, nty), W0,
+                                 nullptr, D0, 0);
   for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
   if (a.static_ok)
     for (int c = tid; c < kSegS * (kSegS + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
@@ -762,13 +950,14 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 256 ? 2 : 1)
     const int next = tile + gridDim.x;
     if (next < ntiles)
       stage_tile<S, kSegS, LB, RT>(a, tile_geo<LB, RT>(a, axis, next % ntx, next / ntx, nty),
-                                   Wb[b ^ 1], nullptr, Db[b ^ 1], 0);
+                                   W0 + (b ^ 1) * TD, nullptr, D0 + (b ^ 1) * 2 * NT, 0);
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_group 1;\n" ::);  // the current tile (and the tables) landed
     const TileGeo g = tile_geo<LB, RT>(a, axis, tile % ntx, tile / ntx, nty);
-    const double bfold = tile_prefetch<S, kSegS, LB, RT>(a, g, Db[b]);
+    const double bfold = tile_prefetch<S, kSegS, LB, RT>(a, g, D0 + b * 2 * NT);
     __syncthreads();
-    tile_body<S, kSegS, CN, LB, RT>(a, g, T, Mi, Wb[b], nullptr, X, Db[b], FP, bfold);
+    tile_body<S, kSegS, CN, LB, RT>(a, g, T, Mi, W0 + b * TD, nullptr, X, D0 + b * 2 * NT, FP,
+                                    bfold);
     __syncthreads();  // buffer b is restaged two tiles later
   }
   cp_async_wait_all();
@@ -906,6 +1095,16 @@ static bool pipe_enabled(const SweepArgs& a) {
   return on && epi_needs(a.epi) == 0 && a.ends == nullptr;
 }
 
+// Column sweeps run register-direct (k_sweep_col) unless PBG_COL=0 selects the staged-tile
+// kernels, for comparison.
+static bool col_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PBG_COL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int S, int P, bool CN, int LB, bool RT>
 static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
   const int nouter = (axis == 0 ? a.L.n1 : a.L.n0) - 2;
@@ -939,7 +1138,21 @@ static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
 // Axis 0 rows are one field plane apart (MB strides): 128-byte row chunks keep DRAM pages
 // and TLB entries busy (64-byte chunks run at ~55% of copy bandwidth there, measured).
 template <int S, int P, bool CN>
+static void launch_col(const SweepArgs& a, int axis, cudaStream_t st) {
+  constexpr int LB = 16;
+  const int nouter = (axis == 0 ? a.L.n1 : a.L.n0) - 2;
+  const int ntx = (a.L.n2 - 2 + LB - 1) / LB;
+  const size_t smem =
+      sizeof(double) * (kTabDoubles + P * (P + 2) + 4 * LB * P + kFlowHdr + flow_stage_n(a));
+  auto kern = k_sweep_col<S, P, CN, LB>;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<dim3(ntx, nouter), dim3(LB, P), smem, st>>>(a, axis);
+}
+
+template <int S, int P, bool CN>
 static void launch_strided_SC(const SweepArgs& a, int axis, cudaStream_t st) {
+  if (axis < 2 && col_enabled()) return launch_col<S, P, CN>(a, axis, st);
   // 16-column tiles (128-byte row chunks) unless a second staged tile (AOS/MAOS epilogue
   // operand) would halve the resident blocks.
   // Tiles must also fit the 227 KB of shared memory per block (long lines with AOS/MAOS).
