@@ -435,8 +435,9 @@ __device__ __forceinline__ void stage_tile(const SweepArgs& a, const TileGeo& g,
   const int m = a.m, nl = m + 2;
   const int K = (RT ? L.n1 : L.n2) - 2;
   const double* gy_all = needY == 1 ? a.src : a.acc;
-  cp_async16(D + 2 * tid,
-             a.desc + 2 * (((long long)(g.outer - 1) * kSegS + seg) * K + (g.c0 - 1 + lane)));
+  if (D)
+    cp_async16(D + 2 * tid,
+               a.desc + 2 * (((long long)(g.outer - 1) * kSegS + seg) * K + (g.c0 - 1 + lane)));
   if (RT) {
     // rows 1..m+1 of each line in 16-byte chunks (row 1 is 256-byte aligned), row 0 alone
     const int nch = (m + 1) / 2;  // full chunks; an odd last row goes alone
@@ -703,7 +704,7 @@ __device__ __forceinline__ void add_at(double (&r)[S], int j, double v) {
 // cmask (a rolled loop, so the rare source loads are not hoisted into registers).
 template <int S>
 __device__ __forceinline__ void fix_regs(double (&r)[S], unsigned cmask, double coef,
-                                         const double* rr, long long st) {
+                                         const double* rr, int st) {
   while (cmask) {
     const int j = __ffs(cmask) - 1;
     cmask &= cmask - 1;
@@ -711,59 +712,21 @@ __device__ __forceinline__ void fix_regs(double (&r)[S], unsigned cmask, double 
   }
 }
 
-// Column sweeps without a staged tile (axes 0 and 1).  Thread (lane, seg) loads the S rows
-// of its segment straight into registers -- one warp-wide load covers two 128-byte row
-// chunks of 16 adjacent columns -- eliminates, joins the block-wide reduced system, and
-// stores its rows back from registers.  Shared memory holds only the tables and the
-// reduced-system scratch: no block-wide wait for a staged tile, no shared-memory round trip
-// of the field.  Block (LB columns, kSegS segments), grid (column groups, outer index).
+// Per-tile work of the column kernels once the thread's rows are in registers: r[j] = row
+// i0+1+j of the line (rows past m+1 zero), wl / wr = raw rows i0 and i0+S+1 (CN only).
+// Prologue, CN explicit half, folds, elimination, reduced system (block-wide barriers: every
+// thread of the block calls this), reconstruction, epilogue and the store of rows 1..m.
 template <int S, int kSegS, bool CN, int LB>
-__global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
-    k_sweep_col(const SweepArgs a, const int axis) {
-  extern __shared__ double sm[];
-  constexpr int NT = LB * kSegS;
-  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
-  const int lane = threadIdx.x, seg = threadIdx.y, tid = seg * LB + lane;
-  const TileGeo g = tile_geo<LB, false>(a, axis, blockIdx.x, blockIdx.y, gridDim.y);
+__device__ __forceinline__ void col_body(const SweepArgs& a, const TileGeo& g, double (&r)[S],
+                                         double wl, double wr, unsigned long long amask,
+                                         unsigned long long w1, double bfold, const double* T,
+                                         const double* Mi, double* X, const double* FP) {
+  const int lane = threadIdx.x, seg = threadIdx.y;
   const int m = a.m, i0 = seg * S;
   const bool act = lane < g.ncols;
-  const long long st = g.stride, gl = g.base + lane;  // this thread's line
-  const int K = a.L.n2 - 2;                            // lines per outer index
-
-  // The own descriptor and rows first (registers), then the tables (shared memory).
-  unsigned long long amask = 0ull, w1 = 0ull;
-  if (act) {
-    const ulonglong2 dd = *reinterpret_cast<const ulonglong2*>(
-        a.desc + 2 * (((long long)(g.outer - 1) * kSegS + seg) * K + (g.c0 - 1 + lane)));
-    amask = dd.x;
-    w1 = dd.y;
-  }
+  const int st = g.stride;  // 32-bit row offsets: one IMAD.WIDE per address
+  const long long gl = g.base + lane;
   const uint32_t sbits = (uint32_t)w1, cmask = (uint32_t)(w1 >> 32);
-  double r[S];
-  const double* srow = a.src + gl + (long long)(i0 + 1) * st;
-#pragma unroll
-  for (int j = 0; j < S; ++j) r[j] = (act && i0 + 1 + j <= m + 1) ? srow[j * st] : 0.0;
-  double bfold = 0.0;
-  if (act) {
-    if (seg == 0) bfold = a.bnd[gl];
-    else if (seg == (m - 1) / S) bfold = a.bnd[gl + a.hi_off];
-  }
-  double* T = sm;
-  double* Mi = T + kTabDoubles;
-  double* X = Mi + kSegS * (kSegS + 2);
-  double* FP = X + 4 * NT;
-  if (tid < 4) FP[tid] = tid == 0 ? a.decay0 : (tid == 1 ? a.sat0 : (tid == 2 ? a.decay1 : a.sat1));
-  if (tid < 2) reinterpret_cast<int*>(FP + 4)[tid] = a.foff[tid];
-  for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
-  if (a.static_ok)
-    for (int c = tid; c < kSegS * (kSegS + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
-  const bool flow = uses_flow(a.pro, a.epi);
-  if (flow)
-    for (int c = tid; c < a.fpoly_n / 2; c += NT) cp_async16(FP + kFlowHdr + 2 * c, a.fpoly + 2 * c);
-  cp_async_wait_all();
-  __syncthreads();
-  if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
-
   const double* rr = a.rho + gl + (long long)(i0 + 1) * st;  // source of row j: rr[j * st]
   // Prologue on the own rows: w = pm*flow(u) or w = u + dta*rho (charged nodes).
   if (a.pro == PRO_FLOW) {
@@ -782,19 +745,17 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
     fix_regs<S>(r, cmask, a.pro_coef, rr, st);
   }
   if (CN) {  // explicit half along the axis; the rows just outside the segment, prologue applied
-    auto outside = [&](int p) {  // w at row p (0..m+1) of this line
+    auto outside = [&](int p, double w) {  // w = raw value of row p (0..m+1) of this line
       if (p > m + 1 || !act) return 0.0;
-      if (p == 0 || p == m + 1) return a.pro == PRO_FLOW ? a.bnd[gl + (p ? a.hi_off : 0ll)]
-                                                          : a.src[gl + (long long)p * st];
-      double w = a.src[gl + (long long)p * st];
+      if (p == 0 || p == m + 1) return a.pro == PRO_FLOW ? a.bnd[gl + (p ? a.hi_off : 0ll)] : w;
       const uint32_t c = a.codes[gl + (long long)p * st];
       if (a.pro == PRO_FLOW) w = flow_sm(FP, w, c & 1u, a.pm);
       else if (a.pro == PRO_SRC && ((c >> 4) & 1u))
         w = __dadd_rn(w, __dmul_rn(a.pro_coef, a.rho[gl + (long long)p * st]));
       return w;
     };
-    double wl = outside(i0);
-    const double wr = outside(i0 + S + 1);
+    wl = outside(i0, wl);
+    wr = outside(i0 + S + 1, wr);
 #pragma unroll
     for (int j = 0; j < S; ++j) {
       const double wc = r[j], wn = j + 1 < S ? r[j + 1] : wr;
@@ -839,9 +800,14 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
   const int epi = a.epi;
   bool bad = false;
   if ((epi == EPI_STORE || epi == EPI_SRC || epi == EPI_MAOS0) && !a.check) {
+    if (i0 + S <= m) {  // whole segment inside the line: no per-row predicates
 #pragma unroll
-    for (int j = 0; j < S; ++j)
-      if (i0 + 1 + j <= m) drow[j * st] = r[j];
+      for (int j = 0; j < S; ++j) drow[j * st] = r[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < S; ++j)
+        if (i0 + 1 + j <= m) drow[j * st] = r[j];
+    }
   } else {
     const double* yrow = (epi == EPI_AOS0 ? a.src : a.acc) + gl + (long long)(i0 + 1) * st;
     const bool needY = epi_needs(epi) != 0;
@@ -865,14 +831,85 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
       bad |= is_bad(x, a.thr);
     }
   }
-  if (a.check) {
-    if (__any_sync(__activemask(), bad) && bad) atomicMin(a.div_step, a.step);
-  }
+  if (a.check && bad) atomicMin(a.div_step, a.step);
 }
 
-// Single-tile kernel: block (x = column / row group, y = outer index).  Used when a second
-// staged operand (AOS/MAOS), the slab ends-only mode or a short launch rules out the
-// pipelined kernel below.
+// Stage the block's tables (uniform-segment LU tables, clean-line inverse, flow palette and
+// interval tables) with cp.async; the caller commits.
+template <int kSegS>
+__device__ __forceinline__ void stage_tables(const SweepArgs& a, double* T, double* Mi,
+                                             double* FP, int tid, int NT) {
+  if (tid < 4) FP[tid] = tid == 0 ? a.decay0 : (tid == 1 ? a.sat0 : (tid == 2 ? a.decay1 : a.sat1));
+  if (tid < 2) reinterpret_cast<int*>(FP + 4)[tid] = a.foff[tid];
+  for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
+  if (a.static_ok)
+    for (int c = tid; c < kSegS * (kSegS + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
+  if (uses_flow(a.pro, a.epi))
+    for (int c = tid; c < a.fpoly_n / 2; c += NT) cp_async16(FP + kFlowHdr + 2 * c, a.fpoly + 2 * c);
+}
+
+template <int kSegS>
+__device__ __forceinline__ const unsigned long long* col_desc(const SweepArgs& a,
+                                                              const TileGeo& g) {
+  return a.desc + 2 * (((long long)(g.outer - 1) * kSegS + threadIdx.y) * (a.L.n2 - 2) +
+                       (g.c0 - 1 + threadIdx.x));
+}
+
+// Column sweeps without a staged tile (axes 0 and 1).  Thread (lane, seg) loads the S rows
+// of its segment straight into registers -- one warp-wide load covers two 128-byte row
+// chunks of 16 adjacent columns -- eliminates, joins the block-wide reduced system, and
+// stores its rows back from registers.  Shared memory holds only the tables and the
+// reduced-system scratch.  Block (LB columns, kSegS segments), grid (column groups, outer).
+template <int S, int kSegS, bool CN, int LB>
+__global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
+    k_sweep_col(const SweepArgs a, const int axis) {
+  extern __shared__ double sm[];
+  constexpr int NT = LB * kSegS;
+  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
+  const int tid = threadIdx.y * LB + threadIdx.x;
+  const TileGeo g = tile_geo<LB, false>(a, axis, blockIdx.x, blockIdx.y, gridDim.y);
+  const int m = a.m, i0 = threadIdx.y * S;
+  const bool act = threadIdx.x < g.ncols;
+  const int st = g.stride;
+  const long long gl = g.base + threadIdx.x;
+  unsigned long long amask = 0ull, w1 = 0ull;
+  if (act) {
+    const ulonglong2 dd = *reinterpret_cast<const ulonglong2*>(col_desc<kSegS>(a, g));
+    amask = dd.x;
+    w1 = dd.y;
+  }
+  double r[S];
+  const double* srow = a.src + gl + (long long)(i0 + 1) * st;
+  if (act && i0 + S <= m + 1) {  // whole segment inside rows 1..m+1: no per-row predicates
+#pragma unroll
+    for (int j = 0; j < S; ++j) r[j] = srow[j * st];
+  } else {
+#pragma unroll
+    for (int j = 0; j < S; ++j) r[j] = (act && i0 + 1 + j <= m + 1) ? srow[j * st] : 0.0;
+  }
+  double wl = 0.0, wr = 0.0;
+  if (CN && act) {
+    if (i0 <= m + 1) wl = a.src[gl + (long long)i0 * st];
+    if (i0 + S + 1 <= m + 1) wr = a.src[gl + (long long)(i0 + S + 1) * st];
+  }
+  double bfold = 0.0;
+  if (act) {
+    if (threadIdx.y == 0) bfold = a.bnd[gl];
+    else if ((int)threadIdx.y == (m - 1) / S) bfold = a.bnd[gl + a.hi_off];
+  }
+  double* T = sm;
+  double* Mi = T + kTabDoubles;
+  double* X = Mi + kSegS * (kSegS + 2);
+  double* FP = X + 4 * NT;
+  stage_tables<kSegS>(a, T, Mi, FP, tid, NT);
+  cp_async_wait_all();
+  __syncthreads();
+  if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
+  col_body<S, kSegS, CN, LB>(a, g, r, wl, wr, amask, w1, bfold, T, Mi, X, FP);
+}
+
+// Staged-tile kernel: block (x = column / row group, y = outer index).  Serves the row
+// sweeps (axis 2) and, with PBG_COL=0, the column sweeps.
 template <int S, int kSegS, bool CN, int LB, bool RT>
 __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSegS <= 256 ? 3 : 2))
     k_sweep_strided(const SweepArgs a, const int axis) {
@@ -909,58 +946,6 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
   __syncthreads();
   if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
   tile_body<S, kSegS, CN, LB, RT>(a, g, T, Mi, W, Yt, X, D, FP, bfold);
-}
-
-// Persistent, double-buffered kernel (plain launches: no second staged operand, no ends-only
-// mode): one block per SM walks tiles blockIdx.x, blockIdx.x + gridDim.x, ...; the next tile
-// is staged into the other buffer while the current one is solved and stored, so the memory
-// traffic of tile k+1 overlaps the compute of tile k.
-template <int S, int kSegS, bool CN, int LB, bool RT>
-__global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 256 ? 2 : 1)
-    k_sweep_pipe(const SweepArgs a, const int axis, const int ntx, const int nty) {
-  extern __shared__ double sm[];
-  using TS = TileShape<S, kSegS, LB, RT>;
-  constexpr int NT = TS::NT, TD = TS::TD;
-  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
-  const int tid = threadIdx.y * LB + threadIdx.x;
-  double* T = sm;
-  double* Mi = T + kTabDoubles;
-  double* X = Mi + kSegS * (kSegS + 2);
-  double* const W0 = X + 4 * NT;  // buffer b: W0 + b * TD, D0 + b * 2 * NT
-  unsigned long long* const D0 = reinterpret_cast<unsigned long long*>(W0 + 2 * TD);
-  double* FP = reinterpret_cast<double*>(D0 + 4 * NT);
-  if (tid < 4) FP[tid] = tid == 0 ? a.decay0 : (tid == 1 ? a.sat0 : (tid == 2 ? a.decay1 : a.sat1));
-  if (tid < 2) reinterpret_cast<int*>(FP + 4)[tid] = a.foff[tid];
-  const int ntiles = ntx * nty;
-  int tile = blockIdx.x;
-  if (tile < ntiles)
-    stage_tile<S, kSegS, LB, RT>(a, tile_geo<LB, RT>(a, axis, tile % ntx, tile / ntx, nty), W0,
-                                 nullptr, D0, 0);
-  for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
-  if (a.static_ok)
-    for (int c = tid; c < kSegS * (kSegS + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
-  if (uses_flow(a.pro, a.epi))
-    for (int c = tid; c < a.fpoly_n / 2; c += NT) cp_async16(FP + kFlowHdr + 2 * c, a.fpoly + 2 * c);
-  asm volatile("cp.async.commit_group;\n" ::);
-  if (dstep < a.step) {  // an earlier step diverged: nothing more to compute
-    cp_async_wait_all();
-    return;
-  }
-  for (int b = 0; tile < ntiles; tile += gridDim.x, b ^= 1) {
-    const int next = tile + gridDim.x;
-    if (next < ntiles)
-      stage_tile<S, kSegS, LB, RT>(a, tile_geo<LB, RT>(a, axis, next % ntx, next / ntx, nty),
-                                   W0 + (b ^ 1) * TD, nullptr, D0 + (b ^ 1) * 2 * NT, 0);
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 1;\n" ::);  // the current tile (and the tables) landed
-    const TileGeo g = tile_geo<LB, RT>(a, axis, tile % ntx, tile / ntx, nty);
-    const double bfold = tile_prefetch<S, kSegS, LB, RT>(a, g, D0 + b * 2 * NT);
-    __syncthreads();
-    tile_body<S, kSegS, CN, LB, RT>(a, g, T, Mi, W0 + b * TD, nullptr, X, D0 + b * 2 * NT, FP,
-                                    bfold);
-    __syncthreads();  // buffer b is restaged two tiles later
-  }
-  cp_async_wait_all();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1078,23 +1063,6 @@ static int seg_P(int axis, int m) {
   return m <= 128 ? 8 : (m <= 256 ? 16 : 32);
 }
 
-template <int LB, bool RT>
-static size_t pipe_smem(int S, int kSegS, int fpoly_n) {
-  return sizeof(double) * (kTabDoubles + kSegS * (kSegS + 2) + 4 * LB * kSegS +
-                           2 * tile_doubles<LB, RT>(S, kSegS) + 2 * 2 * LB * kSegS + kFlowHdr +
-                           fpoly_n);
-}
-
-// The persistent double-buffered kernel serves every launch without a second staged operand
-// or the slab ends-only mode (PBG_PIPE=0 selects the single-tile kernel, for comparison).
-static bool pipe_enabled(const SweepArgs& a) {
-  static const bool on = [] {
-    const char* e = getenv("PBG_PIPE");
-    return !(e && e[0] == '0');
-  }();
-  return on && epi_needs(a.epi) == 0 && a.ends == nullptr;
-}
-
 // Column sweeps run register-direct (k_sweep_col) unless PBG_COL=0 selects the staged-tile
 // kernels, for comparison.
 static bool col_enabled() {
@@ -1111,22 +1079,6 @@ static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
   const int nlines = (RT ? a.L.n1 : a.L.n2) - 2;
   const int ntx = (nlines + LB - 1) / LB;
   dim3 block(LB, P);
-  if (pipe_enabled(a)) {
-    const size_t smem = pipe_smem<LB, RT>(S, P, flow_stage_n(a));
-    if (smem <= 232448) {
-      auto kern = k_sweep_pipe<S, P, CN, LB, RT>;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      int dev = 0, nsm = 148, bps = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, LB * P, smem);
-      if (bps > 0) {
-        const int grid = std::min(ntx * nouter, nsm * bps);
-        kern<<<grid, block, smem, st>>>(a, axis, ntx, nouter);
-        return;
-      }
-    }
-  }
   dim3 grid(ntx, nouter);
   const size_t smem = strided_smem<LB, RT>(S, P, epi_needs(a.epi) != 0, flow_stage_n(a));
   if (smem > 48 * 1024)
