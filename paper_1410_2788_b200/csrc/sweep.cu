@@ -67,13 +67,14 @@ __host__ __device__ __forceinline__ int epi_needs(int epi) {
                                 : 0);
 }
 
-// Flow palette constants staged in shared memory: (decay, sat) pairs indexed by the solute
-// bit, the two table offsets, then the interval tables (FP + kFlowHdr).
+// Flow interval tables staged in shared memory at FP + kFlowHdr (kFlowHdr: alignment slack).
 constexpr int kFlowHdr = 6;
-__device__ __forceinline__ double flow_sm(const double* FP, double w, uint32_t s, double pm) {
-  const double2 v = reinterpret_cast<const double2*>(FP)[s];
-  const int off = reinterpret_cast<const int*>(FP + 4)[s];
-  return sinh_flow_poly(w, v.x, v.y, pm, FP + kFlowHdr + off);
+// Palette constants come from the kernel parameters (constant bank, selected by the solute
+// bit), the interval tables from shared memory.
+__device__ __forceinline__ double flow_sm(const SweepArgs& a, const double* FP, double w,
+                                          uint32_t s, double pm) {
+  const double d = s ? a.decay1 : a.decay0, sat = s ? a.sat1 : a.sat0;
+  return sinh_flow_poly(w, d, sat, pm, FP + kFlowHdr + (s ? a.foff[1] : a.foff[0]));
 }
 
 __host__ __device__ __forceinline__ bool uses_flow(int pro, int epi) {
@@ -220,16 +221,6 @@ __device__ __forceinline__ void seg_finish(const SweepArgs& a, const double* Tv,
     uni_finish<S, WS>(r, [&](int q, int j) { return Tv[q * kTabRows + j]; }, tm, t, w0);
 }
 
-// Reduced-system coefficients of separator k (needs the next segment's first-row values).
-__device__ __forceinline__ void reduced_row(const SegOut& o, double yFn, double aFn,
-                                            double bFn, double& A, double& B, double& C,
-                                            double& R) {
-  A = o.as * o.aL;
-  B = o.bs + o.as * o.bL + o.cs * aFn;
-  C = o.cs * bFn;
-  R = o.rs - o.as * o.yL - o.cs * yFn;
-}
-
 // ---------------------------------------------------------------------------------------
 // Strided axes (0, 1).  blockDim = (LB columns, 32 segments); block (x = k group, y = outer).
 // Shared memory: tables | reduced inverse | W[NR][LB] stage/solution | Y[NR][LB] (AOS/MAOS)
@@ -312,8 +303,8 @@ __device__ __forceinline__ void reduced_solve(const SweepArgs& a, const SegOut& 
       bFn = sC[tid + LB];
     }
     __syncthreads();
-    double A, B, Cc, R;
-    reduced_row(o, yFn, aFn, bFn, A, B, Cc, R);
+    double A = o.as * o.aL, B = o.bs + o.as * o.bL + o.cs * aFn, Cc = o.cs * bFn,
+           R = o.rs - o.as * o.yL - o.cs * yFn;
 #pragma unroll
     for (int d = 1; d < kSegS; d <<= 1) {
       sA[tid] = A;
@@ -554,13 +545,13 @@ __device__ __forceinline__ void tile_body(const SweepArgs& a, const TileGeo& g, 
       for (int p = 1 + tid; p < nl - 1; p += NT) {
         const int sg = (p - 1) / S, sb = (p - 1) - sg * S;
         for (int l = 0; l < ncols; ++l)
-          W[l * RS + 1 + p] = flow_sm(FP, W[l * RS + 1 + p], solute(sg, sb, l), pm);
+          W[l * RS + 1 + p] = flow_sm(a, FP, W[l * RS + 1 + p], solute(sg, sb, l), pm);
       }
     } else {
       const int l = tid % LB;
       for (int p = 1 + tid / LB; p < nl - 1; p += NT / LB) {
         const int sg = (p - 1) / S;
-        W[p * LB + l] = flow_sm(FP, W[p * LB + l], solute(sg, (p - 1) - sg * S, l), pm);
+        W[p * LB + l] = flow_sm(a, FP, W[p * LB + l], solute(sg, (p - 1) - sg * S, l), pm);
       }
     }
     __syncthreads();
@@ -573,7 +564,14 @@ __device__ __forceinline__ void tile_body(const SweepArgs& a, const TileGeo& g, 
     // Phase 2: rhs of the own rows (registers), local elimination.
     const bool active = lane < ncols;
     double r[S];
-    {
+    if (RT && !CN && S % 2 == 0) {  // rows i0+1.. of a row tile: 16-byte aligned pairs
+#pragma unroll
+      for (int j = 0; j < S; j += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(w0 + j);
+        r[j] = v.x;
+        r[j + 1] = v.y;
+      }
+    } else {
       const double* wrow = w0;
 #pragma unroll
       for (int j = 0; j < S; ++j) {
@@ -600,9 +598,27 @@ __device__ __forceinline__ void tile_body(const SweepArgs& a, const TileGeo& g, 
     reduced_solve<S, kSegS, LB>(a, o, Mi, X, active, amask, t, tm);
 
     // Phase 4: reconstruct the inner rows, separator = t; sparse source epilogue (LODIE1).
-    if (!a.ends || seg == 0 || seg == (m - 1) / S)  // ends-only: rows 1 and m
-      seg_finish<S, WS>(a, Tv, r, tm, t, w0);
-    if (i0 + S - 1 < m) w0[(S - 1) * WS] = t;
+    if (RT && S % 2 == 0) {
+      // Row tiles: the separator slot of the last segment lies past row m (inside the line's
+      // stride, never stored), so whole 16-byte pairs are written.
+      if (Tv == nullptr) {
+#pragma unroll
+        for (int j = 0; j < S - 1; ++j)
+          r[j] = fma(a.tmid[TQ_BE * kTabRows + j], t, fma(a.tmid[TQ_AL * kTabRows + j], tm, r[j]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < S - 1; ++j)
+          r[j] = fma(Tv[TQ_BE * kTabRows + j], t, fma(Tv[TQ_AL * kTabRows + j], tm, r[j]));
+      }
+      r[S - 1] = t;
+#pragma unroll
+      for (int j = 0; j < S; j += 2)
+        *reinterpret_cast<double2*>(w0 + j) = make_double2(r[j], r[j + 1]);
+    } else {
+      if (!a.ends || seg == 0 || seg == (m - 1) / S)  // ends-only: rows 1 and m
+        seg_finish<S, WS>(a, Tv, r, tm, t, w0);
+      if (i0 + S - 1 < m) w0[(S - 1) * WS] = t;
+    }
     if (a.epi == EPI_SRC && cmask)
       charged_fixup(cmask, a.epi_coef, [&](int j) { return w0 + j * WS; }, rho_row);
     __syncthreads();
@@ -669,10 +685,10 @@ __device__ __forceinline__ void tile_body(const SweepArgs& a, const TileGeo& g, 
       const double pm = a.pm;
       switch (epi) {
         case EPI_FLOW:
-          loop([&](int c, uint32_t b) { return flow_sm(FP, W[c], b, 1.0); });
+          loop([&](int c, uint32_t b) { return flow_sm(a, FP, W[c], b, 1.0); });
           break;
         case EPI_AOS0:
-          loop([&](int c, uint32_t b) { return __dadd_rn(flow_sm(FP, Yt[c], b, pm), W[c]); });
+          loop([&](int c, uint32_t b) { return __dadd_rn(flow_sm(a, FP, Yt[c], b, pm), W[c]); });
           break;
         case EPI_AOS1:
         case EPI_MAOS1: loop([&](int c, uint32_t) { return __dadd_rn(Yt[c], W[c]); }); break;
@@ -733,7 +749,7 @@ __device__ __forceinline__ void col_body(const SweepArgs& a, const TileGeo& g, d
     const double pm = a.pm;
 #pragma unroll
     for (int j = 0; j < S; ++j)
-      if (i0 + 1 + j <= m) r[j] = flow_sm(FP, r[j], (sbits >> j) & 1u, pm);
+      if (i0 + 1 + j <= m) r[j] = flow_sm(a, FP, r[j], (sbits >> j) & 1u, pm);
     const int jf = m - i0;  // the far face row m+1, if inside this segment: Dirichlet data
     if (CN && act && jf >= 0 && jf < S) {
       const double bh = a.bnd[gl + a.hi_off];
@@ -749,7 +765,7 @@ __device__ __forceinline__ void col_body(const SweepArgs& a, const TileGeo& g, d
       if (p > m + 1 || !act) return 0.0;
       if (p == 0 || p == m + 1) return a.pro == PRO_FLOW ? a.bnd[gl + (p ? a.hi_off : 0ll)] : w;
       const uint32_t c = a.codes[gl + (long long)p * st];
-      if (a.pro == PRO_FLOW) w = flow_sm(FP, w, c & 1u, a.pm);
+      if (a.pro == PRO_FLOW) w = flow_sm(a, FP, w, c & 1u, a.pm);
       else if (a.pro == PRO_SRC && ((c >> 4) & 1u))
         w = __dadd_rn(w, __dmul_rn(a.pro_coef, a.rho[gl + (long long)p * st]));
       return w;
@@ -819,8 +835,8 @@ __device__ __forceinline__ void col_body(const SweepArgs& a, const TileGeo& g, d
       const double yv = needY ? yrow[j * st] : 0.0;
       double x;
       switch (epi) {
-        case EPI_FLOW: x = flow_sm(FP, r[j], sb, 1.0); break;
-        case EPI_AOS0: x = __dadd_rn(flow_sm(FP, yv, sb, pm), r[j]); break;
+        case EPI_FLOW: x = flow_sm(a, FP, r[j], sb, 1.0); break;
+        case EPI_AOS0: x = __dadd_rn(flow_sm(a, FP, yv, sb, pm), r[j]); break;
         case EPI_AOS1:
         case EPI_MAOS1: x = __dadd_rn(yv, r[j]); break;
         case EPI_AOS2: x = __dmul_rn(0.25, __dadd_rn(yv, r[j])); break;
@@ -839,8 +855,6 @@ __device__ __forceinline__ void col_body(const SweepArgs& a, const TileGeo& g, d
 template <int kSegS>
 __device__ __forceinline__ void stage_tables(const SweepArgs& a, double* T, double* Mi,
                                              double* FP, int tid, int NT) {
-  if (tid < 4) FP[tid] = tid == 0 ? a.decay0 : (tid == 1 ? a.sat0 : (tid == 2 ? a.decay1 : a.sat1));
-  if (tid < 2) reinterpret_cast<int*>(FP + 4)[tid] = a.foff[tid];
   for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
   if (a.static_ok)
     for (int c = tid; c < kSegS * (kSegS + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
@@ -912,14 +926,12 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
 // sweeps (axis 2) and, with PBG_COL=0, the column sweeps.
 template <int S, int kSegS, bool CN, int LB, bool RT>
 __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSegS <= 256 ? 3 : 2))
-    k_sweep_strided(const SweepArgs a, const int axis) {
+    k_sweep_strided(const SweepArgs a, const int axis, const int ntx, const int nty) {
   extern __shared__ double sm[];
   using TS = TileShape<S, kSegS, LB, RT>;
   constexpr int NT = TS::NT, TD = TS::TD;
-  // divergence flag: issue the load now, decide after staging
   const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
   const int tid = threadIdx.y * LB + threadIdx.x;
-  const TileGeo g = tile_geo<LB, RT>(a, axis, blockIdx.x, blockIdx.y, gridDim.y);
   const int needY = epi_needs(a.epi);
   double* T = sm;
   double* Mi = T + kTabDoubles;
@@ -927,25 +939,29 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
   double* Yt = W + TD;
   double* X = Yt + (needY ? TD : 0);
   unsigned long long* D = reinterpret_cast<unsigned long long*>(X + 4 * NT);
-  double* FP = reinterpret_cast<double*>(D + 2 * NT);  // flow palette and tables
-  if (tid < 4) FP[tid] = tid == 0 ? a.decay0 : (tid == 1 ? a.sat0 : (tid == 2 ? a.decay1 : a.sat1));
-  if (tid < 2) reinterpret_cast<int*>(FP + 4)[tid] = a.foff[tid];
-
-  // Phase 1: asynchronous staging of the tile (own descriptor first), then the tables.
-  stage_tile<S, kSegS, LB, RT>(a, g, W, Yt, D, needY);
-  asm volatile("cp.async.commit_group;\n" ::);
+  double* FP = reinterpret_cast<double*>(D + 2 * NT);  // flow tables at FP + kFlowHdr
+  // The tables once per block; the block then walks tiles blockIdx.x, + gridDim.x, ...
   for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
   if (a.static_ok)
     for (int c = tid; c < kSegS * (kSegS + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
   if (uses_flow(a.pro, a.epi))
     for (int c = tid; c < a.fpoly_n / 2; c += NT) cp_async16(FP + kFlowHdr + 2 * c, a.fpoly + 2 * c);
   asm volatile("cp.async.commit_group;\n" ::);
-  asm volatile("cp.async.wait_group 1;\n" ::);
-  const double bfold = tile_prefetch<S, kSegS, LB, RT>(a, g, D);
-  cp_async_wait_all();
-  __syncthreads();
-  if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
-  tile_body<S, kSegS, CN, LB, RT>(a, g, T, Mi, W, Yt, X, D, FP, bfold);
+  if (dstep < a.step) {  // an earlier step diverged: nothing more to compute
+    cp_async_wait_all();
+    return;
+  }
+  const int ntiles = ntx * nty;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const TileGeo g = tile_geo<LB, RT>(a, axis, tile % ntx, tile / ntx, nty);
+    stage_tile<S, kSegS, LB, RT>(a, g, W, Yt, D, needY);
+    asm volatile("cp.async.commit_group;\n" ::);
+    cp_async_wait_all();
+    const double bfold = tile_prefetch<S, kSegS, LB, RT>(a, g, D);
+    __syncthreads();
+    tile_body<S, kSegS, CN, LB, RT>(a, g, T, Mi, W, Yt, X, D, FP, bfold);
+    __syncthreads();  // the tile buffers are restaged by the next iteration
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1079,12 +1095,17 @@ static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
   const int nlines = (RT ? a.L.n1 : a.L.n2) - 2;
   const int ntx = (nlines + LB - 1) / LB;
   dim3 block(LB, P);
-  dim3 grid(ntx, nouter);
   const size_t smem = strided_smem<LB, RT>(S, P, epi_needs(a.epi) != 0, flow_stage_n(a));
+  auto kern = k_sweep_strided<S, P, CN, LB, RT>;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_sweep_strided<S, P, CN, LB, RT>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_sweep_strided<S, P, CN, LB, RT><<<grid, block, smem, st>>>(a, axis);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // persistent blocks: as many as fit at once (the tables are staged once per block)
+  int dev = 0, nsm = 148, bps = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, LB * P, smem);
+  const int grid = std::min(ntx * nouter, nsm * std::max(bps, 1));
+  kern<<<grid, block, smem, st>>>(a, axis, ntx, nouter);
 }
 
 // Axis 0 rows are one field plane apart (MB strides): 128-byte row chunks keep DRAM pages
