@@ -43,6 +43,8 @@
 #include <tuple>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "sweep.cuh"
 
 namespace pbg {
@@ -887,10 +889,15 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
   const int st = g.stride;
   const long long gl = g.base + threadIdx.x;
   unsigned long long amask = 0ull, w1 = 0ull;
-  if (act) {
-    const ulonglong2 dd = *reinterpret_cast<const ulonglong2*>(col_desc<kSegS>(a, g));
-    amask = dd.x;
-    w1 = dd.y;
+  if (act) {  // word 1 (solute / charged bits) only where a prologue or epilogue needs it
+    const unsigned long long* dp = col_desc<kSegS>(a, g);
+    if (a.pro != PRO_NONE || a.has_extra || a.epi != EPI_STORE) {
+      const ulonglong2 dd = *reinterpret_cast<const ulonglong2*>(dp);
+      amask = dd.x;
+      w1 = dd.y;
+    } else {
+      amask = *dp;
+    }
   }
   double r[S];
   const double* srow = a.src + gl + (long long)(i0 + 1) * st;
@@ -1002,6 +1009,124 @@ __global__ void k_build_desc(const Layout L, int axis, int S, int P,
   }
 }
 
+// LU factors, alpha and beta of one general segment (5 x kTabRows doubles at F): rows j of
+// the segment are rows i0+j of the line; `first` = the segment starts the line (row 0 has no
+// sub-diagonal), d = m - i0 (row j >= d is a decoupled padding row, row d-1 has no
+// super-diagonal).  Same recurrences as the uniform tables (make_tables).
+__device__ void seg_factors(const AxisCoef& co, unsigned long long eb, int first, int d, int S,
+                            double* F) {
+  double cpp = 0.0, dap = 1.0, lastinv = 0.0, lastc = 0.0;
+  for (int j = 0; j < S - 1; ++j) {
+    const uint32_t em = (uint32_t)(eb >> j) & 1u, ep = (uint32_t)(eb >> (j + 1)) & 1u;
+    double av, bv, cv;
+    if (j >= d) {
+      av = 0.0;
+      bv = 1.0;
+      cv = 0.0;
+    } else {
+      av = (first && j == 0) ? 0.0 : (em ? co.sub[1] : co.sub[0]);
+      cv = (j == d - 1) ? 0.0 : (ep ? co.sup[1] : co.sup[0]);
+      bv = em ? (ep ? co.diag[3] : co.diag[2]) : (ep ? co.diag[1] : co.diag[0]);
+    }
+    const double inv = 1.0 / (bv - av * cpp);
+    const double cpj = cv * inv;
+    const double da = -(av * dap) * inv;
+    F[TQ_INV * kTabRows + j] = inv;
+    F[TQ_G * kTabRows + j] = av * inv;
+    F[TQ_CP * kTabRows + j] = cpj;
+    F[TQ_AL * kTabRows + j] = da;  // forward values, replaced by alpha below
+    cpp = cpj;
+    dap = da;
+    lastinv = inv;
+    lastc = cv;
+  }
+  double bb = -lastc * lastinv, aa = F[TQ_AL * kTabRows + S - 2];
+  F[TQ_BE * kTabRows + S - 2] = bb;
+  for (int j = S - 3; j >= 0; --j) {
+    const double c = F[TQ_CP * kTabRows + j];
+    aa = F[TQ_AL * kTabRows + j] - c * aa;
+    bb = -c * bb;
+    F[TQ_AL * kTabRows + j] = aa;
+    F[TQ_BE * kTabRows + j] = bb;
+  }
+}
+
+// General-segment factors depend only on (eps bits, first, min(m - i0, S)): segments that
+// share that key share one table.  The key space (S <= 16: 24 bits) is marked in a bitmap,
+// ranked by a prefix count, and each distinct key gets its factors once -- a few MB that stay
+// in L2 instead of 1.3 KB per segment streamed from HBM by every sweep.
+constexpr int kDedupMaxS = 16;
+__host__ __device__ __forceinline__ int key_bits(int S) { return S + 1 + 1 + 5; }
+
+__device__ __forceinline__ bool seg_general(unsigned long long w0, int S, int i0, int m,
+                                            int first, unsigned& key) {
+  const unsigned long long eb = eps_bits(w0, S);
+  const unsigned long long allm = (1ull << S) - 1ull, bits = eb & allm;
+  if (bits == 0ull || bits == allm) {
+    if (i0 + S <= m) return false;
+    if (i0 + S - 1 == m && !first) return false;
+  }
+  const int d = min(max(m - i0, 0), S);
+  key = (unsigned)eb | ((unsigned)first << (S + 1)) | ((unsigned)d << (S + 2));
+  return true;
+}
+
+__global__ void k_mark_keys(const Layout L, int axis, int S, int P,
+                            const unsigned long long* __restrict__ desc,
+                            unsigned* __restrict__ bitmap) {
+  const int m = (axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2)) - 2;
+  const int K = (axis == 2 ? L.n1 : L.n2) - 2;
+  const long long nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * K;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nseg;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int seg = (int)((t / K) % P);
+    unsigned key;
+    if (seg_general(desc[2 * t], S, seg * S, m, seg == 0, key))
+      if (!((bitmap[key >> 5] >> (key & 31)) & 1u)) atomicOr(bitmap + (key >> 5), 1u << (key & 31));
+  }
+}
+
+__global__ void k_popc_words(const unsigned* __restrict__ bitmap, int nw, int* __restrict__ cnt) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x)
+    cnt[w] = __popc(bitmap[w]);
+}
+
+// One thread per bitmap word: the factors of every distinct key, at its rank.
+__global__ void k_key_factors(AxisCoef co, int S, const unsigned* __restrict__ bitmap,
+                              const int* __restrict__ base, int nw, double* __restrict__ gfac) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
+    unsigned bits = bitmap[w];
+    int rank = base[w];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const unsigned key = ((unsigned)w << 5) | (unsigned)b;
+      const unsigned long long eb = key & ((2u << S) - 1u);
+      const int first = (key >> (S + 1)) & 1u, d = (int)(key >> (S + 2));
+      seg_factors(co, eb, first, d, S, gfac + (long long)rank * 5 * kTabRows);
+      ++rank;
+    }
+  }
+}
+
+__global__ void k_assign_slots(const Layout L, int axis, int S, int P,
+                               unsigned long long* __restrict__ desc,
+                               const unsigned* __restrict__ bitmap, const int* __restrict__ base) {
+  const int m = (axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2)) - 2;
+  const int K = (axis == 2 ? L.n1 : L.n2) - 2;
+  const long long nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * K;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nseg;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int seg = (int)((t / K) % P);
+    const unsigned long long w0 = desc[2 * t];
+    unsigned key;
+    if (!seg_general(w0, S, seg * S, m, seg == 0, key)) continue;
+    const unsigned w = key >> 5, below = bitmap[w] & ((1u << (key & 31)) - 1u);
+    const int rank = base[w] + __popc(below);
+    desc[2 * t] = w0 | ((unsigned long long)(rank + 1) << kSlotShift);
+  }
+}
+
 // General segments (not one dielectric, or partial at the line end): their LU factors,
 // alpha and beta are static for the march, so they are computed once here (same
 // recurrences as the uniform tables, per-row coefficients) and read like a table by the
@@ -1031,33 +1156,7 @@ __global__ void k_seg_factors(const Layout L, int axis, int S, int P, AxisCoef c
       continue;
     }
     const int slot = atomicAdd(counter, 1);
-    double* F = gfac + (long long)slot * 5 * kTabRows;
-    double cpp = 0.0, dap = 1.0, lastinv = 0.0, lastc = 0.0;
-    for (int j = 0; j < S - 1; ++j) {
-      double av, bv, cv;
-      row_coefs(co, i0 + j, m, (uint32_t)(eb >> j) & 1u, (uint32_t)(eb >> (j + 1)) & 1u, av, bv,
-                cv);
-      const double inv = 1.0 / (bv - av * cpp);
-      const double cpj = cv * inv;
-      const double da = -(av * dap) * inv;
-      F[TQ_INV * kTabRows + j] = inv;
-      F[TQ_G * kTabRows + j] = av * inv;
-      F[TQ_CP * kTabRows + j] = cpj;
-      F[TQ_AL * kTabRows + j] = da;  // forward values, replaced by alpha below
-      cpp = cpj;
-      dap = da;
-      lastinv = inv;
-      lastc = cv;
-    }
-    double bb = -lastc * lastinv, aa = F[TQ_AL * kTabRows + S - 2];
-    F[TQ_BE * kTabRows + S - 2] = bb;
-    for (int j = S - 3; j >= 0; --j) {
-      const double c = F[TQ_CP * kTabRows + j];
-      aa = F[TQ_AL * kTabRows + j] - c * aa;
-      bb = -c * bb;
-      F[TQ_AL * kTabRows + j] = aa;
-      F[TQ_BE * kTabRows + j] = bb;
-    }
+    seg_factors(co, eb, first, min(max(m - i0, 0), S), S, gfac + (long long)slot * 5 * kTabRows);
     desc[2 * t] = w0 | ((unsigned long long)(slot + 1) << kSlotShift);
   }
 }
@@ -1408,23 +1507,59 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
   k_build_desc<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, codes,
                                          aux.desc);
   PBG_LAUNCH_CHECK("k_build_desc");
-  int* counter = nullptr;
-  PBG_CUDA(cudaMallocAsync(&counter, sizeof(int), st));
-  PBG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-  k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, a.co, 0,
-                                          aux.desc, counter, nullptr);
-  PBG_LAUNCH_CHECK("k_seg_factors");
-  int ngen = 0;
-  PBG_CUDA(cudaMemcpyAsync(&ngen, counter, sizeof(int), cudaMemcpyDeviceToHost, st));
-  PBG_CUDA(cudaStreamSynchronize(st));  // also: the host staging vector dies here
-  PBG_CUDA(cudaMallocAsync(&aux.gfac, ((size_t)ngen + 1) * 5 * kTabRows * sizeof(double), st));
-  if (ngen > 0) {
+  if (S <= kDedupMaxS) {
+    const int nw = 1 << (key_bits(S) - 5);
+    unsigned* bitmap = nullptr;
+    int *cnt = nullptr, *base = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, base, nw, st);
+    PBG_CUDA(cudaMallocAsync(&bitmap, (size_t)nw * sizeof(unsigned), st));
+    PBG_CUDA(cudaMallocAsync(&cnt, (size_t)nw * sizeof(int), st));
+    PBG_CUDA(cudaMallocAsync(&base, (size_t)nw * sizeof(int), st));
+    PBG_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+    PBG_CUDA(cudaMemsetAsync(bitmap, 0, (size_t)nw * sizeof(unsigned), st));
+    k_mark_keys<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, aux.desc, bitmap);
+    PBG_LAUNCH_CHECK("k_mark_keys");
+    k_popc_words<<<(nw + 255) / 256, 256, 0, st>>>(bitmap, nw, cnt);
+    PBG_LAUNCH_CHECK("k_popc_words");
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, base, nw, st);
+    PBG_LAUNCH_CHECK("cub::DeviceScan");
+    int last[2] = {0, 0};
+    PBG_CUDA(cudaMemcpyAsync(&last[0], base + nw - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PBG_CUDA(cudaMemcpyAsync(&last[1], cnt + nw - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PBG_CUDA(cudaStreamSynchronize(st));  // also: the host staging vector dies here
+    const int ndist = last[0] + last[1];
+    PBG_CUDA(cudaMallocAsync(&aux.gfac, ((size_t)ndist + 1) * 5 * kTabRows * sizeof(double), st));
+    if (ndist > 0) {
+      k_key_factors<<<(nw + 255) / 256, 256, 0, st>>>(a.co, S, bitmap, base, nw, aux.gfac);
+      PBG_LAUNCH_CHECK("k_key_factors");
+      k_assign_slots<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, aux.desc, bitmap, base);
+      PBG_LAUNCH_CHECK("k_assign_slots");
+    }
+    PBG_CUDA(cudaFreeAsync(bitmap, st));
+    PBG_CUDA(cudaFreeAsync(cnt, st));
+    PBG_CUDA(cudaFreeAsync(base, st));
+    PBG_CUDA(cudaFreeAsync(tmp, st));
+  } else {  // long segments: one table per general segment
+    int* counter = nullptr;
+    PBG_CUDA(cudaMallocAsync(&counter, sizeof(int), st));
     PBG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-    k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, a.co, 1,
-                                           aux.desc, counter, aux.gfac);
+    k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, a.co, 0,
+                                            aux.desc, counter, nullptr);
     PBG_LAUNCH_CHECK("k_seg_factors");
+    int ngen = 0;
+    PBG_CUDA(cudaMemcpyAsync(&ngen, counter, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PBG_CUDA(cudaStreamSynchronize(st));  // also: the host staging vector dies here
+    PBG_CUDA(cudaMallocAsync(&aux.gfac, ((size_t)ngen + 1) * 5 * kTabRows * sizeof(double), st));
+    if (ngen > 0) {
+      PBG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
+      k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, a.co, 1,
+                                             aux.desc, counter, aux.gfac);
+      PBG_LAUNCH_CHECK("k_seg_factors");
+    }
+    PBG_CUDA(cudaFreeAsync(counter, st));
   }
-  PBG_CUDA(cudaFreeAsync(counter, st));
   a.gfac = aux.gfac;
   a.tab = aux.buf;
   a.minv = aux.buf + kTabDoubles;
