@@ -75,8 +75,11 @@ constexpr int kFlowHdr = 6;
 // bit), the interval tables from shared memory.
 __device__ __forceinline__ double flow_sm(const SweepArgs& a, const double* FP, double w,
                                           uint32_t s, double pm) {
-  const double d = s ? a.decay1 : a.decay0, sat = s ? a.sat1 : a.sat0;
-  return sinh_flow_poly(w, d, sat, pm, FP + kFlowHdr + (s ? a.foff[1] : a.foff[0]));
+  if (s) {  // solute palette: usually no ions (decay 1, the flow is the identity)
+    if (a.decay1 >= 1.0 || w != w) return pm != 1.0 ? pm * w : w;
+    return sinh_flow_poly(w, a.decay1, a.sat1, pm, FP + kFlowHdr + a.foff[1]);
+  }
+  return sinh_flow_poly(w, a.decay0, a.sat0, pm, FP + kFlowHdr + a.foff[0]);
 }
 
 __host__ __device__ __forceinline__ bool uses_flow(int pro, int epi) {
@@ -108,7 +111,9 @@ __device__ __forceinline__ double fast_rcp(double x) {
 }
 
 __device__ __forceinline__ bool is_bad(double v, double thr) {
-  return !isfinite(v) || fabs(v) > thr;
+  // non-finite or above the threshold; thr is clamped to DBL_MAX so that +-inf and NaN fail
+  // the single comparison
+  return !(fabs(v) <= fmin(thr, 1.7976931348623157e308));
 }
 
 // CN explicit half for row values (wm, wc, wp) with the row's eps bits (em, ep).
