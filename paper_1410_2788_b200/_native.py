@@ -15,7 +15,7 @@ import re
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpbg.so")
+LIB_PATH = os.environ.get("PBG_LIB") or os.path.join(_HERE, "_lib", "libpbg.so")  # PBG_LIB: A/B builds
 
 PBG_OFFSET = 31
 VARIANT_IDS = {"LODIE1": 0, "LODIE2": 1, "LODCN1": 2, "LODCN2": 3, "AOSIE1": 4, "AOSIE2": 5,

@@ -1193,6 +1193,28 @@ static bool col_enabled() {
   return on;
 }
 
+// Per (kernel, dynamic shared memory, device): raise the shared-memory limit once and cache
+// the resident blocks per SM x SM count, so launches issue no attribute / occupancy queries
+// (the config-5 batch issues ~40k launches from 8 host threads).
+static int resident_blocks(const void* fn, int nthreads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, size_t, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(fn, smem, dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int nsm = 148, bps = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, nthreads, smem);
+  const int r = nsm * std::max(bps, 1);
+  cache[key] = r;
+  return r;
+}
+
 template <int S, int P, bool CN, int LB, bool RT>
 static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
   const int nouter = (axis == 0 ? a.L.n1 : a.L.n0) - 2;
@@ -1201,14 +1223,8 @@ static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
   dim3 block(LB, P);
   const size_t smem = strided_smem<LB, RT>(S, P, epi_needs(a.epi) != 0, flow_stage_n(a));
   auto kern = k_sweep_strided<S, P, CN, LB, RT>;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // persistent blocks: as many as fit at once (the tables are staged once per block)
-  int dev = 0, nsm = 148, bps = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, LB * P, smem);
-  const int grid = std::min(ntx * nouter, nsm * std::max(bps, 1));
+  const int grid = std::min(ntx * nouter, resident_blocks((const void*)kern, LB * P, smem));
   kern<<<grid, block, smem, st>>>(a, axis, ntx, nouter);
 }
 
@@ -1222,8 +1238,7 @@ static void launch_col(const SweepArgs& a, int axis, cudaStream_t st) {
   const size_t smem =
       sizeof(double) * (kTabDoubles + P * (P + 2) + 4 * LB * P + kFlowHdr + flow_stage_n(a));
   auto kern = k_sweep_col<S, P, CN, LB>;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  resident_blocks((const void*)kern, LB * P, smem);  // shared-memory limit, once
   kern<<<dim3(ntx, nouter), dim3(LB, P), smem, st>>>(a, axis);
 }
 
