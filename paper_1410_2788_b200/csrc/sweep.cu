@@ -1242,6 +1242,16 @@ static void launch_col(const SweepArgs& a, int axis, cudaStream_t st) {
   kern<<<dim3(ntx, nouter), dim3(LB, P), smem, st>>>(a, axis);
 }
 
+// Row tiles of 16 lines for lines of <= 256 rows (256 threads per block: fewer duplicated
+// per-block tables per SM than 8-line tiles); PBG_RT16=0 keeps 8-line tiles, for comparison.
+static bool rt16_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PBG_RT16");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int S, int P, bool CN>
 static void launch_strided_SC(const SweepArgs& a, int axis, cudaStream_t st) {
   if (axis < 2 && col_enabled()) return launch_col<S, P, CN>(a, axis, st);
@@ -1255,6 +1265,7 @@ static void launch_strided_SC(const SweepArgs& a, int axis, cudaStream_t st) {
   else if (axis == 0) launch_strided_SCL<S, P, CN, 8, false>(a, axis, st);
   else if (axis == 1 && wide) launch_strided_SCL<S, P, CN, 16, false>(a, axis, st);
   else if (axis == 1) launch_strided_SCL<S, P, CN, 8, false>(a, axis, st);
+  else if (P <= 16 && rt16_enabled()) launch_strided_SCL<S, P, CN, 16, true>(a, axis, st);
   else launch_strided_SCL<S, P, CN, 8, true>(a, axis, st);
 }
 
