@@ -248,6 +248,13 @@ PBG_API int pbg_flow_dense(int64_t n, const double* w, const double* kappa2, dou
 #define PBG_FLOW_TABLE_DOUBLES 1008
 PBG_API int pbg_flow_table(double decay, double* out);
 
+/* Host only: the small-argument form the sweep kernels use for solvent nodes with
+ * |w| <= 2 (before the table): flow = w * sum g_q t^q, t = fma(w, w, -2), q = 0..15
+ * (PBG_FLOW_SMALL_DOUBLES coefficients g_q, Horner with fma).  Same replaced reference
+ * code as pbg_flow_table; exported for testing. */
+#define PBG_FLOW_SMALL_DOUBLES 16
+PBG_API int pbg_flow_small(double decay, double* out);
+
 /* Direct vacuum Poisson solve (vacuum_potential_fast, energy.py:59-85): -eps_m * d2(out) =
  * rho on the interior with out = bnd on the faces (bnd: pitched field whose faces hold the
  * Dirichlet data).  Boundary lifting, type-I DST along each axis (cuFFT D2Z of the odd

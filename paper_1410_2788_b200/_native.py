@@ -89,6 +89,7 @@ _SIGS = {
     "pbg_flow_dense": ([c_int64, c_void_p, c_void_p, c_double, c_double, c_void_p, c_void_p],
                        ctypes.c_int),
     "pbg_flow_table": ([c_double, c_void_p], ctypes.c_int),
+    "pbg_flow_small": ([c_double, c_void_p], ctypes.c_int),
     "pbg_energy_atoms": ([_P(PbgGrid), c_void_p, c_int32, c_void_p, c_void_p, c_double,
                           c_double, c_void_p, c_void_p, c_double, c_double, c_double,
                           _P(c_double), c_void_p], ctypes.c_int),

@@ -94,6 +94,23 @@ __device__ __forceinline__ double flow_poly(double x, const double* P) {
   return fma(p, t, q0.y);
 }
 
+// Small-argument flow: for |w| <= kFSmallX, F(w) = w * G(w^2) with G analytic in y = w^2
+// (nearest singularity at y = -pi^2), so one degree-15 polynomial in t = y - kFSmallX^2 / 2
+// (Chebyshev interpolation on y in [0, kFSmallX^2], built per decay on the host in extended
+// precision, sweep.cu build_flow_small) gives F to ~1 ulp relative.  Its 16 coefficients are
+// kernel parameters (constant-bank operands, the same for every lane): no table loads, so the
+// solvent far field -- most of the grid -- costs 17 fp64 operations and no shared memory.
+constexpr int kFSmallN = 16;
+constexpr double kFSmallX = 2.0;
+
+__host__ __device__ __forceinline__ double flow_small(double w, const double* g) {
+  const double t = fma(w, w, -0.5 * kFSmallX * kFSmallX);
+  double p = g[kFSmallN - 1];
+#pragma unroll
+  for (int q = kFSmallN - 2; q >= 0; --q) p = fma(p, t, g[q]);
+  return w * p;
+}
+
 // pm * flow(w) with the interval table P of decay d: d >= 1 passes w through, |w| > 38
 // (tanh(w/2) rounds to +-1 in the reference) gives +-sat = +-2 atanh(d), NaN propagates.
 __device__ __forceinline__ double sinh_flow_poly(double w, double d, double sat, double pm,

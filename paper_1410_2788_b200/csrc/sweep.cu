@@ -79,6 +79,10 @@ __device__ __forceinline__ double flow_sm(const SweepArgs& a, const double* FP, 
     if (a.decay1 >= 1.0 || w != w) return pm != 1.0 ? pm * w : w;
     return sinh_flow_poly(w, a.decay1, a.sat1, pm, FP + kFlowHdr + a.foff[1]);
   }
+  if (a.fsmall_on && fabs(w) <= kFSmallX) {  // solvent far field: no table loads
+    const double out = flow_small(w, a.fsmall);
+    return pm != 1.0 ? pm * out : out;
+  }
   return sinh_flow_poly(w, a.decay0, a.sat0, pm, FP + kFlowHdr + a.foff[0]);
 }
 
@@ -1410,50 +1414,81 @@ static bool make_reduced_inverse(const AxisCoef& co, const double* tab, int S, i
   return true;
 }
 
+// Interpolates f at the n Chebyshev nodes of [c - r, c + r] in extended precision and
+// re-expands the Chebyshev series in powers of t = x - c: out[q] = coefficient of t^q.
+template <int n, typename F>
+static void cheb_powers(F f, long double c, long double r, double* out) {
+  const long double pi = 3.141592653589793238462643383279502884L;
+  long double y[n], g[n];
+  for (int k = 0; k < n; ++k) y[k] = f(c + r * std::cos(pi * (k + 0.5L) / n));
+  for (int j = 0; j < n; ++j) {
+    long double acc = 0.0L;
+    for (int k = 0; k < n; ++k) acc += y[k] * std::cos(pi * j * (k + 0.5L) / n);
+    g[j] = (j == 0 ? 1.0L : 2.0L) * acc / n;
+  }
+  // sum_j g_j T_j(u), u = t / r, in powers of u (T_{j+1} = 2u T_j - T_{j-1})
+  long double Tp[n] = {0}, Tc[n] = {0}, b[n] = {0};
+  Tp[0] = 1.0L;
+  Tc[1] = 1.0L;
+  b[0] = g[0];
+  b[1] = g[1];
+  for (int j = 2; j < n; ++j) {
+    long double Tn[n] = {0};
+    for (int q = 0; q + 1 < n; ++q) Tn[q + 1] = 2.0L * Tc[q];
+    for (int q = 0; q < n; ++q) {
+      Tn[q] -= Tp[q];
+      b[q] += g[j] * Tn[q];
+      Tp[q] = Tc[q];
+      Tc[q] = Tn[q];
+    }
+  }
+  long double rp = 1.0L;
+  for (int q = 0; q < n; ++q, rp *= r) out[q] = (double)(b[q] / rp);
+}
+
 // Flow interval table of decay d (pbg_internal.cuh, flow_poly): on interval [lo, hi] the
 // map F(x) = 2 artanh(d tanh(x/2)) is interpolated at the 10 Chebyshev nodes in extended
 // precision, and the Chebyshev series is re-expanded in powers of t = x - c.
 static void build_flow_poly(double d, double* out) {
-  constexpr int n = 10;
-  const long double pi = 3.141592653589793238462643383279502884L;
   for (int iv = 0; iv < kFPolyIv; ++iv) {
     const int e = iv / 16, s = iv % 16;
     const double lo = std::ldexp(1.0 + s / 16.0, e) - 1.0;
     const double hi = std::ldexp(1.0 + (s + 1) / 16.0, e) - 1.0;
     const double c = 0.5 * (lo + hi);
     const long double r = 0.5L * ((long double)hi - (long double)lo);
-    long double y[n], g[n];
-    for (int k = 0; k < n; ++k) {
-      const long double x = (long double)c + r * std::cos(pi * (k + 0.5L) / n);
-      y[k] = 2.0L * std::atanh((long double)d * std::tanh(0.5L * x));
-    }
-    for (int j = 0; j < n; ++j) {
-      long double acc = 0.0L;
-      for (int k = 0; k < n; ++k) acc += y[k] * std::cos(pi * j * (k + 0.5L) / n);
-      g[j] = (j == 0 ? 1.0L : 2.0L) * acc / n;
-    }
-    // sum_j g_j T_j(u), u = t / r, in powers of u (T_{j+1} = 2u T_j - T_{j-1})
-    long double Tp[n] = {0}, Tc[n] = {0}, b[n] = {0};
-    Tp[0] = 1.0L;
-    Tc[1] = 1.0L;
-    b[0] = g[0];
-    b[1] = g[1];
-    for (int j = 2; j < n; ++j) {
-      long double Tn[n] = {0};
-      for (int q = 0; q + 1 < n; ++q) Tn[q + 1] = 2.0L * Tc[q];
-      for (int q = 0; q < n; ++q) {
-        Tn[q] -= Tp[q];
-        b[q] += g[j] * Tn[q];
-        Tp[q] = Tc[q];
-        Tc[q] = Tn[q];
-      }
-    }
     double* o = out + iv * kFPolyStride;
     o[0] = c;
-    long double rp = 1.0L;
-    for (int q = 0; q < n; ++q, rp *= r) o[1 + q] = (double)(b[q] / rp);
+    cheb_powers<10>(
+        [&](long double x) { return 2.0L * std::atanh((long double)d * std::tanh(0.5L * x)); },
+        (long double)c, r, o + 1);
     o[kFPolyStride - 1] = 0.0;
   }
+}
+
+// Small-argument flow of decay d (pbg_internal.cuh, flow_small): G(y) = F(sqrt y) / sqrt y on
+// y in [0, kFSmallX^2] (G(0) = d), in powers of t = y - kFSmallX^2 / 2.
+static void build_flow_small(double d, double* out) {
+  const long double Y = (long double)kFSmallX * kFSmallX;
+  cheb_powers<kFSmallN>(
+      [&](long double y) {
+        const long double x = std::sqrt(y);
+        return 2.0L * std::atanh((long double)d * std::tanh(0.5L * x)) / x;
+      },
+      0.5L * Y, 0.5L * Y, out);
+}
+
+// Host cache of the small-argument coefficients per decay (set_decays runs per launch).
+static void flow_small_coefs(double d, double* out) {
+  static std::mutex mu;
+  static std::map<double, std::vector<double>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(d);
+  if (it == cache.end()) {
+    std::vector<double> g(kFSmallN);
+    build_flow_small(d, g.data());
+    it = cache.emplace(d, std::move(g)).first;
+  }
+  std::copy(it->second.begin(), it->second.end(), out);
 }
 
 // Device copy of the interval tables of a decay pair, [palette slot][kFPolyDoubles], cached
@@ -1497,6 +1532,8 @@ void set_decays(SweepArgs& a, double d0, double d1) {
   a.fpoly_n = ntab * kFPolyDoubles;
   a.foff[0] = 0;  // palette 0 has slot 0 when it needs one
   a.foff[1] = (d0 < 1.0 && d1 < 1.0 && d1 != d0) ? kFPolyDoubles : 0;
+  a.fsmall_on = d0 >= 0.0 && d0 < 1.0;
+  if (a.fsmall_on) flow_small_coefs(d0, a.fsmall);
 }
 
 SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, double factor) {
@@ -1745,6 +1782,14 @@ extern "C" PBG_API int pbg_flow_table(double decay, double* out) {
   if (!out) return fail(PBG_E_INVALID, "null pointer");
   if (!(decay >= 0.0 && decay < 1.0)) return fail(PBG_E_INVALID, "decay must be in [0, 1)");
   build_flow_poly(decay, out);
+  return PBG_OK;
+}
+
+extern "C" PBG_API int pbg_flow_small(double decay, double* out) {
+  static_assert(kFSmallN == PBG_FLOW_SMALL_DOUBLES, "small-argument flow size");
+  if (!out) return fail(PBG_E_INVALID, "null pointer");
+  if (!(decay >= 0.0 && decay < 1.0)) return fail(PBG_E_INVALID, "decay must be in [0, 1)");
+  build_flow_small(decay, out);
   return PBG_OK;
 }
 

@@ -1,5 +1,5 @@
-"""CPU checks of the flow interval table the sweep kernels evaluate (pbg_flow_table, host
-only): the piecewise polynomial, evaluated the way the device does, against the oracle's
+"""CPU checks of the flow interval table and the small-argument polynomial the sweep kernels
+evaluate (pbg_flow_table / pbg_flow_small, host only): the piecewise polynomial, evaluated the way the device does, against the oracle's
 restatement of _apply_flow (pbsplit/schemes.py:88-103) and an extended-precision value."""
 
 import ctypes
@@ -76,3 +76,48 @@ def test_flow_table_rejects_bad_decay():
     out = np.zeros(N)
     for d in (1.0, 1.5, -0.1, float("nan")):
         assert lib.pbg_flow_table(d, out.ctypes.data_as(ctypes.c_void_p)) != 0
+
+
+def small(decay):
+    lib = nat.load_library()
+    out = np.zeros(16, dtype=np.float64)
+    nat.check(lib.pbg_flow_small(decay, out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def small_eval(w, g):
+    """Device evaluation (pbg_internal.cuh flow_small) in numpy, |w| <= 2."""
+    t = w * w - 2.0
+    p = np.full_like(w, g[-1])
+    for q in g[-2::-1]:
+        p = p * t + q
+    return w * p
+
+
+@pytest.mark.parametrize("decay", [0.529131809679411, 0.6541980527948197, 0.880466373414563,
+                                   0.9186325916063356, 0.99, 0.1, 1e-3, 0.0])
+def test_flow_small_matches_reference_flow(decay):
+    g = small(decay)
+    rng = np.random.default_rng(3)
+    w = np.concatenate([rng.uniform(-2, 2, 20000), rng.uniform(-1e-3, 1e-3, 2000),
+                        [0.0, -0.0, 2.0, -2.0, 1e-300, np.nextafter(2.0, 0)]])
+    got = small_eval(w, g)
+    assert np.max(np.abs(got - O.sinh_flow(w, decay))) <= 4e-15
+    mp.mp.dps = 30
+    sub = w[::41]
+    exact = np.array([float(2 * mp.atanh(decay * mp.tanh(mp.mpf(v) / 2))) for v in sub])
+    err = np.abs(small_eval(sub, g) - exact)
+    # ~1 ulp relative (numpy has no fma; the device Horner is fused)
+    assert np.max(err / np.maximum(np.abs(exact), 1e-300)) <= 1e-15
+    assert np.max(err) <= 1e-15
+    # the small form and the table agree where both apply
+    if decay > 0:
+        T = table(decay)
+        assert np.max(np.abs(got - poly_eval(w, T))) <= 1e-15
+
+
+def test_flow_small_rejects_bad_decay():
+    lib = nat.load_library()
+    out = np.zeros(16)
+    for d in (1.0, -0.1, float("nan")):
+        assert lib.pbg_flow_small(d, out.ctypes.data_as(ctypes.c_void_p)) != 0
