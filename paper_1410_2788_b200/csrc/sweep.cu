@@ -86,6 +86,24 @@ __device__ __forceinline__ double flow_sm(const SweepArgs& a, const double* FP, 
   return sinh_flow_poly(w, a.decay0, a.sat0, pm, FP + kFlowHdr + a.foff[0]);
 }
 
+// pm * flow of four independent nodes in place: the small-argument polynomial for all of
+// them first (branch-free, so the four Horner chains interleave), then flow_sm for the rare
+// others (solute palette, |w| > kFSmallX, no small form).  Same results as flow_sm per node.
+__device__ __forceinline__ void flow_group(const SweepArgs& a, const double* FP, double& w0,
+                                           double& w1, double& w2, double& w3, uint32_t s0,
+                                           uint32_t s1, uint32_t s2, uint32_t s3, double pm) {
+  const double x0 = flow_small(w0, a.fsmall), x1 = flow_small(w1, a.fsmall);
+  const double x2 = flow_small(w2, a.fsmall), x3 = flow_small(w3, a.fsmall);
+  auto fin = [&](double& w, double x, uint32_t s) {
+    if (s || !a.fsmall_on || !(fabs(w) <= kFSmallX)) w = flow_sm(a, FP, w, s, pm);
+    else w = pm != 1.0 ? pm * x : x;
+  };
+  fin(w0, x0, s0);
+  fin(w1, x1, s1);
+  fin(w2, x2, s2);
+  fin(w3, x3, s3);
+}
+
 __host__ __device__ __forceinline__ bool uses_flow(int pro, int epi) {
   return pro == PRO_FLOW || epi == EPI_FLOW || epi == EPI_AOS0;
 }
@@ -671,7 +689,30 @@ __device__ __forceinline__ void tile_body(const SweepArgs& a, const TileGeo& g, 
         }
       }
     };
-    if (plain && RT) {  // rows 1..m: 16-byte chunks (1,2), (3,4), ...; an odd last row alone
+    if (RT && !CN && epi == EPI_FLOW) {  // LODIE2 flow: four lines at a time
+      for (int p = 1 + tid; p <= m; p += NT) {
+        double* gp = a.dst + base + p;
+        const int sg = (p - 1) / S, sb = (p - 1) - sg * S;
+        int l = 0;
+        for (; l + 4 <= ncols; l += 4) {
+          double x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[u] = W[(l + u) * RS + 1 + p];
+          flow_group(a, FP, x[0], x[1], x[2], x[3], solute(sg, sb, l), solute(sg, sb, l + 1),
+                     solute(sg, sb, l + 2), solute(sg, sb, l + 3), 1.0);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            gp[(long long)(l + u) * L.pitch] = x[u];
+            bad |= is_bad(x[u], a.thr);
+          }
+        }
+        for (; l < ncols; ++l) {
+          const double x = flow_sm(a, FP, W[l * RS + 1 + p], solute(sg, sb, l), 1.0);
+          gp[(long long)l * L.pitch] = x;
+          bad |= is_bad(x, a.thr);
+        }
+      }
+    } else if (plain && RT) {  // rows 1..m: 16-byte chunks (1,2), (3,4), ...; an odd last row alone
       const int nch = m / 2;
       for (int c = tid; c < nch; c += NT) {
         double* g = a.dst + base + 1 + 2 * c;
