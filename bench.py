@@ -208,23 +208,35 @@ def e2e_measure(p, c, dp, nsteps):
     return wall, h2d, d2h, float(np.isfinite(out_h[n0 // 2].numpy()).all())
 
 
-def oracle_slab(p, dp, nplanes):
-    """CPU oracle problem for planes i < nplanes of the device problem (test/baseline
-    infrastructure): same codes, source and faces; plane nplanes-1 acts as a Dirichlet face."""
-    import torch
-
-    from oracle import pbs_oracle as O
+def host_planes(dp, grid, i0, i1):
+    """Planes i0 <= i < i1 of the device problem's codes, source and boundary buffers."""
     from paper_1410_2788_b200 import _native as nat
 
-    g = p.grid
-    n0, n1, n2 = g.shape
+    n0, n1, n2 = grid.shape
     pitch = dp.gs.pitch
     sl = slice(nat.PBG_OFFSET, nat.PBG_OFFSET + n2)
     nn = n0 * n1 * pitch
-    codes = dp.codes[:nn].view(n0, n1, pitch)[:nplanes, :, sl].cpu().numpy()
-    rho = dp.rho[:nn].view(n0, n1, pitch)[:nplanes, :, sl].cpu().numpy().copy()
-    bv = dp.bnd[:nn].view(n0, n1, pitch)[:nplanes, :, sl].cpu().numpy().copy()
+    pick = lambda t: t[:nn].view(n0, n1, pitch)[i0:i1, :, sl].cpu().numpy()
+    return pick(dp.codes), pick(dp.rho), pick(dp.bnd)
+
+
+def oracle_slab(p, dp, nplanes, planes=None, i0=0):
+    """CPU oracle problem for planes i0 <= i < i0+nplanes of the device problem (test/baseline
+    infrastructure): same codes, source and faces; the slab's first and last planes act as
+    Dirichlet faces.  `planes` = host_planes(...) of a range starting at plane 0 of the slab
+    sample set (reused by the reference arm's workers)."""
+    from oracle import pbs_oracle as O
+
+    g = p.grid
+    n0, n1, n2 = g.shape
+    if planes is None:
+        planes = host_planes(dp, g, i0, i0 + nplanes)
+        i0 = 0
+    codes = planes[0][i0:i0 + nplanes]
+    rho = planes[1][i0:i0 + nplanes].copy()
+    bv = planes[2][i0:i0 + nplanes].copy()
     rho[-1] = 0.0
+    rho[0] = 0.0
     eps = dp.pal.as_tuple()[0]
     k2p = dp.pal.as_tuple()[1]
     pick = lambda bit, pal: np.where((codes & bit) != 0, pal[1], pal[0])
@@ -234,7 +246,6 @@ def oracle_slab(p, dp, nplanes):
     og = O.OGrid(g.lo, g.h, (nplanes, n1, n2))
     init = np.zeros(og.shape)
     O.apply_faces(init, bv)
-    del torch
     return O.OProblem(og, region, rho, np.zeros(og.shape), bv, p.alpha, init)
 
 
@@ -540,30 +551,64 @@ def slab_main(args, c, p, t_asm, world, rank, local, dist):
     dist.destroy_process_group()
 
 
+_REF = {}  # reference-arm state, inherited by the forked workers (not pickled)
+
+
+def _reference_worker(i0):
+    """One host core of the reference arm: build its plane sample's oracle stepper (untimed),
+    wait for the others, then time `steps` steps.  Runs in a forked child (numpy only)."""
+    p, dp, planes, nplanes, variant, dt, steps, barrier = (
+        _REF[k] for k in ("p", "dp", "planes", "nplanes", "variant", "dt", "steps", "barrier"))
+    from oracle import pbs_oracle as O
+
+    op = oracle_slab(p, dp, nplanes, planes=planes, i0=i0)
+    st = O.OStepper(op, variant, dt)
+    u = op.initial.copy()
+    barrier.wait(timeout=900)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        u = st.step(u)
+    return time.perf_counter() - t0
+
+
 def reference_arm(args, world, rank):
     """CPU reference arm: the numpy oracle port of pbsplit's Stepper (the reference itself
-    is Python and cannot travel to the box), on a bounded sample of the same workload."""
+    is Python and cannot travel to the box) on every host core the process may use: one
+    forked worker per core, each stepping its own 65-plane sample of the same workload
+    concurrently; throughput = all workers' interior updates / the slowest worker's time."""
     if rank != 0:
         return
+    import multiprocessing as mp
+
     import torch
 
     torch.cuda.set_device(0)
     c, p, _ = build_problem(args.config)  # device assembly only to produce identical inputs
     from paper_1410_2788_b200.schemes import device_problem
-    from oracle import pbs_oracle as O
 
     dp = device_problem(p)
     nplanes = 65
-    op = oracle_slab(p, dp, nplanes)
-    st = O.OStepper(op, c.variant, c.dt)
-    u = op.initial.copy()
+    n0 = p.grid.shape[0]
+    cores = len(os.sched_getaffinity(0))
+    try:  # ~40 sample-sized fp64 arrays per worker (stepper factors and temporaries)
+        import psutil
+
+        per = 40 * 8 * nplanes * p.grid.shape[1] * p.grid.shape[2]
+        cores = max(1, min(cores, int(0.6 * psutil.virtual_memory().available // per)))
+    except ImportError:
+        pass
+    nw = cores
+    offs = [w * (n0 - nplanes) // max(1, nw - 1) for w in range(nw)] if nw > 1 else [0]
+    planes = host_planes(dp, p.grid, 0, n0)  # shared with the forked workers
     steps = max(1, min(args.steps, 3))
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        u = st.step(u)
-    wall = time.perf_counter() - t0
+    ctx = mp.get_context("fork")
+    _REF.update(p=p, dp=dp, planes=planes, nplanes=nplanes, variant=c.variant, dt=c.dt, steps=steps,
+                barrier=ctx.Barrier(nw))
+    with ctx.Pool(nw) as pool:
+        walls = pool.map(_reference_worker, offs, chunksize=1)
     nint = (nplanes - 2) * (c.n - 2) ** 2
-    v = nint * steps / wall
+    wall = max(walls)
+    v = nw * nint * steps / wall
     line = {"metric": "LOD grid-point updates/s (fp64)", "value": v,
             "unit": "grid-point updates/s", "n_gpus": world, "steps": steps, "warmup": 0,
             "ms_per_step": wall / steps * 1e3, "higher_is_better": True, "scaling": "weak",
@@ -571,10 +616,13 @@ def reference_arm(args, world, rank):
             "config": {"workload": c.name, "grid": [c.n] * 3, "variant": c.variant,
                        "dt": c.dt, "sample_planes": nplanes},
             "impl": "reference",
-            "cpu_baseline": {"value": v, "unit": "grid-point updates/s", "cores": 1,
+            "cpu_baseline": {"value": v, "unit": "grid-point updates/s", "cores": nw,
                              "kind": "port",
-                             "sample": f"{steps} {c.variant} step(s) of {c.name} restricted "
-                                       f"to planes i<{nplanes} ({nint} interior nodes)"},
+                             "sample": f"{nw} concurrent workers (one per host core), each "
+                                       f"{steps} {c.variant} step(s) of {c.name} restricted "
+                                       f"to its own {nplanes}-plane slab ({nint} interior "
+                                       f"nodes); per-worker s: "
+                                       f"{[round(w, 2) for w in walls]}"},
             "e2e": {"value": v, "unit": "grid-point updates/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
