@@ -1022,11 +1022,239 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
 }
 
 // ---------------------------------------------------------------------------------------
+// Row sweeps (axis 2) with G = 32 or 16 lanes per line, for lines of m = G*S - 1 interior
+// rows (n2 = 65, 129, 257, 513) and the LOD epilogues (store, LODIE1 source, LODIE2 flow).
+// Lane `seg` of a line owns segment seg (rows seg*S+1 .. seg*S+S; the last separator is the
+// far face, a padding row), so the reduced system over the G separators is solved inside the
+// warp (clean lines: the static inverse, one dot product; others: PCR with shuffles).  Warps
+// never wait for one another: after the block stages its tables, each warp stages its own
+// 32/G lines (cp.async, 16-byte chunks, segments padded by two doubles so that the lanes'
+// 16-byte row loads are conflict-free), solves them, and stores them in coalesced 256-byte
+// row runs, then takes the next lines.  Descriptors are line-major here (G per line).
+constexpr int kRWarps = 8;
+
+// Line-major descriptor index of axis-2 line (i, j).
+__device__ __forceinline__ long long line_desc(const Layout& L, int i, int j) {
+  return (long long)(i - 1) * (L.n1 - 2) + (j - 1);
+}
+
+template <int S, int G>
+struct RowWarp {
+  static constexpr int NL = 32 / G;         // lines per warp
+  static constexpr int SP = S + 2;          // padded segment stride (doubles)
+  static constexpr int LW = G * SP + 2;     // one line buffer (rows 1..G*S at pos(p))
+  static constexpr int RW = G + 2;          // separator scratch of one line
+  static constexpr int WD = NL * (LW + RW); // per-warp doubles
+  __device__ static __forceinline__ int pos(int p) {  // p = 1..G*S
+    return 2 + (p - 1) + 2 * ((p - 1) / S);
+  }
+};
+
+__host__ __device__ constexpr size_t rowwarp_smem(int S, int G, int fpoly_n) {
+  return sizeof(double) * (kTabDoubles + G * (G + 2) +
+                           (size_t)kRWarps * (32 / G) * (G * (S + 2) + 2 + G + 2) + kFlowHdr +
+                           fpoly_n);
+}
+
+template <int S, int G>
+__global__ void __launch_bounds__(kRWarps * 32, 3)
+    k_sweep_rowwarp(const SweepArgs a, const int nlines) {
+  extern __shared__ double sm[];
+  using RW = RowWarp<S, G>;
+  constexpr int NL = RW::NL;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int NT = kRWarps * 32;
+  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sub = lane / G, seg = lane % G;
+  double* T = sm;
+  double* Mi = T + kTabDoubles;             // G x (G + 2) (rows padded)
+  double* Wb = Mi + G * (G + 2);
+  double* FP = Wb + kRWarps * RW::WD;       // flow tables at FP + kFlowHdr
+  for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
+  if (a.static_ok)
+    for (int c = tid; c < G * (G + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
+  if (uses_flow(a.pro, a.epi))
+    for (int c = tid; c < a.fpoly_n / 2; c += NT) cp_async16(FP + kFlowHdr + 2 * c, a.fpoly + 2 * c);
+  asm volatile("cp.async.commit_group;\n" ::);
+  cp_async_wait_all();
+  __syncthreads();
+  if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
+
+  const Layout& L = a.L;
+  const int m = a.m, K = L.n1 - 2, i0 = seg * S;
+  double* W = Wb + warp * RW::WD + sub * RW::LW;          // this lane's line
+  double* sR = Wb + warp * RW::WD + NL * RW::LW + sub * RW::RW;
+  bool bad = false;
+  for (int wl = blockIdx.x * kRWarps + warp; wl * NL < nlines; wl += gridDim.x * kRWarps) {
+    const int line = wl * NL + sub;
+    const bool valid = NL == 1 || line < nlines;  // NL == 1: the loop condition
+    // planes in reverse (the axis-1 sweep before this one wrote the last planes last)
+    const int i = valid ? (L.n0 - 2) - line / K : 1, j = valid ? 1 + line % K : 1;
+    const long long base = L.at(i, j, 0);
+    unsigned long long amask = 0ull;
+    uint32_t sbits = 0u, cmask = 0u;
+    double bfold = 0.0;
+    if (valid) {
+      // stage rows 1..G*S (row G*S = m+1, the far face) in 16-byte chunks
+      const double* gsrc = a.src + base + 1;
+#pragma unroll
+      for (int q = 0; q < S / 2; ++q) {
+        const int c = seg + G * q;  // chunk c: rows 2c+1, 2c+2 (one segment, S even)
+        cp_async16(W + RW::pos(2 * c + 1), gsrc + 2 * c);
+      }
+      const ulonglong2 dd = *reinterpret_cast<const ulonglong2*>(
+          a.desc + 2 * (line_desc(L, i, j) * G + seg));
+      amask = dd.x;
+      sbits = (uint32_t)dd.y;
+      cmask = (uint32_t)(dd.y >> 32);
+      if (seg == 0) bfold = a.bnd[base];
+      else if (seg == (m - 1) / S) bfold = a.bnd[base + a.hi_off];
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    {  // the warp's next lines towards L2 while this one is solved (LODIE1 c4: 533 -> 498 us)
+      const int nl = (wl + gridDim.x * kRWarps) * NL + sub;
+      if (nl < nlines) {
+        const double* np = a.src + L.at((L.n0 - 2) - nl / K, 1 + nl % K, 0) + 1;
+        for (int c = seg; c < G * S / 16; c += G)  // 128-byte lines
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(np + 16 * c));
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+
+    double r[S];
+#pragma unroll
+    for (int q = 0; q < S; q += 2) {
+      const double2 v = valid ? *reinterpret_cast<const double2*>(W + 2 + seg * RW::SP + q)
+                              : make_double2(0.0, 0.0);
+      r[q] = v.x;
+      r[q + 1] = v.y;
+    }
+    if (seg == 0 && valid)
+      r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], bfold));
+    if (seg == (m - 1) / S && valid)
+      fold_high<S>(a, r, amask, seg == 0 ? a.bnd[base + a.hi_off] : bfold);
+    SegOut o;
+    const double* Tv = seg_eliminate<S>(a, r, amask, i0, seg == 0, T, o);
+
+    // reduced system over the G separators of each line
+    double t, tm;
+    const bool nx = seg + 1 < G;
+    const double yFn = __shfl_down_sync(FULL, o.yF, 1, G);
+    const bool clean = __all_sync(FULL, eps_bits(amask, S) == 0ull) && a.static_ok;
+    if (clean) {
+      sR[seg] = o.rs - o.as * o.yL - o.cs * (nx ? yFn : 0.0);
+      __syncwarp();
+      const double2* Rr = reinterpret_cast<const double2*>(sR);
+      const double2* Mr = reinterpret_cast<const double2*>(Mi + seg * (G + 2));
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int q = 0; q < G / 2; q += 2) {
+        const double2 r0 = Rr[q], m0 = Mr[q], r1 = Rr[q + 1], m1 = Mr[q + 1];
+        s0 = fma(m0.x, r0.x, s0);
+        s1 = fma(m0.y, r0.y, s1);
+        s2 = fma(m1.x, r1.x, s2);
+        s3 = fma(m1.y, r1.y, s3);
+      }
+      t = (s0 + s1) + (s2 + s3);
+    } else {  // parallel cyclic reduction with shuffles
+      const double aFn = __shfl_down_sync(FULL, o.aF, 1, G);
+      const double bFn = __shfl_down_sync(FULL, o.bF, 1, G);
+      double A = o.as * o.aL, B = o.bs + o.as * o.bL + o.cs * (nx ? aFn : 0.0),
+             Cc = o.cs * (nx ? bFn : 0.0), R = o.rs - o.as * o.yL - o.cs * (nx ? yFn : 0.0);
+#pragma unroll
+      for (int d = 1; d < G; d <<= 1) {
+        const double iB = fast_rcp(B);
+        const double Am = __shfl_up_sync(FULL, A, d, G), iBm = __shfl_up_sync(FULL, iB, d, G),
+                     Cm = __shfl_up_sync(FULL, Cc, d, G), Rm = __shfl_up_sync(FULL, R, d, G);
+        const double Ap = __shfl_down_sync(FULL, A, d, G), iBp = __shfl_down_sync(FULL, iB, d, G),
+                     Cp = __shfl_down_sync(FULL, Cc, d, G), Rp = __shfl_down_sync(FULL, R, d, G);
+        const bool lo = seg >= d, hi = seg + d < G;
+        const double k1 = lo ? -A * iBm : 0.0, k2 = hi ? -Cc * iBp : 0.0;
+        A = lo ? k1 * Am : 0.0;
+        Cc = hi ? k2 * Cp : 0.0;
+        B = B + (lo ? k1 * Cm : 0.0) + (hi ? k2 * Ap : 0.0);
+        R = R + (lo ? k1 * Rm : 0.0) + (hi ? k2 * Rp : 0.0);
+      }
+      t = R * fast_rcp(B);
+    }
+    tm = __shfl_up_sync(FULL, t, 1, G);
+    if (seg == 0) tm = 0.0;
+
+    // reconstruct the own rows (separator = t) and put them back into the line buffer
+    if (Tv == nullptr) {
+#pragma unroll
+      for (int q = 0; q < S - 1; ++q)
+        r[q] = fma(a.tmid[TQ_BE * kTabRows + q], t, fma(a.tmid[TQ_AL * kTabRows + q], tm, r[q]));
+    } else {
+#pragma unroll
+      for (int q = 0; q < S - 1; ++q)
+        r[q] = fma(Tv[TQ_BE * kTabRows + q], t, fma(Tv[TQ_AL * kTabRows + q], tm, r[q]));
+    }
+    r[S - 1] = t;
+    if (a.epi == EPI_SRC && cmask) fix_regs<S>(r, cmask, a.epi_coef, a.rho + base + i0 + 1, 1);
+    if (valid) {
+#pragma unroll
+      for (int q = 0; q < S; q += 2)
+        *reinterpret_cast<double2*>(W + 2 + seg * RW::SP + q) = make_double2(r[q], r[q + 1]);
+    }
+    __syncwarp();
+
+    // epilogue + coalesced store of rows 1..m of each line: lane = row within a 32-row run
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      const int ln = wl * NL + l;
+      if (ln >= nlines) break;  // warp-uniform
+      const long long bl = NL == 1 ? base : L.at((L.n0 - 2) - ln / K, 1 + ln % K, 0);
+      const double* Wl = Wb + warp * RW::WD + l * RW::LW;
+      double* gdst = a.dst + bl;
+      if (a.epi == EPI_FLOW) {  // lanes = consecutive rows: the small-argument form for
+                                // almost every node, solute bits from the owning lane
+#pragma unroll
+        for (int q = 0; q < G * S / 32; q += 4) {
+          double x[4];
+          uint32_t sv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int p = 1 + lane + 32 * (q + u);
+            x[u] = Wl[RW::pos(p)];
+            sv[u] = (__shfl_sync(FULL, sbits, l * G + (p - 1) / S) >> ((p - 1) % S)) & 1u;
+          }
+          flow_group(a, FP, x[0], x[1], x[2], x[3], sv[0], sv[1], sv[2], sv[3], 1.0);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int p = 1 + lane + 32 * (q + u);
+            if (p <= m) {
+              gdst[p] = x[u];
+              bad |= is_bad(x[u], a.thr);
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < G * S / 32; ++q) {
+          const int p = 1 + lane + 32 * q;
+          if (p <= m) {
+            const double x = Wl[RW::pos(p)];
+            gdst[p] = x;
+            if (a.check) bad |= is_bad(x, a.thr);
+          }
+        }
+      }
+    }
+    __syncwarp();  // the line buffers are restaged by the next lines
+  }
+  if (a.check && __any_sync(FULL, bad) && lane == 0) atomicMin(a.div_step, a.step);
+}
+
+// ---------------------------------------------------------------------------------------
 // Segment descriptors, built once per march and axis from the 1-byte node codes:
 //   word 0: bit j = eps bit (axis) of the node of row i0+j, j = 0..S (zero past node m+1)
 //   word 1: bits 0..S-1 solute bit of the nodes of rows i0..i0+S-1; bits 32.. charged bits
-// Layout: strided axes ((outer-1)*32 + seg)*K + (k-1); contiguous axis line*32 + seg.
-__global__ void k_build_desc(const Layout L, int axis, int S, int P,
+// Layout: ((outer-1)*P + seg)*K + (line-1); line-major ((outer-1)*K + line-1)*P + seg for the
+// row-warp sweeps (lm).
+__global__ void k_build_desc(const Layout L, int axis, int S, int P, int lm,
                              const uint8_t* __restrict__ codes,
                              unsigned long long* __restrict__ desc) {
   const int m = (axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2)) - 2;
@@ -1035,10 +1263,18 @@ __global__ void k_build_desc(const Layout L, int axis, int S, int P,
   const int sh = 1 + axis;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nseg;
        t += (long long)gridDim.x * blockDim.x) {
-    const int c = 1 + (int)(t % K);
-    const long long os = t / K;
-    const int seg = (int)(os % P);
-    const int outer = 1 + (int)(os / P);
+    int c, seg, outer;
+    if (lm) {  // line-major (row-warp sweeps): t = (line * P + seg)
+      seg = (int)(t % P);
+      const long long line = t / P;
+      c = 1 + (int)(line % K);
+      outer = 1 + (int)(line / K);
+    } else {
+      c = 1 + (int)(t % K);
+      const long long os = t / K;
+      seg = (int)(os % P);
+      outer = 1 + (int)(os / P);
+    }
     const long long base =
         axis == 0 ? L.at(0, outer, c) : (axis == 1 ? L.at(outer, 0, c) : L.at(outer, c, 0));
     const long long stride = axis == 0 ? L.s0 : (axis == 1 ? L.pitch : 1);
@@ -1121,7 +1357,7 @@ __device__ __forceinline__ bool seg_general(unsigned long long w0, int S, int i0
   return true;
 }
 
-__global__ void k_mark_keys(const Layout L, int axis, int S, int P,
+__global__ void k_mark_keys(const Layout L, int axis, int S, int P, int lm,
                             const unsigned long long* __restrict__ desc,
                             unsigned* __restrict__ bitmap) {
   const int m = (axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2)) - 2;
@@ -1129,7 +1365,7 @@ __global__ void k_mark_keys(const Layout L, int axis, int S, int P,
   const long long nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * K;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nseg;
        t += (long long)gridDim.x * blockDim.x) {
-    const int seg = (int)((t / K) % P);
+    const int seg = lm ? (int)(t % P) : (int)((t / K) % P);
     unsigned key;
     if (seg_general(desc[2 * t], S, seg * S, m, seg == 0, key))
       if (!((bitmap[key >> 5] >> (key & 31)) & 1u)) atomicOr(bitmap + (key >> 5), 1u << (key & 31));
@@ -1159,7 +1395,7 @@ __global__ void k_key_factors(AxisCoef co, int S, const unsigned* __restrict__ b
   }
 }
 
-__global__ void k_assign_slots(const Layout L, int axis, int S, int P,
+__global__ void k_assign_slots(const Layout L, int axis, int S, int P, int lm,
                                unsigned long long* __restrict__ desc,
                                const unsigned* __restrict__ bitmap, const int* __restrict__ base) {
   const int m = (axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2)) - 2;
@@ -1167,7 +1403,7 @@ __global__ void k_assign_slots(const Layout L, int axis, int S, int P,
   const long long nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * K;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nseg;
        t += (long long)gridDim.x * blockDim.x) {
-    const int seg = (int)((t / K) % P);
+    const int seg = lm ? (int)(t % P) : (int)((t / K) % P);
     const unsigned long long w0 = desc[2 * t];
     unsigned key;
     if (!seg_general(w0, S, seg * S, m, seg == 0, key)) continue;
@@ -1182,7 +1418,7 @@ __global__ void k_assign_slots(const Layout L, int axis, int S, int P,
 // recurrences as the uniform tables, per-row coefficients) and read like a table by the
 // sweeps.  Pass 0 counts, pass 1 assigns slots (atomic; values do not depend on the slot)
 // and writes factors + slot into descriptor word 0.
-__global__ void k_seg_factors(const Layout L, int axis, int S, int P, AxisCoef co, int pass,
+__global__ void k_seg_factors(const Layout L, int axis, int S, int P, int lm, AxisCoef co, int pass,
                               unsigned long long* __restrict__ desc, int* __restrict__ counter,
                               double* __restrict__ gfac) {
   const int m = (axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2)) - 2;
@@ -1190,7 +1426,7 @@ __global__ void k_seg_factors(const Layout L, int axis, int S, int P, AxisCoef c
   const long long nseg = (long long)((axis == 0 ? L.n1 : L.n0) - 2) * P * K;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nseg;
        t += (long long)gridDim.x * blockDim.x) {
-    const int seg = (int)((t / K) % P);
+    const int seg = lm ? (int)(t % P) : (int)((t / K) % P);
     const int i0 = seg * S, first = seg == 0;
     const unsigned long long w0 = desc[2 * t];
     const unsigned long long eb = eps_bits(w0, S);
@@ -1228,6 +1464,28 @@ static int seg_P(int axis, int m) {
   return m <= 128 ? 8 : (m <= 256 ? 16 : 32);
 }
 
+// Row-warp sweeps (k_sweep_rowwarp) for axis 2: lines of G*S - 1 interior rows where they
+// measured faster than the row tiles, and the LOD epilogues; PBG_ROWWARP=0 keeps the row-tile
+// kernel, for comparison.
+static int rowwarp_G(int m) {
+  if (m + 1 == 512) return 32;  // S = 16 (c4: 734 -> 645 us with the LODIE2 flow)
+  if (m + 1 == 128) return 16;  // S = 8  (c2: 25 -> 22 us)
+  // m + 1 = 256 (16 x 16) keeps the row-tile kernel: 103 vs 108 us (LODIE2, c3)
+  return 0;
+}
+static int rowwarp_S(int m) {
+  const int G = rowwarp_G(m);
+  return G ? (m + 1) / G : 0;
+}
+static bool rowwarp_ok(const SweepArgs& a, int axis) {
+  static const bool on = [] {
+    const char* e = getenv("PBG_ROWWARP");
+    return !(e && e[0] == '0');
+  }();
+  return on && axis == 2 && !a.cn && a.pro == PRO_NONE && !a.has_extra && !a.ends &&
+         (a.epi == EPI_STORE || a.epi == EPI_FLOW || a.epi == EPI_SRC) && rowwarp_S(a.m) != 0;
+}
+
 // Column sweeps run register-direct (k_sweep_col) unless PBG_COL=0 selects the staged-tile
 // kernels, for comparison.
 static bool col_enabled() {
@@ -1244,14 +1502,20 @@ static bool col_enabled() {
 static int resident_blocks(const void* fn, int nthreads, size_t smem) {
   static std::mutex mu;
   static std::map<std::tuple<const void*, size_t, int>, int> cache;
+  static std::map<std::pair<const void*, int>, size_t> limit;  // attribute set per kernel
   int dev = 0;
   cudaGetDevice(&dev);
   const auto key = std::make_tuple(fn, smem, dev);
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  if (smem > 48 * 1024)
+  // The limit only ever grows: lowering it for a smaller launch would make a later, cached
+  // larger launch of the same kernel fail.
+  size_t& lim = limit[std::make_pair(fn, dev)];
+  if (smem > 48 * 1024 && smem > lim) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    lim = smem;
+  }
   int nsm = 148, bps = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, nthreads, smem);
@@ -1334,7 +1598,27 @@ static void launch_strided_SP(const SweepArgs& a, int axis, cudaStream_t st) {
     default: return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 768)"); \
   }
 
+template <int S, int G>
+static void launch_rowwarp_SG(const SweepArgs& a, cudaStream_t st) {
+  const int nlines = (a.L.n0 - 2) * (a.L.n1 - 2);
+  const size_t smem = rowwarp_smem(S, G, flow_stage_n(a));
+  auto kern = k_sweep_rowwarp<S, G>;
+  const int per_block = kRWarps * (32 / G);
+  const int grid = std::min((nlines + per_block - 1) / per_block,
+                            resident_blocks((const void*)kern, kRWarps * 32, smem));
+  kern<<<grid, kRWarps * 32, smem, st>>>(a, nlines);
+}
+
 static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
+  if (a.rw) {
+    switch (rowwarp_G(a.m) * 100 + rowwarp_S(a.m)) {
+      case 3216: launch_rowwarp_SG<16, 32>(a, st); break;
+      case 1608: launch_rowwarp_SG<8, 16>(a, st); break;
+      default: return fail(PBG_E_UNSUPPORTED, "row-warp sweep without a segment length");
+    }
+    PBG_LAUNCH_CHECK("k_sweep_rowwarp");
+    return PBG_OK;
+  }
   const int P = seg_P(axis, a.m), S = seg_S(a.m, P);
   if (P == 8) {
 #define PBG_STRIDED8(S) launch_strided_SP<S, 8>(a, axis, st)
@@ -1599,8 +1883,10 @@ static long long desc_segments(const Layout& L, int axis, int P) {
 
 int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
                         cudaStream_t st) {
-  const int P = seg_P(axis, a.m);
-  const int S = seg_S(a.m, P);
+  a.rw = rowwarp_ok(a, axis) ? 1 : 0;
+  const int P = a.rw ? rowwarp_G(a.m) : seg_P(axis, a.m);
+  const int S = a.rw ? rowwarp_S(a.m) : seg_S(a.m, P);
+  const int lm = a.rw;
   if (S < 2) return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 768)");
   std::vector<double> host(kTabDoubles + kSeg * (kSeg + 2), 0.0);
   make_tables(a.co, S, host.data());
@@ -1613,7 +1899,7 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
   const long long nseg = desc_segments(a.L, axis, P);
   // +64 words of slack: tiles past the last interior column read (unused) descriptors
   PBG_CUDA(cudaMallocAsync(&aux.desc, (2 * nseg + 64) * sizeof(unsigned long long), st));
-  k_build_desc<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, codes,
+  k_build_desc<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, codes,
                                          aux.desc);
   PBG_LAUNCH_CHECK("k_build_desc");
   if (S <= kDedupMaxS) {
@@ -1628,7 +1914,7 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
     PBG_CUDA(cudaMallocAsync(&base, (size_t)nw * sizeof(int), st));
     PBG_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
     PBG_CUDA(cudaMemsetAsync(bitmap, 0, (size_t)nw * sizeof(unsigned), st));
-    k_mark_keys<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, aux.desc, bitmap);
+    k_mark_keys<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, aux.desc, bitmap);
     PBG_LAUNCH_CHECK("k_mark_keys");
     k_popc_words<<<(nw + 255) / 256, 256, 0, st>>>(bitmap, nw, cnt);
     PBG_LAUNCH_CHECK("k_popc_words");
@@ -1643,7 +1929,7 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
     if (ndist > 0) {
       k_key_factors<<<(nw + 255) / 256, 256, 0, st>>>(a.co, S, bitmap, base, nw, aux.gfac);
       PBG_LAUNCH_CHECK("k_key_factors");
-      k_assign_slots<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, aux.desc, bitmap, base);
+      k_assign_slots<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, aux.desc, bitmap, base);
       PBG_LAUNCH_CHECK("k_assign_slots");
     }
     PBG_CUDA(cudaFreeAsync(bitmap, st));
@@ -1654,7 +1940,7 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
     int* counter = nullptr;
     PBG_CUDA(cudaMallocAsync(&counter, sizeof(int), st));
     PBG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-    k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, a.co, 0,
+    k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, a.co, 0,
                                             aux.desc, counter, nullptr);
     PBG_LAUNCH_CHECK("k_seg_factors");
     int ngen = 0;
@@ -1663,7 +1949,7 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
     PBG_CUDA(cudaMallocAsync(&aux.gfac, ((size_t)ngen + 1) * 5 * kTabRows * sizeof(double), st));
     if (ngen > 0) {
       PBG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-      k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, a.co, 1,
+      k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, a.co, 1,
                                              aux.desc, counter, aux.gfac);
       PBG_LAUNCH_CHECK("k_seg_factors");
     }

@@ -79,6 +79,8 @@ struct SweepArgs {
   const double* fpoly;
   int foff[2];
   int fpoly_n;
+  // Axis 2 runs the row-warp kernel (line-major descriptors, P = 32), set by prepare_axis.
+  int rw;
   // Small-argument flow of palette 0 (pbg_internal.cuh flow_small), when decay0 < 1.
   int fsmall_on;
   double fsmall[kFSmallN];

@@ -60,3 +60,18 @@ def test_line_longer_than_supported_is_refused():
                       initial=pb.ScalarField.zeros(g), eps_m=1.0, eps_s=1.0)
     with pytest.raises(NotImplementedError):
         pb.march(p, pb.MarchConfig(dt=0.1, T=0.1, variant="LODIE2"))
+
+
+# Row-warp sweeps (axis 2 lines of 32*S - 1 or 16*S - 1 interior rows: one or two lines per
+# warp, an odd line count leaves half a warp idle) with each LOD epilogue, against the oracle.
+RW_SHAPES = [(5, 6, 513), (7, 9, 129), (6, 5, 129)]
+
+
+@pytest.mark.parametrize("shape", RW_SHAPES)
+def test_row_warp_lines_vs_oracle(shape):
+    p, op = problems(shape, seed=1)
+    for v in ["LODIE1", "LODIE2", "ADI1", "LODCN2"]:
+        rep = pb.march(p, pb.MarchConfig(dt=0.2, T=0.6, variant=v))
+        orep = O.march(op, v, 0.2, 0.6)
+        assert rep.steps_taken == orep.steps_taken == 3, v
+        assert rel_err(rep.final.data, orep.final) <= 1e-12, (shape, v)
