@@ -255,6 +255,12 @@ PBG_API int pbg_flow_table(double decay, double* out);
 #define PBG_FLOW_SMALL_DOUBLES 16
 PBG_API int pbg_flow_small(double decay, double* out);
 
+/* Host only: the tier used first, for |w| <= 0.5: flow = w * sum g_q t^q,
+ * t = fma(w, w, -0.125), q = 0..7 (PBG_FLOW_TINY_DOUBLES coefficients).  Exported for
+ * testing. */
+#define PBG_FLOW_TINY_DOUBLES 8
+PBG_API int pbg_flow_tiny(double decay, double* out);
+
 /* Direct vacuum Poisson solve (vacuum_potential_fast, energy.py:59-85): -eps_m * d2(out) =
  * rho on the interior with out = bnd on the faces (bnd: pitched field whose faces hold the
  * Dirichlet data).  Boundary lifting, type-I DST along each axis (cuFFT D2Z of the odd

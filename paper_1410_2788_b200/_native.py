@@ -90,6 +90,7 @@ _SIGS = {
                        ctypes.c_int),
     "pbg_flow_table": ([c_double, c_void_p], ctypes.c_int),
     "pbg_flow_small": ([c_double, c_void_p], ctypes.c_int),
+    "pbg_flow_tiny": ([c_double, c_void_p], ctypes.c_int),
     "pbg_energy_atoms": ([_P(PbgGrid), c_void_p, c_int32, c_void_p, c_void_p, c_double,
                           c_double, c_void_p, c_void_p, c_double, c_double, c_double,
                           _P(c_double), c_void_p], ctypes.c_int),

@@ -80,22 +80,22 @@ __device__ __forceinline__ double flow_sm(const SweepArgs& a, const double* FP, 
     return sinh_flow_poly(w, a.decay1, a.sat1, pm, FP + kFlowHdr + a.foff[1]);
   }
   if (a.fsmall_on && fabs(w) <= kFSmallX) {  // solvent far field: no table loads
-    const double out = flow_small(w, a.fsmall);
+    const double out = fabs(w) <= kFTinyX ? flow_tiny(w, a.ftiny) : flow_small(w, a.fsmall);
     return pm != 1.0 ? pm * out : out;
   }
   return sinh_flow_poly(w, a.decay0, a.sat0, pm, FP + kFlowHdr + a.foff[0]);
 }
 
-// pm * flow of four independent nodes in place: the small-argument polynomial for all of
-// them first (branch-free, so the four Horner chains interleave), then flow_sm for the rare
-// others (solute palette, |w| > kFSmallX, no small form).  Same results as flow_sm per node.
+// pm * flow of four independent nodes in place: the tiny-argument polynomial for all of
+// them first (branch-free, so the four Horner chains interleave), then flow_sm for the rarer
+// others (solute palette, |w| > kFTinyX, no small form).  Same results as flow_sm per node.
 __device__ __forceinline__ void flow_group(const SweepArgs& a, const double* FP, double& w0,
                                            double& w1, double& w2, double& w3, uint32_t s0,
                                            uint32_t s1, uint32_t s2, uint32_t s3, double pm) {
-  const double x0 = flow_small(w0, a.fsmall), x1 = flow_small(w1, a.fsmall);
-  const double x2 = flow_small(w2, a.fsmall), x3 = flow_small(w3, a.fsmall);
+  const double x0 = flow_tiny(w0, a.ftiny), x1 = flow_tiny(w1, a.ftiny);
+  const double x2 = flow_tiny(w2, a.ftiny), x3 = flow_tiny(w3, a.ftiny);
   auto fin = [&](double& w, double x, uint32_t s) {
-    if (s || !a.fsmall_on || !(fabs(w) <= kFSmallX)) w = flow_sm(a, FP, w, s, pm);
+    if (s || !a.fsmall_on || !(fabs(w) <= kFTinyX)) w = flow_sm(a, FP, w, s, pm);
     else w = pm != 1.0 ? pm * x : x;
   };
   fin(w0, x0, s0);
@@ -1792,9 +1792,10 @@ static void build_flow_poly(double d, double* out) {
 
 // Small-argument flow of decay d (pbg_internal.cuh, flow_small): G(y) = F(sqrt y) / sqrt y on
 // y in [0, kFSmallX^2] (G(0) = d), in powers of t = y - kFSmallX^2 / 2.
-static void build_flow_small(double d, double* out) {
-  const long double Y = (long double)kFSmallX * kFSmallX;
-  cheb_powers<kFSmallN>(
+template <int n>
+static void build_flow_even(double d, double X, double* out) {
+  const long double Y = (long double)X * X;
+  cheb_powers<n>(
       [&](long double y) {
         const long double x = std::sqrt(y);
         return 2.0L * std::atanh((long double)d * std::tanh(0.5L * x)) / x;
@@ -1802,18 +1803,24 @@ static void build_flow_small(double d, double* out) {
       0.5L * Y, 0.5L * Y, out);
 }
 
-// Host cache of the small-argument coefficients per decay (set_decays runs per launch).
-static void flow_small_coefs(double d, double* out) {
+static void build_flow_small(double d, double* out) { build_flow_even<kFSmallN>(d, kFSmallX, out); }
+static void build_flow_tiny(double d, double* out) { build_flow_even<kFTinyN>(d, kFTinyX, out); }
+
+// Host cache of the small- and tiny-argument coefficients per decay (set_decays runs per
+// launch).
+static void flow_small_coefs(double d, double* small, double* tiny) {
   static std::mutex mu;
   static std::map<double, std::vector<double>> cache;
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(d);
   if (it == cache.end()) {
-    std::vector<double> g(kFSmallN);
+    std::vector<double> g(kFSmallN + kFTinyN);
     build_flow_small(d, g.data());
+    build_flow_tiny(d, g.data() + kFSmallN);
     it = cache.emplace(d, std::move(g)).first;
   }
-  std::copy(it->second.begin(), it->second.end(), out);
+  std::copy(it->second.begin(), it->second.begin() + kFSmallN, small);
+  std::copy(it->second.begin() + kFSmallN, it->second.end(), tiny);
 }
 
 // Device copy of the interval tables of a decay pair, [palette slot][kFPolyDoubles], cached
@@ -1858,7 +1865,7 @@ void set_decays(SweepArgs& a, double d0, double d1) {
   a.foff[0] = 0;  // palette 0 has slot 0 when it needs one
   a.foff[1] = (d0 < 1.0 && d1 < 1.0 && d1 != d0) ? kFPolyDoubles : 0;
   a.fsmall_on = d0 >= 0.0 && d0 < 1.0;
-  if (a.fsmall_on) flow_small_coefs(d0, a.fsmall);
+  if (a.fsmall_on) flow_small_coefs(d0, a.fsmall, a.ftiny);
 }
 
 SweepArgs base_args(const pbg_grid* g, const pbg_palette* pal, int axis, double factor) {
@@ -2117,6 +2124,14 @@ extern "C" PBG_API int pbg_flow_small(double decay, double* out) {
   if (!out) return fail(PBG_E_INVALID, "null pointer");
   if (!(decay >= 0.0 && decay < 1.0)) return fail(PBG_E_INVALID, "decay must be in [0, 1)");
   build_flow_small(decay, out);
+  return PBG_OK;
+}
+
+extern "C" PBG_API int pbg_flow_tiny(double decay, double* out) {
+  static_assert(kFTinyN == PBG_FLOW_TINY_DOUBLES, "tiny-argument flow size");
+  if (!out) return fail(PBG_E_INVALID, "null pointer");
+  if (!(decay >= 0.0 && decay < 1.0)) return fail(PBG_E_INVALID, "decay must be in [0, 1)");
+  build_flow_tiny(decay, out);
   return PBG_OK;
 }
 

@@ -84,6 +84,7 @@ struct SweepArgs {
   // Small-argument flow of palette 0 (pbg_internal.cuh flow_small), when decay0 < 1.
   int fsmall_on;
   double fsmall[kFSmallN];
+  double ftiny[kFTinyN];
   // Strided axes: offset (from the line base) of the high boundary value in bnd; normally
   // plane m+1 of a field, one plane for the two-plane ghost buffers of the slab march.
   long long hi_off;

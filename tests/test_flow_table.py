@@ -121,3 +121,44 @@ def test_flow_small_rejects_bad_decay():
     out = np.zeros(16)
     for d in (1.0, -0.1, float("nan")):
         assert lib.pbg_flow_small(d, out.ctypes.data_as(ctypes.c_void_p)) != 0
+
+
+def tiny(decay):
+    lib = nat.load_library()
+    out = np.zeros(8, dtype=np.float64)
+    nat.check(lib.pbg_flow_tiny(decay, out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def tiny_eval(w, g):
+    """Device evaluation (pbg_internal.cuh flow_tiny) in numpy, |w| <= 0.5."""
+    t = w * w - 0.125
+    p = np.full_like(w, g[-1])
+    for q in g[-2::-1]:
+        p = p * t + q
+    return w * p
+
+
+@pytest.mark.parametrize("decay", [0.529131809679411, 0.6541980527948197, 0.880466373414563,
+                                   0.9186325916063356, 0.99, 0.1, 1e-3, 0.0])
+def test_flow_tiny_matches_reference_flow(decay):
+    g = tiny(decay)
+    rng = np.random.default_rng(4)
+    w = np.concatenate([rng.uniform(-0.5, 0.5, 20000), rng.uniform(-1e-3, 1e-3, 2000),
+                        [0.0, -0.0, 0.5, -0.5, 1e-300, np.nextafter(0.5, 0)]])
+    got = tiny_eval(w, g)
+    assert np.max(np.abs(got - O.sinh_flow(w, decay))) <= 4e-15
+    mp.mp.dps = 30
+    sub = w[::41]
+    exact = np.array([float(2 * mp.atanh(decay * mp.tanh(mp.mpf(v) / 2))) for v in sub])
+    err = np.abs(tiny_eval(sub, g) - exact)
+    assert np.max(err / np.maximum(np.abs(exact), 1e-300)) <= 1e-15
+    if decay > 0:  # agrees with the small-argument form where both apply
+        assert np.max(np.abs(got - small_eval(w, small(decay)))) <= 1e-16
+
+
+def test_flow_tiny_rejects_bad_decay():
+    lib = nat.load_library()
+    out = np.zeros(8)
+    for d in (1.0, -0.1, float("nan")):
+        assert lib.pbg_flow_tiny(d, out.ctypes.data_as(ctypes.c_void_p)) != 0
