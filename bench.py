@@ -377,9 +377,12 @@ def main():
                              "field), no flush", "assembly_s": round(t_asm, 3)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(c.name, dom),
-                         "kernel": ["k_sweep_strided axis 0 (column tiles, + source)",
-                                    "k_sweep_strided axis 1 (column tiles)",
-                                    "k_sweep_strided axis 2 (row tiles, + flow)"][dom],
+                         "kernel": ["k_sweep_col axis 0 (register-direct column tiles, "
+                                    "+ source)",
+                                    "k_sweep_col axis 1 (register-direct column tiles)",
+                                    ("k_sweep_rowwarp axis 2 (one warp per line, + flow)"
+                                     if c.n in (513, 129) else
+                                     "k_sweep_strided axis 2 (row tiles, + flow)")][dom],
                          "kernel_ms": per_ms, "peak_kind": peak_kind,
                          "step_GBps_48B": step_gbs, "step_frac": step_gbs / peak},
             "cpu_baseline": cpu,
