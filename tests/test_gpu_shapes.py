@@ -17,7 +17,7 @@ SHAPES = [(3, 3, 3), (4, 5, 6), (18, 19, 20), (131, 10, 9), (9, 260, 11), (7, 8,
 VARIANTS = ["LODIE1", "LODCN2", "AOSCN1", "MAOSIE", "ADI2"]
 
 
-def problems(shape, seed=0):
+def problems(shape, seed=0, faces=1.0, source=5.0):
     h = 0.25
     lo = (-0.35 * (shape[0] - 1) * h, -0.6 * (shape[1] - 1) * h, -0.45 * (shape[2] - 1) * h)
     hi = tuple(lo[a] + (shape[a] - 1) * h for a in range(3))
@@ -25,10 +25,10 @@ def problems(shape, seed=0):
     assert g.shape == shape
     R = 0.3 * min(hi[a] - lo[a] for a in range(3)) + 0.3
     rng = np.random.default_rng(seed)
-    bvals = rng.standard_normal(shape)
+    bvals = faces * rng.standard_normal(shape)
     rho = np.zeros(shape)
     idx = tuple(rng.integers(1, max(2, s - 1), size=7) for s in shape)
-    rho[idx] = rng.standard_normal(7) * 5.0
+    rho[idx] = rng.standard_normal(7) * source
     region = pb.build_region_maps(g, pb.AnalyticSphere(R), 2.0, 80.0, 1.3)
     init = np.zeros(shape)
     bspec = pb.BoundarySpec(g, bvals)
@@ -74,4 +74,21 @@ def test_row_warp_lines_vs_oracle(shape):
         rep = pb.march(p, pb.MarchConfig(dt=0.2, T=0.6, variant=v))
         orep = O.march(op, v, 0.2, 0.6)
         assert rep.steps_taken == orep.steps_taken == 3, v
+        assert rel_err(rep.final.data, orep.final) <= 1e-12, (shape, v)
+
+
+@pytest.mark.parametrize("shape", [(5, 6, 513), (7, 9, 129)])
+def test_row_warp_divergence_vs_oracle(shape):
+    # zero faces and a strong source: max|u| grows step by step, so a threshold between the
+    # step-2 and step-6 maxima trips inside the march (the row-warp sweep raises the flag);
+    # the march must stop at the oracle's step and return that step's field
+    p, op = problems(shape, seed=2, faces=0.0, source=500.0)
+    for v in ["LODIE2", "LODIE1"]:
+        amax = [np.max(np.abs(O.march(op, v, 0.2, 0.2 * k).final)) for k in (2, 6)]
+        assert amax[1] > amax[0] > 0.0
+        thr = 0.5 * (amax[0] + amax[1])
+        orep = O.march(op, v, 0.2, 2.0, threshold=thr)
+        rep = pb.march(p, pb.MarchConfig(dt=0.2, T=2.0, variant=v, divergence_threshold=thr))
+        assert orep.diverged and 2 < orep.steps_taken <= 6, v
+        assert rep.diverged and rep.steps_taken == orep.steps_taken, v
         assert rel_err(rep.final.data, orep.final) <= 1e-12, (shape, v)
