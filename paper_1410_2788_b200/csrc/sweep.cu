@@ -1201,31 +1201,28 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
     }
     __syncwarp();
 
-    // epilogue + coalesced store of rows 1..m of each line: lane = row within a 32-row run
+    // epilogue + coalesced store of rows 1..m: the G lanes of a line take consecutive rows
+    // (G * 8 = 128- or 256-byte runs), each lane S of them; an idle half-warp (odd line
+    // count) joins the shuffles but stores nothing
+    {
+      double* gdst = a.dst + base;
+      if (a.epi == EPI_FLOW) {  // the tiny-argument form for almost every node, solute bits
+                                // from the lane owning the row's segment
 #pragma unroll
-    for (int l = 0; l < NL; ++l) {
-      const int ln = wl * NL + l;
-      if (ln >= nlines) break;  // warp-uniform
-      const long long bl = NL == 1 ? base : L.at((L.n0 - 2) - ln / K, 1 + ln % K, 0);
-      const double* Wl = Wb + warp * RW::WD + l * RW::LW;
-      double* gdst = a.dst + bl;
-      if (a.epi == EPI_FLOW) {  // lanes = consecutive rows: the small-argument form for
-                                // almost every node, solute bits from the owning lane
-#pragma unroll
-        for (int q = 0; q < G * S / 32; q += 4) {
+        for (int q = 0; q < S; q += 4) {
           double x[4];
           uint32_t sv[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int p = 1 + lane + 32 * (q + u);
-            x[u] = Wl[RW::pos(p)];
-            sv[u] = (__shfl_sync(FULL, sbits, l * G + (p - 1) / S) >> ((p - 1) % S)) & 1u;
+            const int p = 1 + seg + G * (q + u);
+            x[u] = W[RW::pos(p)];
+            sv[u] = (__shfl_sync(FULL, sbits, sub * G + (p - 1) / S) >> ((p - 1) % S)) & 1u;
           }
           flow_group(a, FP, x[0], x[1], x[2], x[3], sv[0], sv[1], sv[2], sv[3], 1.0);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int p = 1 + lane + 32 * (q + u);
-            if (p <= m) {
+            const int p = 1 + seg + G * (q + u);
+            if (valid && p <= m) {
               gdst[p] = x[u];
               bad |= is_bad(x[u], a.thr);
             }
@@ -1233,10 +1230,10 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
         }
       } else {
 #pragma unroll
-        for (int q = 0; q < G * S / 32; ++q) {
-          const int p = 1 + lane + 32 * q;
-          if (p <= m) {
-            const double x = Wl[RW::pos(p)];
+        for (int q = 0; q < S; ++q) {
+          const int p = 1 + seg + G * q;
+          if (valid && p <= m) {
+            const double x = W[RW::pos(p)];
             gdst[p] = x;
             if (a.check) bad |= is_bad(x, a.thr);
           }
@@ -1469,8 +1466,8 @@ static int seg_P(int axis, int m) {
 // kernel, for comparison.
 static int rowwarp_G(int m) {
   if (m + 1 == 512) return 32;  // S = 16 (c4: 734 -> 645 us with the LODIE2 flow)
+  if (m + 1 == 256) return 16;  // S = 16 (c3: 100 -> 95 us; two lines per warp)
   if (m + 1 == 128) return 16;  // S = 8  (c2: 25 -> 22 us)
-  // m + 1 = 256 (16 x 16) keeps the row-tile kernel: 103 vs 108 us (LODIE2, c3)
   return 0;
 }
 static int rowwarp_S(int m) {
@@ -1613,6 +1610,7 @@ static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
   if (a.rw) {
     switch (rowwarp_G(a.m) * 100 + rowwarp_S(a.m)) {
       case 3216: launch_rowwarp_SG<16, 32>(a, st); break;
+      case 1616: launch_rowwarp_SG<16, 16>(a, st); break;
       case 1608: launch_rowwarp_SG<8, 16>(a, st); break;
       default: return fail(PBG_E_UNSUPPORTED, "row-warp sweep without a segment length");
     }
