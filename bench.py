@@ -381,7 +381,7 @@ def main():
                                     "+ source)",
                                     "k_sweep_col axis 1 (register-direct column tiles)",
                                     ("k_sweep_rowwarp axis 2 (one warp per line, + flow)"
-                                     if c.n in (513, 129) else
+                                     if c.n in (513, 257, 129) else
                                      "k_sweep_strided axis 2 (row tiles, + flow)")][dom],
                          "kernel_ms": per_ms, "peak_kind": peak_kind,
                          "step_GBps_48B": step_gbs, "step_frac": step_gbs / peak},

@@ -77,8 +77,9 @@ for ax, r in enumerate(rows[2:5]):  # the capture holds K0, K1, K2 of one step, 
               f"{float(g(r, 'smsp__inst_executed.sum')) * 32 / NODES:.1f} | "
               f"{float(g(r, 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active')):.1f} | {sts} |")
 md += ["", "Template arguments: `k_sweep_col<S, P, CN, LB>` (axes 0, 1: register-direct column "
-       "tiles) and `k_sweep_strided<S, P, CN, LB, RT>` (axis 2: staged row tiles) = rows per "
-       "segment, segments per line, Crank-Nicolson, lines per tile, row tiles.  Algorithmic "
+       "tiles), `k_sweep_strided<S, P, CN, LB, RT>` (staged tiles) = rows per segment, "
+       "segments per line, Crank-Nicolson, lines per tile, row tiles; `k_sweep_rowwarp<S, G>` "
+       "(axis 2, one warp per line) = rows per segment, lanes per line.  Algorithmic "
        "bytes per sweep launch: 16 B x 133,432,831 interior nodes = 2.135 GB."]
 open(os.path.join(out, f"ncu_{tag}_summary.md"), "w").write("\n".join(md) + "\n")
 tr = json.load(open(os.path.join(out, "ncu_traffic.json")))
