@@ -57,6 +57,20 @@ def _max_abs(field) -> float:
     return float(np.max(np.abs(data)))
 
 
+_STREAMS = {}
+
+
+def _stream_pool(torch, count: int):
+    """The same `count` CUDA streams on every call (per device): the caching allocator keeps
+    blocks per stream, so fresh streams per batch would miss the blocks a previous batch (or
+    the warm-up) left cached and allocate again inside the batch."""
+    dev = torch.cuda.current_device()
+    pool = _STREAMS.setdefault(dev, [])
+    while len(pool) < count:
+        pool.append(torch.cuda.Stream())
+    return pool[:count]
+
+
 def march_many(jobs, streams: int = 8, march_fn=None):
     """Run `jobs` = [(key, problem, MarchConfig)] concurrently on `streams` CUDA streams.
     Returns {key: MarchReport}.  `march_fn` (problem, config) -> report defaults to the
@@ -65,7 +79,7 @@ def march_many(jobs, streams: int = 8, march_fn=None):
         return {key: march_fn(prob, cfg) for key, prob, cfg in jobs}
     torch = nat.torch_cuda()
     fn = march
-    pool = [torch.cuda.Stream() for _ in range(max(1, streams))]
+    pool = _stream_pool(torch, max(1, streams))
     local = threading.local()
     lock = threading.Lock()
     counter = [0]

@@ -558,17 +558,7 @@ extern "C" PBG_API int pbg_march_host(const pbg_march_desc* t, const uint8_t* co
   if (rc) return rc;
   if (!codes_h || !faces_h || !final_h) return fail(PBG_E_INVALID, "null host buffer");
   cudaStream_t st = (cudaStream_t)stream;
-  static bool pool_set = false;
-  if (!pool_set) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    pool_set = true;
-  }
+  keep_pool_memory();
   Layout L = make_layout(&t->grid);
   const size_t nelem = (size_t)L.n0 * L.n1 * L.pitch + 64;  // pbg_layout's nelem
   const size_t nf = (size_t)face_count(L);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 
 #include "pbg.h"
@@ -21,6 +22,23 @@ struct Layout {
     return (long long)i * s0 + (long long)j * pitch + k + kOff;
   }
 };
+
+// The march's per-axis scratch comes from cudaMallocAsync on the device's default pool,
+// whose release threshold is 0: every stream synchronisation would hand the pool's memory
+// back to the driver and the next march would map it again (measured as host-side cost of
+// concurrent config-5 marches).  Keep it cached, once per device.
+inline void keep_pool_memory() {
+  static std::once_flag flags[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::call_once(flags[dev], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
 
 inline Layout make_layout(const pbg_grid* g) {
   Layout L;

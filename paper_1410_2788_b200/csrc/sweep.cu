@@ -2160,6 +2160,7 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
     return fail(PBG_E_INVALID, "dt, alpha must be positive and nsteps >= 1");
   if (!d->codes || !d->rho || !d->initial || !d->work[0] || !d->work[1])
     return fail(PBG_E_INVALID, "null device buffer");
+  keep_pool_memory();
   if (d->variant == PBG_ADI1 || d->variant == PBG_ADI2 || d->variant == PBG_EULER)
     return march_extra(d, steps_taken, diverged_step, result_slot, device_ms,
                        (cudaStream_t)stream);
