@@ -17,7 +17,7 @@ torch.cuda.synchronize()
 nint = 95 ** 3
 for v in ("LODIE2", "AOSIE1"):
     jobs = [((i, v), p, pb.MarchConfig(dt=c.dt, T=c.dt * steps, variant=v)) for i, (c, p) in enumerate(probs)]
-    for s in (1, 2, 4, 8, 16):
+    for s in (4, 8, 12, 16, 24, 32):
         march_many(jobs[:s], streams=s)
         torch.cuda.synchronize()
         t0 = time.perf_counter()

@@ -11,3 +11,7 @@ python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_sweep -s 9 -c 3 -o gpurun_out/c4_full_$TAG python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_sweep -s 9 -c 3 -o gpurun_out/c3_full_$TAG python bench.py --config c3 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full_c3.log 2>&1
+# the two reports together exceed gpurun's 64 MiB copy-back: keep their raw pages only
+for c in c4 c3; do
+  ncu -i gpurun_out/${c}_full_$TAG.ncu-rep --page raw --csv > gpurun_out/${c}_full_${TAG}_raw.csv 2>/dev/null && rm -f gpurun_out/${c}_full_$TAG.ncu-rep
+done

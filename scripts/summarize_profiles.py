@@ -52,8 +52,11 @@ if lpath != os.path.join(out, f"launches_{tag}.csv"):
 
 # full captures: c4 (always) and c3 (when the c3 capture exists)
 def full_capture(rep, cname, nodes, cmd):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if rep.endswith(".csv"):  # raw page exported on the box
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     g = lambda r, k: r[hdr.index(k)]
@@ -89,6 +92,8 @@ tr = json.load(open(os.path.join(out, "ncu_traffic.json")))
 for cname, nodes, fname, cfg in (("c4-protein10000-513", NODES, "c4", ""),
                                  ("c3-protein2500-257", 16581375, "c3", " --config c3")):
     rep = os.path.join(go, f"{fname}_full_{tag}.ncu-rep")
+    if not os.path.exists(rep):
+        rep = os.path.join(go, f"{fname}_full_{tag}_raw.csv")
     if not os.path.exists(rep):
         continue
     cmd = (f"ncu --set full --clock-control none --import-source on -k regex:k_sweep -s 9 -c 3 "
