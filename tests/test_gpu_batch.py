@@ -45,3 +45,22 @@ def test_run_config5_small_batch_vs_oracle():
         ref = O.march(op, it.variant, c.dt, 5 * c.dt).final
         assert abs(it.max_abs - np.max(np.abs(ref))) <= 1e-9 * np.max(np.abs(ref))
         assert not it.diverged and it.steps_taken == 5
+
+
+def test_stream_pool_persists_and_repeats_bitwise():
+    """march_many reuses one stream pool per device (the allocator's per-stream blocks from a
+    warm-up stay usable), and a repeated batch reproduces the first bit for bit."""
+    from paper_1410_2788_b200 import batch as B
+
+    sizes = batch_sizes()
+    probs = [config5_problem(i, sizes[i]) for i in range(2)]
+    jobs = [((i, v), p, pb.MarchConfig(dt=c.dt, T=c.dt * 4, variant=v))
+            for i, (c, p) in enumerate(probs) for v in ("AOSIE1", "LODIE2")]
+    first = march_many(jobs, streams=3)
+    import torch
+
+    pool = list(B._STREAMS[torch.cuda.current_device()][:3])
+    second = march_many(jobs, streams=3)
+    assert B._STREAMS[torch.cuda.current_device()][:3] == pool
+    for key in first:
+        assert np.array_equal(first[key].final.data, second[key].final.data)
