@@ -1468,6 +1468,7 @@ static int rowwarp_G(int m) {
   if (m + 1 == 512) return 32;  // S = 16 (c4: 734 -> 645 us with the LODIE2 flow)
   if (m + 1 == 256) return 16;  // S = 16 (c3: 100 -> 95 us; two lines per warp)
   if (m + 1 == 128) return 16;  // S = 8  (c2: 25 -> 22 us)
+  if (m + 1 == 96) return 8;    // S = 12, four lines per warp (c5 97^3 lines)
   return 0;
 }
 static int rowwarp_S(int m) {
@@ -1612,6 +1613,7 @@ static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
       case 3216: launch_rowwarp_SG<16, 32>(a, st); break;
       case 1616: launch_rowwarp_SG<16, 16>(a, st); break;
       case 1608: launch_rowwarp_SG<8, 16>(a, st); break;
+      case 812: launch_rowwarp_SG<12, 8>(a, st); break;
       default: return fail(PBG_E_UNSUPPORTED, "row-warp sweep without a segment length");
     }
     PBG_LAUNCH_CHECK("k_sweep_rowwarp");

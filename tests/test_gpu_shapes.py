@@ -62,9 +62,10 @@ def test_line_longer_than_supported_is_refused():
         pb.march(p, pb.MarchConfig(dt=0.1, T=0.1, variant="LODIE2"))
 
 
-# Row-warp sweeps (axis 2 lines of 32*S - 1 or 16*S - 1 interior rows: one or two lines per
-# warp, an odd line count leaves half a warp idle) with each LOD epilogue, against the oracle.
-RW_SHAPES = [(5, 6, 513), (7, 9, 257), (6, 5, 129), (4, 5, 257)]
+# Row-warp sweeps (axis 2 lines of 32*S - 1, 16*S - 1 or 8*S - 1 interior rows: one, two or
+# four lines per warp, a line count off the multiple leaves part of a warp idle) with each
+# LOD epilogue, against the oracle.
+RW_SHAPES = [(5, 6, 513), (7, 9, 257), (6, 5, 129), (4, 5, 257), (5, 6, 97), (7, 9, 97)]
 
 
 @pytest.mark.parametrize("shape", RW_SHAPES)
@@ -77,7 +78,7 @@ def test_row_warp_lines_vs_oracle(shape):
         assert rel_err(rep.final.data, orep.final) <= 1e-12, (shape, v)
 
 
-@pytest.mark.parametrize("shape", [(5, 6, 513), (7, 9, 257), (7, 9, 129)])
+@pytest.mark.parametrize("shape", [(5, 6, 513), (7, 9, 257), (7, 9, 129), (7, 9, 97)])
 def test_row_warp_divergence_vs_oracle(shape):
     # zero faces and a strong source: max|u| grows step by step, so a threshold between the
     # step-2 and step-6 maxima trips inside the march (the row-warp sweep raises the flag);
