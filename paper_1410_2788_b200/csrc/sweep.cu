@@ -1228,6 +1228,18 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
             }
           }
         }
+      } else if (a.epi == EPI_AOS2) {  // AOS: 0.25 * (accumulated branches + this branch),
+                                       // read and written in place, same rounding as tiles
+        const double* gy = a.acc + base;
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+          const int p = 1 + seg + G * q;
+          if (valid && p <= m) {
+            const double x = __dmul_rn(0.25, __dadd_rn(gy[p], W[RW::pos(p)]));
+            gdst[p] = x;
+            if (a.check) bad |= is_bad(x, a.thr);
+          }
+        }
       } else {
 #pragma unroll
         for (int q = 0; q < S; ++q) {
@@ -1481,7 +1493,8 @@ static bool rowwarp_ok(const SweepArgs& a, int axis) {
     return !(e && e[0] == '0');
   }();
   return on && axis == 2 && !a.cn && a.pro == PRO_NONE && !a.has_extra && !a.ends &&
-         (a.epi == EPI_STORE || a.epi == EPI_FLOW || a.epi == EPI_SRC) && rowwarp_S(a.m) != 0;
+         (a.epi == EPI_STORE || a.epi == EPI_FLOW || a.epi == EPI_SRC || a.epi == EPI_AOS2) &&
+         rowwarp_S(a.m) != 0;
 }
 
 // Column sweeps run register-direct (k_sweep_col) unless PBG_COL=0 selects the staged-tile

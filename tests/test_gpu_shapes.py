@@ -71,7 +71,7 @@ RW_SHAPES = [(5, 6, 513), (7, 9, 257), (6, 5, 129), (4, 5, 257), (5, 6, 97), (7,
 @pytest.mark.parametrize("shape", RW_SHAPES)
 def test_row_warp_lines_vs_oracle(shape):
     p, op = problems(shape, seed=1)
-    for v in ["LODIE1", "LODIE2", "ADI1", "LODCN2"]:
+    for v in ["LODIE1", "LODIE2", "ADI1", "LODCN2", "AOSIE1"]:
         rep = pb.march(p, pb.MarchConfig(dt=0.2, T=0.6, variant=v))
         orep = O.march(op, v, 0.2, 0.6)
         assert rep.steps_taken == orep.steps_taken == 3, v
