@@ -380,9 +380,11 @@ def main():
                          "kernel": ["k_sweep_col axis 0 (register-direct column tiles, "
                                     "+ source)",
                                     "k_sweep_col axis 1 (register-direct column tiles)",
-                                    ("k_sweep_rowwarp axis 2 (one warp per line, + flow)"
-                                     if c.n in (513, 257, 129) else
-                                     "k_sweep_strided axis 2 (row tiles, + flow)")][dom],
+                                    ({513: "k_sweep_rowwarp axis 2 (one line per warp, + flow)",
+                                      257: "k_sweep_rowwarp axis 2 (two lines per warp, + flow)",
+                                      129: "k_sweep_rowwarp axis 2 (two lines per warp, + flow)",
+                                      97: "k_sweep_rowwarp axis 2 (four lines per warp, + flow)"}
+                                     .get(c.n, "k_sweep_strided axis 2 (row tiles, + flow)"))][dom],
                          "kernel_ms": per_ms, "peak_kind": peak_kind,
                          "step_GBps_48B": step_gbs, "step_frac": step_gbs / peak},
             "cpu_baseline": cpu,
