@@ -291,10 +291,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":  # host only: no torch, no package, no libpbg.so
+        return reference_arm(args, world, rank)
     import torch
 
-    if args.impl == "reference":
-        return reference_arm(args, world, rank)
     torch.cuda.set_device(local)
     dist = None
     mode = args.mode or ("slab" if world > 1 else "single")
@@ -570,80 +570,131 @@ def slab_main(args, c, p, t_asm, world, rank, local, dist):
     dist.destroy_process_group()
 
 
-_REF = {}  # reference-arm state, inherited by the forked workers (not pickled)
+def _configs():
+    """paper_1410_2788_b200/configs.py loaded by file path: the reference arm must not import
+    the package (which loads libpbg.so) -- only the seeded input generator."""
+    import importlib.util
+
+    path = os.path.join(ROOT, "paper_1410_2788_b200", "configs.py")
+    spec = importlib.util.spec_from_file_location("_pbg_configs", path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules.setdefault("_pbg_configs", mod)
+    spec.loader.exec_module(mod)
+    return mod
 
 
-def _reference_worker(i0):
-    """One host core of the reference arm: build its plane sample's oracle stepper (untimed),
-    wait for the others, then time `steps` steps.  Runs in a forked child (numpy only)."""
-    p, dp, planes, nplanes, variant, dt, steps, barrier = (
-        _REF[k] for k in ("p", "dp", "planes", "nplanes", "variant", "dt", "steps", "barrier"))
+def host_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+_FACE = {}  # face points of the current BoundarySpec face, inherited by forked workers
+
+
+def _face_chunk(span):
     from oracle import pbs_oracle as O
 
-    op = oracle_slab(p, dp, nplanes, planes=planes, i0=i0)
-    st = O.OStepper(op, variant, dt)
-    u = op.initial.copy()
-    barrier.wait(timeout=900)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        u = st.step(u)
-    return time.perf_counter() - t0
+    lo, hi = span
+    return O.coulomb_values(_FACE["pts"][lo:hi], _FACE["atoms"], _FACE["eps_s"], _FACE["kbar"])
+
+
+def oracle_problem_cpu(c, cfg_mod, workers):
+    """The benched problem built on the host by the oracle restatement of protein_problem's
+    assembly on the cubic box (culled classification, np.add.at deposit, screened-Coulomb
+    faces).  Face values are computed per point exactly as coulomb_screened_values does
+    (problem.py:106-117: a per-point sum over the atoms in order), split over forked workers
+    by point ranges, so the values are identical to a serial evaluation."""
+    import multiprocessing as mp
+
+    from oracle import pbs_oracle as O
+
+    atoms = cfg_mod.synthetic_atoms(c.n_atoms, c.ball_radius, c.seed)
+    kbar = cfg_mod.kappa_bar(c.ionic_strength)
+    lo, hi = cfg_mod.cubic_box(atoms, c.n, c.h)
+    g = O.grid_from_bounds(lo, hi, c.h)
+    region = O.union_region(g, atoms, c.eps_m, c.eps_s, kbar ** 2)
+    qfrac, rho = O.deposit(g, atoms)
+    _FACE.update(atoms=atoms, eps_s=c.eps_s, kbar=kbar)
+    ctx = mp.get_context("fork")
+
+    def fn(pts):
+        _FACE["pts"] = pts
+        n = pts.shape[0]
+        spans = [(w * n // workers, (w + 1) * n // workers) for w in range(workers)]
+        with ctx.Pool(workers) as pool:
+            parts = pool.map(_face_chunk, spans, chunksize=1)
+        return np.concatenate(parts)
+
+    bvals = O.faces_from_function(g, fn)
+    init = np.zeros(g.shape)
+    O.apply_faces(init, bvals)
+    return O.OProblem(g, region, rho, qfrac, bvals, 1.0, init, c.eps_m, c.eps_s, kbar,
+                      list(atoms))
 
 
 def reference_arm(args, world, rank):
-    """CPU reference arm: the numpy oracle port of pbsplit's Stepper (the reference itself
-    is Python and cannot travel to the box) on every host core the process may use: one
-    forked worker per core, each stepping its own 65-plane sample of the same workload
-    concurrently; throughput = all workers' interior updates / the slowest worker's time."""
+    """CPU reference arm: the reference's own CPU algorithm for the benched workload, i.e.
+    the numpy oracle port of pbsplit's Stepper/march (the reference is Python and cannot
+    travel to the box; the port is pinned to it and times at 0.8-0.93x of it),
+    on the SAME full grid and the same number of steps as our arm: inputs built on the host
+    (no torch, no libpbg.so), W untimed warm-up steps, then K steps timed like
+    MarchReport.wall_time (schemes.py:413-422: the step loop with its per-step max|u|
+    divergence test, setup excluded).  The reference is single-threaded numpy (one core);
+    only the untimed setup uses the other cores.  Rank 0 only (N > 1: the others exit)."""
     if rank != 0:
         return
-    import multiprocessing as mp
+    from oracle import pbs_oracle as O
 
-    import torch
-
-    torch.cuda.set_device(0)
-    c, p, _ = build_problem(args.config)  # device assembly only to produce identical inputs
-    from paper_1410_2788_b200.schemes import device_problem
-
-    dp = device_problem(p)
-    nplanes = 65
-    n0 = p.grid.shape[0]
-    cores = len(os.sched_getaffinity(0))
-    try:  # ~40 sample-sized fp64 arrays per worker (stepper factors and temporaries)
-        import psutil
-
-        per = 40 * 8 * nplanes * p.grid.shape[1] * p.grid.shape[2]
-        cores = max(1, min(cores, int(0.6 * psutil.virtual_memory().available // per)))
-    except ImportError:
-        pass
-    nw = cores
-    offs = [w * (n0 - nplanes) // max(1, nw - 1) for w in range(nw)] if nw > 1 else [0]
-    planes = host_planes(dp, p.grid, 0, n0)  # shared with the forked workers
-    steps = max(1, min(args.steps, 3))
-    ctx = mp.get_context("fork")
-    _REF.update(p=p, dp=dp, planes=planes, nplanes=nplanes, variant=c.variant, dt=c.dt, steps=steps,
-                barrier=ctx.Barrier(nw))
-    with ctx.Pool(nw) as pool:
-        walls = pool.map(_reference_worker, offs, chunksize=1)
-    nint = (nplanes - 2) * (c.n - 2) ** 2
-    wall = max(walls)
-    v = nw * nint * steps / wall
+    cfg_mod = _configs()
+    if args.config not in cfg_mod.CONFIGS:
+        print(json.dumps({"impl": "reference",
+                          "unavailable": f"reference arm covers {sorted(cfg_mod.CONFIGS)}"}))
+        return
+    c = cfg_mod.CONFIGS[args.config]
+    workers = max(1, len(os.sched_getaffinity(0)))
+    t0 = time.perf_counter()
+    op = oracle_problem_cpu(c, cfg_mod, workers)
+    st = O.OStepper(op, c.variant, c.dt)
+    t_setup = time.perf_counter() - t0
+    u = op.initial.copy()
+    thr = 1e12
+    for _ in range(args.warmup):
+        u = st.step(u)
+        np.max(np.abs(u))
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        u = st.step(u)
+        amax = np.max(np.abs(u))
+        if not np.isfinite(amax) or amax > thr:
+            raise RuntimeError(f"reference march diverged at step {k + 1}")
+    wall = time.perf_counter() - t0
+    nint = (c.n - 2) ** 3
+    v = nint * args.steps / wall
+    sample = (f"full {c.name} grid ({c.n}^3, {nint} interior nodes), {args.steps} timed "
+              f"{c.variant} steps after {args.warmup} warm-up steps, numpy oracle port of "
+              f"pbsplit Stepper/march, single-threaded; host {host_model()}, nproc {workers}; "
+              f"setup {t_setup:.1f} s untimed")
     line = {"metric": "LOD grid-point updates/s (fp64)", "value": v,
-            "unit": "grid-point updates/s", "n_gpus": world, "steps": steps, "warmup": 0,
-            "ms_per_step": wall / steps * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
-            "config": {"workload": c.name, "grid": [c.n] * 3, "variant": c.variant,
-                       "dt": c.dt, "sample_planes": nplanes},
+            "unit": "grid-point updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, configs.py)",
+            "config": {"workload": c.name, "grid": [c.n] * 3, "atoms": c.n_atoms, "h": c.h,
+                       "variant": c.variant, "dt": c.dt, "interior_nodes": nint,
+                       "parallelism": "one host core"},
             "impl": "reference",
-            "cpu_baseline": {"value": v, "unit": "grid-point updates/s", "cores": nw,
-                             "kind": "port",
-                             "sample": f"{nw} concurrent workers (one per host core), each "
-                                       f"{steps} {c.variant} step(s) of {c.name} restricted "
-                                       f"to its own {nplanes}-plane slab ({nint} interior "
-                                       f"nodes); per-worker s: "
-                                       f"{[round(w, 2) for w in walls]}"},
+            "cpu_baseline": {"value": v, "unit": "grid-point updates/s", "cores": 1,
+                             "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "grid-point updates/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "host": {"model": host_model(), "nproc": workers},
+            "final_max_abs": float(np.max(np.abs(u)))}
     print(json.dumps(line), flush=True)
 
 

@@ -44,6 +44,8 @@
 #include <vector>
 
 #include <cub/cub.cuh>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "sweep.cuh"
 
@@ -933,7 +935,7 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
   constexpr int NT = LB * kSegS;
   const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
   const int tid = threadIdx.y * LB + threadIdx.x;
-  const TileGeo g = tile_geo<LB, false>(a, axis, blockIdx.x, blockIdx.y, gridDim.y);
+  const TileGeo g = tile_geo<LB, false>(a, axis, blockIdx.x, blockIdx.y + a.o0, gridDim.y);
   const int m = a.m, i0 = threadIdx.y * S;
   const bool act = threadIdx.x < g.ncols;
   const int st = g.stride;
@@ -1056,6 +1058,145 @@ __host__ __device__ constexpr size_t rowwarp_smem(int S, int G, int fpoly_n) {
                            fpoly_n);
 }
 
+// Line solve of the row-warp sweeps once lane `seg` holds rows seg*S+1 .. seg*S+S of its line
+// in r[]: Dirichlet folds, segment elimination, the reduced system over the G separators of
+// the line inside the warp (clean lines: the static inverse, one dot product; others: PCR with
+// shuffles), reconstruction (separator = t) and the LODIE1 sparse source.  sR: G + 2 doubles
+// of per-line scratch.
+template <int S, int G>
+__device__ __forceinline__ void rw_solve(const SweepArgs& a, double (&r)[S],
+                                         unsigned long long amask, uint32_t cmask, double bfold,
+                                         bool valid, int seg, const double* T, const double* Mi,
+                                         double* sR, long long base) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int m = a.m, i0 = seg * S;
+  if (seg == 0 && valid)
+    r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], bfold));
+  if (seg == (m - 1) / S && valid)
+    fold_high<S>(a, r, amask, seg == 0 ? a.bnd[base + a.hi_off] : bfold);
+  SegOut o;
+  const double* Tv = seg_eliminate<S>(a, r, amask, i0, seg == 0, T, o);
+
+  // reduced system over the G separators of each line
+  double t, tm;
+  const bool nx = seg + 1 < G;
+  const double yFn = __shfl_down_sync(FULL, o.yF, 1, G);
+  const bool clean = __all_sync(FULL, eps_bits(amask, S) == 0ull) && a.static_ok;
+  if (clean) {
+    sR[seg] = o.rs - o.as * o.yL - o.cs * (nx ? yFn : 0.0);
+    __syncwarp();
+    const double2* Rr = reinterpret_cast<const double2*>(sR);
+    const double2* Mr = reinterpret_cast<const double2*>(Mi + seg * (G + 2));
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int q = 0; q < G / 2; q += 2) {
+      const double2 r0 = Rr[q], m0 = Mr[q], r1 = Rr[q + 1], m1 = Mr[q + 1];
+      s0 = fma(m0.x, r0.x, s0);
+      s1 = fma(m0.y, r0.y, s1);
+      s2 = fma(m1.x, r1.x, s2);
+      s3 = fma(m1.y, r1.y, s3);
+    }
+    t = (s0 + s1) + (s2 + s3);
+  } else {  // parallel cyclic reduction with shuffles
+    const double aFn = __shfl_down_sync(FULL, o.aF, 1, G);
+    const double bFn = __shfl_down_sync(FULL, o.bF, 1, G);
+    double A = o.as * o.aL, B = o.bs + o.as * o.bL + o.cs * (nx ? aFn : 0.0),
+           Cc = o.cs * (nx ? bFn : 0.0), R = o.rs - o.as * o.yL - o.cs * (nx ? yFn : 0.0);
+#pragma unroll
+    for (int d = 1; d < G; d <<= 1) {
+      const double iB = fast_rcp(B);
+      const double Am = __shfl_up_sync(FULL, A, d, G), iBm = __shfl_up_sync(FULL, iB, d, G),
+                   Cm = __shfl_up_sync(FULL, Cc, d, G), Rm = __shfl_up_sync(FULL, R, d, G);
+      const double Ap = __shfl_down_sync(FULL, A, d, G), iBp = __shfl_down_sync(FULL, iB, d, G),
+                   Cp = __shfl_down_sync(FULL, Cc, d, G), Rp = __shfl_down_sync(FULL, R, d, G);
+      const bool lo = seg >= d, hi = seg + d < G;
+      const double k1 = lo ? -A * iBm : 0.0, k2 = hi ? -Cc * iBp : 0.0;
+      A = lo ? k1 * Am : 0.0;
+      Cc = hi ? k2 * Cp : 0.0;
+      B = B + (lo ? k1 * Cm : 0.0) + (hi ? k2 * Ap : 0.0);
+      R = R + (lo ? k1 * Rm : 0.0) + (hi ? k2 * Rp : 0.0);
+    }
+    t = R * fast_rcp(B);
+  }
+  tm = __shfl_up_sync(FULL, t, 1, G);
+  if (seg == 0) tm = 0.0;
+
+  // reconstruct the own rows (separator = t) and put them back into the line buffer
+  if (Tv == nullptr) {
+#pragma unroll
+    for (int q = 0; q < S - 1; ++q)
+      r[q] = fma(a.tmid[TQ_BE * kTabRows + q], t, fma(a.tmid[TQ_AL * kTabRows + q], tm, r[q]));
+  } else {
+#pragma unroll
+    for (int q = 0; q < S - 1; ++q)
+      r[q] = fma(Tv[TQ_BE * kTabRows + q], t, fma(Tv[TQ_AL * kTabRows + q], tm, r[q]));
+  }
+  r[S - 1] = t;
+  if (a.epi == EPI_SRC && cmask) fix_regs<S>(r, cmask, a.epi_coef, a.rho + base + i0 + 1, 1);
+}
+
+// Epilogue + coalesced store of rows 1..m of the warp's lines from the line buffer (at(p) =
+// row p): the G lanes of a line take consecutive rows (G * 8 = 128- or 256-byte runs), each
+// lane S of them; an idle sub-warp (odd line count) joins the shuffles but stores nothing.
+template <int S, int G, typename At>
+__device__ __forceinline__ void rw_store(const SweepArgs& a, At at, bool valid, int seg, int sub,
+                                         uint32_t sbits, const double* FP, long long base,
+                                         bool& bad) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int m = a.m;
+  // epilogue + coalesced store of rows 1..m: the G lanes of a line take consecutive rows
+  // (G * 8 = 128- or 256-byte runs), each lane S of them; an idle half-warp (odd line
+  // count) joins the shuffles but stores nothing
+  {
+    double* gdst = a.dst + base;
+    if (a.epi == EPI_FLOW) {  // the tiny-argument form for almost every node, solute bits
+                              // from the lane owning the row's segment
+#pragma unroll
+      for (int q = 0; q < S; q += 4) {
+        double x[4];
+        uint32_t sv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int p = 1 + seg + G * (q + u);
+          x[u] = at(p);
+          sv[u] = (__shfl_sync(FULL, sbits, sub * G + (p - 1) / S) >> ((p - 1) % S)) & 1u;
+        }
+        flow_group(a, FP, x[0], x[1], x[2], x[3], sv[0], sv[1], sv[2], sv[3], 1.0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int p = 1 + seg + G * (q + u);
+          if (valid && p <= m) {
+            gdst[p] = x[u];
+            bad |= is_bad(x[u], a.thr);
+          }
+        }
+      }
+    } else if (a.epi == EPI_AOS2) {  // AOS: 0.25 * (accumulated branches + this branch),
+                                     // read and written in place, same rounding as tiles
+      const double* gy = a.acc + base;
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const int p = 1 + seg + G * q;
+        if (valid && p <= m) {
+          const double x = __dmul_rn(0.25, __dadd_rn(gy[p], at(p)));
+          gdst[p] = x;
+          if (a.check) bad |= is_bad(x, a.thr);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const int p = 1 + seg + G * q;
+        if (valid && p <= m) {
+          const double x = at(p);
+          gdst[p] = x;
+          if (a.check) bad |= is_bad(x, a.thr);
+        }
+      }
+    }
+  }
+}
+
 template <int S, int G>
 __global__ void __launch_bounds__(kRWarps * 32, 3)
     k_sweep_rowwarp(const SweepArgs a, const int nlines) {
@@ -1083,6 +1224,7 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
 
   const Layout& L = a.L;
   const int m = a.m, K = L.n1 - 2, i0 = seg * S;
+  const int itop = a.on ? a.o0 + a.on : L.n0 - 2;  // planes itop, itop-1, ... (reverse)
   double* W = Wb + warp * RW::WD + sub * RW::LW;          // this lane's line
   double* sR = Wb + warp * RW::WD + NL * RW::LW + sub * RW::RW;
   bool bad = false;
@@ -1090,7 +1232,7 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
     const int line = wl * NL + sub;
     const bool valid = NL == 1 || line < nlines;  // NL == 1: the loop condition
     // planes in reverse (the axis-1 sweep before this one wrote the last planes last)
-    const int i = valid ? (L.n0 - 2) - line / K : 1, j = valid ? 1 + line % K : 1;
+    const int i = valid ? itop - line / K : 1, j = valid ? 1 + line % K : 1;
     const long long base = L.at(i, j, 0);
     unsigned long long amask = 0ull;
     uint32_t sbits = 0u, cmask = 0u;
@@ -1115,7 +1257,7 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
     {  // the warp's next lines towards L2 while this one is solved (LODIE1 c4: 533 -> 498 us)
       const int nl = (wl + gridDim.x * kRWarps) * NL + sub;
       if (nl < nlines) {
-        const double* np = a.src + L.at((L.n0 - 2) - nl / K, 1 + nl % K, 0) + 1;
+        const double* np = a.src + L.at(itop - nl / K, 1 + nl % K, 0) + 1;
         for (int c = seg; c < G * S / 16; c += G)  // 128-byte lines
           asm volatile("prefetch.global.L2 [%0];" ::"l"(np + 16 * c));
       }
@@ -1131,69 +1273,7 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
       r[q] = v.x;
       r[q + 1] = v.y;
     }
-    if (seg == 0 && valid)
-      r[0] = __dadd_rn(r[0], __dmul_rn((amask & 1ull) ? a.co.flo[1] : a.co.flo[0], bfold));
-    if (seg == (m - 1) / S && valid)
-      fold_high<S>(a, r, amask, seg == 0 ? a.bnd[base + a.hi_off] : bfold);
-    SegOut o;
-    const double* Tv = seg_eliminate<S>(a, r, amask, i0, seg == 0, T, o);
-
-    // reduced system over the G separators of each line
-    double t, tm;
-    const bool nx = seg + 1 < G;
-    const double yFn = __shfl_down_sync(FULL, o.yF, 1, G);
-    const bool clean = __all_sync(FULL, eps_bits(amask, S) == 0ull) && a.static_ok;
-    if (clean) {
-      sR[seg] = o.rs - o.as * o.yL - o.cs * (nx ? yFn : 0.0);
-      __syncwarp();
-      const double2* Rr = reinterpret_cast<const double2*>(sR);
-      const double2* Mr = reinterpret_cast<const double2*>(Mi + seg * (G + 2));
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-      for (int q = 0; q < G / 2; q += 2) {
-        const double2 r0 = Rr[q], m0 = Mr[q], r1 = Rr[q + 1], m1 = Mr[q + 1];
-        s0 = fma(m0.x, r0.x, s0);
-        s1 = fma(m0.y, r0.y, s1);
-        s2 = fma(m1.x, r1.x, s2);
-        s3 = fma(m1.y, r1.y, s3);
-      }
-      t = (s0 + s1) + (s2 + s3);
-    } else {  // parallel cyclic reduction with shuffles
-      const double aFn = __shfl_down_sync(FULL, o.aF, 1, G);
-      const double bFn = __shfl_down_sync(FULL, o.bF, 1, G);
-      double A = o.as * o.aL, B = o.bs + o.as * o.bL + o.cs * (nx ? aFn : 0.0),
-             Cc = o.cs * (nx ? bFn : 0.0), R = o.rs - o.as * o.yL - o.cs * (nx ? yFn : 0.0);
-#pragma unroll
-      for (int d = 1; d < G; d <<= 1) {
-        const double iB = fast_rcp(B);
-        const double Am = __shfl_up_sync(FULL, A, d, G), iBm = __shfl_up_sync(FULL, iB, d, G),
-                     Cm = __shfl_up_sync(FULL, Cc, d, G), Rm = __shfl_up_sync(FULL, R, d, G);
-        const double Ap = __shfl_down_sync(FULL, A, d, G), iBp = __shfl_down_sync(FULL, iB, d, G),
-                     Cp = __shfl_down_sync(FULL, Cc, d, G), Rp = __shfl_down_sync(FULL, R, d, G);
-        const bool lo = seg >= d, hi = seg + d < G;
-        const double k1 = lo ? -A * iBm : 0.0, k2 = hi ? -Cc * iBp : 0.0;
-        A = lo ? k1 * Am : 0.0;
-        Cc = hi ? k2 * Cp : 0.0;
-        B = B + (lo ? k1 * Cm : 0.0) + (hi ? k2 * Ap : 0.0);
-        R = R + (lo ? k1 * Rm : 0.0) + (hi ? k2 * Rp : 0.0);
-      }
-      t = R * fast_rcp(B);
-    }
-    tm = __shfl_up_sync(FULL, t, 1, G);
-    if (seg == 0) tm = 0.0;
-
-    // reconstruct the own rows (separator = t) and put them back into the line buffer
-    if (Tv == nullptr) {
-#pragma unroll
-      for (int q = 0; q < S - 1; ++q)
-        r[q] = fma(a.tmid[TQ_BE * kTabRows + q], t, fma(a.tmid[TQ_AL * kTabRows + q], tm, r[q]));
-    } else {
-#pragma unroll
-      for (int q = 0; q < S - 1; ++q)
-        r[q] = fma(Tv[TQ_BE * kTabRows + q], t, fma(Tv[TQ_AL * kTabRows + q], tm, r[q]));
-    }
-    r[S - 1] = t;
-    if (a.epi == EPI_SRC && cmask) fix_regs<S>(r, cmask, a.epi_coef, a.rho + base + i0 + 1, 1);
+    rw_solve<S, G>(a, r, amask, cmask, bfold, valid, seg, T, Mi, sR, base);
     if (valid) {
 #pragma unroll
       for (int q = 0; q < S; q += 2)
@@ -1201,58 +1281,177 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
     }
     __syncwarp();
 
-    // epilogue + coalesced store of rows 1..m: the G lanes of a line take consecutive rows
-    // (G * 8 = 128- or 256-byte runs), each lane S of them; an idle half-warp (odd line
-    // count) joins the shuffles but stores nothing
-    {
-      double* gdst = a.dst + base;
-      if (a.epi == EPI_FLOW) {  // the tiny-argument form for almost every node, solute bits
-                                // from the lane owning the row's segment
+    rw_store<S, G>(a, [&](int p) { return W[RW::pos(p)]; }, valid, seg, sub, sbits, FP, base,
+                   bad);
+    __syncwarp();  // the line buffers are restaged by the next lines
+  }
+  if (a.check && __any_sync(FULL, bad) && lane == 0) atomicMin(a.div_step, a.step);
+}
+
+// ---------------------------------------------------------------------------------------
+// Row sweeps (axis 2) with TMA staging: the same per-warp line solve as k_sweep_rowwarp, but
+// each line is brought into shared memory by ONE tensor copy (cp.async.bulk.tensor, a box of
+// G*S/16 128-byte chunks of the line, 128-byte swizzle) completing on an mbarrier, and every
+// warp keeps two line buffers: the copy of its next line is in flight while the current one
+// is solved and stored.  The swizzle (16-byte unit u of 128-byte chunk c lands at unit
+// u ^ (c & 7)) keeps the lanes' 16-byte segment-row reads and the coalesced store pass free
+// of bank conflicts without padding, so one contiguous copy per line suffices.
+// Shared memory: [NW warps x 2 buffers x NL lines x G*S doubles, 1024-aligned] | tables |
+// reduced inverse | per-line separator scratch | flow tables | mbarriers.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1,
+                                            int c2, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(tm)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Swizzled position of row e (0-based, e = p - 1) in a line buffer of 16-double chunks.
+__device__ __forceinline__ int swz(int e) {
+  const int c = e >> 4;
+  return (c << 4) | ((((e >> 1) & 7) ^ (c & 7)) << 1) | (e & 1);
+}
+
+template <int S, int G, int NW>
+struct RowTma {
+  static constexpr int NL = 32 / G;        // lines per warp
+  static constexpr int LD = G * S;         // doubles per line buffer (rows 1..m+1)
+  static constexpr int WB = NL * LD;       // doubles per warp buffer
+  static constexpr size_t lines_bytes = (size_t)NW * 2 * WB * sizeof(double);
+  static constexpr size_t smem(int fpoly_n) {
+    return 1024 + lines_bytes +
+           sizeof(double) * (kTabDoubles + G * (G + 2) + NW * NL * (G + 2) + kFlowHdr + fpoly_n) +
+           sizeof(unsigned long long) * NW * 2;
+  }
+};
+
+template <int S, int G, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+    k_sweep_rowtma(const SweepArgs a, const int nlines, const __grid_constant__ CUtensorMap tm) {
+  static_assert(S == 16, "one 128-byte chunk per segment");
+  extern __shared__ unsigned char smraw[];
+  using RT = RowTma<S, G, NW>;
+  constexpr int NL = RT::NL, LD = RT::LD, WB = RT::WB;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int NT = NW * 32;
+  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sub = lane / G, seg = lane % G;
+  double* Lb = reinterpret_cast<double*>(
+      smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u));  // 1024-aligned line buffers
+  double* T = Lb + NW * 2 * WB;
+  double* Mi = T + kTabDoubles;         // G x (G + 2)
+  double* sRb = Mi + G * (G + 2);       // NW * NL * (G + 2)
+  double* FP = sRb + NW * NL * (G + 2);  // flow tables at FP + kFlowHdr
+  unsigned long long* bars =
+      reinterpret_cast<unsigned long long*>(FP + kFlowHdr + a.fpoly_n + (a.fpoly_n & 1));
+  for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
+  if (a.static_ok)
+    for (int c = tid; c < G * (G + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
+  if (uses_flow(a.pro, a.epi))
+    for (int c = tid; c < a.fpoly_n / 2; c += NT) cp_async16(FP + kFlowHdr + 2 * c, a.fpoly + 2 * c);
+  asm volatile("cp.async.commit_group;\n" ::);
+  if (tid < NW * 2) mbar_init(bars + tid, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  cp_async_wait_all();
+  __syncthreads();
+  if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
+
+  const Layout& L = a.L;
+  const int m = a.m, K = L.n1 - 2;
+  const int itop = a.on ? a.o0 + a.on : L.n0 - 2;  // planes itop, itop-1, ... (reverse)
+  double* sR = sRb + (warp * NL + sub) * (G + 2);
+  unsigned long long* bar = bars + warp * 2;
+  const int stride = gridDim.x * NW;
+  const int wl0 = blockIdx.x * NW + warp;
+  // lane 0: one tensor copy per valid line of warp-iteration wl into buffer b
+  auto issue = [&](int wl, int b) {
+    int nv = 0;
 #pragma unroll
-        for (int q = 0; q < S; q += 4) {
-          double x[4];
-          uint32_t sv[4];
+    for (int l = 0; l < NL; ++l) nv += wl * NL + l < nlines;
+    mbar_expect_tx(bar + b, (unsigned)(nv * LD * sizeof(double)));
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int p = 1 + seg + G * (q + u);
-            x[u] = W[RW::pos(p)];
-            sv[u] = (__shfl_sync(FULL, sbits, sub * G + (p - 1) / S) >> ((p - 1) % S)) & 1u;
-          }
-          flow_group(a, FP, x[0], x[1], x[2], x[3], sv[0], sv[1], sv[2], sv[3], 1.0);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int p = 1 + seg + G * (q + u);
-            if (valid && p <= m) {
-              gdst[p] = x[u];
-              bad |= is_bad(x[u], a.thr);
-            }
-          }
-        }
-      } else if (a.epi == EPI_AOS2) {  // AOS: 0.25 * (accumulated branches + this branch),
-                                       // read and written in place, same rounding as tiles
-        const double* gy = a.acc + base;
-#pragma unroll
-        for (int q = 0; q < S; ++q) {
-          const int p = 1 + seg + G * q;
-          if (valid && p <= m) {
-            const double x = __dmul_rn(0.25, __dadd_rn(gy[p], W[RW::pos(p)]));
-            gdst[p] = x;
-            if (a.check) bad |= is_bad(x, a.thr);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < S; ++q) {
-          const int p = 1 + seg + G * q;
-          if (valid && p <= m) {
-            const double x = W[RW::pos(p)];
-            gdst[p] = x;
-            if (a.check) bad |= is_bad(x, a.thr);
-          }
-        }
+    for (int l = 0; l < NL; ++l) {
+      const int line = wl * NL + l;
+      if (line < nlines) {
+        const int i = itop - line / K, j = 1 + line % K;
+        tma_load_3d(Lb + (warp * 2 + b) * WB + l * LD, &tm, 0, 0, i * L.n1 + j, bar + b);
       }
     }
-    __syncwarp();  // the line buffers are restaged by the next lines
+  };
+  if (lane == 0) {
+    if (wl0 * NL < nlines) issue(wl0, 0);
+    if ((wl0 + stride) * NL < nlines) issue(wl0 + stride, 1);
+  }
+  bool bad = false;
+  int it = 0;
+  for (int wl = wl0; wl * NL < nlines; wl += stride, ++it) {
+    const int b = it & 1;
+    const int line = wl * NL + sub;
+    const bool valid = NL == 1 || line < nlines;
+    const int i = valid ? itop - line / K : 1, j = valid ? 1 + line % K : 1;
+    const long long base = L.at(i, j, 0);
+    unsigned long long amask = 0ull;
+    uint32_t sbits = 0u, cmask = 0u;
+    double bfold = 0.0;
+    if (valid) {
+      const ulonglong2 dd = *reinterpret_cast<const ulonglong2*>(
+          a.desc + 2 * (line_desc(L, i, j) * G + seg));
+      amask = dd.x;
+      sbits = (uint32_t)dd.y;
+      cmask = (uint32_t)(dd.y >> 32);
+      if (seg == 0) bfold = a.bnd[base];
+      else if (seg == (m - 1) / S) bfold = a.bnd[base + a.hi_off];
+    }
+    double* W = Lb + (warp * 2 + b) * WB + sub * LD;
+    mbar_wait(bar + b, (unsigned)(it >> 1) & 1u);
+
+    double r[S];
+#pragma unroll
+    for (int q = 0; q < S; q += 2) {  // chunk `seg`, 16-byte unit q/2 at its swizzled place
+      const double2 v = valid ? *reinterpret_cast<const double2*>(
+                                    W + seg * 16 + ((((q >> 1) ^ (seg & 7))) << 1))
+                              : make_double2(0.0, 0.0);
+      r[q] = v.x;
+      r[q + 1] = v.y;
+    }
+    rw_solve<S, G>(a, r, amask, cmask, bfold, valid, seg, T, Mi, sR, base);
+    if (valid) {
+#pragma unroll
+      for (int q = 0; q < S; q += 2)
+        *reinterpret_cast<double2*>(W + seg * 16 + ((((q >> 1) ^ (seg & 7))) << 1)) =
+            make_double2(r[q], r[q + 1]);
+    }
+    __syncwarp();
+    rw_store<S, G>(a, [&](int p) { return W[swz(p - 1)]; }, valid, seg, sub, sbits, FP, base,
+                   bad);
+    // the buffer's generic-proxy reads/writes are ordered before the next tensor copy into it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0 && (wl + 2 * stride) * NL < nlines) issue(wl + 2 * stride, b);
   }
   if (a.check && __any_sync(FULL, bad) && lane == 0) atomicMin(a.div_step, a.step);
 }
@@ -1553,7 +1752,7 @@ static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
 template <int S, int P, bool CN>
 static void launch_col(const SweepArgs& a, int axis, cudaStream_t st) {
   constexpr int LB = 16;
-  const int nouter = (axis == 0 ? a.L.n1 : a.L.n0) - 2;
+  const int nouter = axis == 1 && a.on ? a.on : (axis == 0 ? a.L.n1 : a.L.n0) - 2;
   const int ntx = (a.L.n2 - 2 + LB - 1) / LB;
   const size_t smem =
       sizeof(double) * (kTabDoubles + P * (P + 2) + 4 * LB * P + kFlowHdr + flow_stage_n(a));
@@ -1611,7 +1810,7 @@ static void launch_strided_SP(const SweepArgs& a, int axis, cudaStream_t st) {
 
 template <int S, int G>
 static void launch_rowwarp_SG(const SweepArgs& a, cudaStream_t st) {
-  const int nlines = (a.L.n0 - 2) * (a.L.n1 - 2);
+  const int nlines = (a.on ? a.on : a.L.n0 - 2) * (a.L.n1 - 2);
   const size_t smem = rowwarp_smem(S, G, flow_stage_n(a));
   auto kern = k_sweep_rowwarp<S, G>;
   const int per_block = kRWarps * (32 / G);
@@ -1620,7 +1819,87 @@ static void launch_rowwarp_SG(const SweepArgs& a, cudaStream_t st) {
   kern<<<grid, kRWarps * 32, smem, st>>>(a, nlines);
 }
 
+// TMA row-warp sweeps (k_sweep_rowtma) for 16-row segments (m + 1 = 512, 256); PBG_ROWTMA=0
+// keeps the cp.async row-warp kernel, for comparison.  PBG_ROWTMA_NW: warps per block.
+static int rowtma_mode() {
+  static const int v = [] {
+    const char* e = getenv("PBG_ROWTMA");
+    return e && *e ? atoi(e) : 1;
+  }();
+  return v;
+}
+static int rowtma_nw() {
+  static const int v = [] {
+    const char* e = getenv("PBG_ROWTMA_NW");
+    return e && *e ? atoi(e) : 20;
+  }();
+  return v;
+}
+
+using EncodeTiled = PFN_cuTensorMapEncodeTiled_v12000;
+static EncodeTiled encode_tiled() {
+  static EncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  });
+  return fn;
+}
+
+// Tensor map of the axis-2 lines of a field: (16 doubles, chunk, line) with the line index
+// i*n1 + j, based at row 1 (k = 1, 256-byte aligned), 128-byte swizzle.
+static bool line_tensor_map(const SweepArgs& a, int box_chunks, CUtensorMap* tm) {
+  EncodeTiled fn = encode_tiled();
+  if (!fn) return false;
+  const Layout& L = a.L;
+  cuuint64_t dims[3] = {16, (cuuint64_t)((L.pitch - kOff - 1) / 16),
+                        (cuuint64_t)L.n0 * (cuuint64_t)L.n1};
+  cuuint64_t strides[2] = {128, (cuuint64_t)L.pitch * sizeof(double)};
+  cuuint32_t box[3] = {16, (cuuint32_t)box_chunks, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)(a.src + kOff + 1), dims, strides,
+            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int S, int G, int NW>
+static bool launch_rowtma_SGN(const SweepArgs& a, cudaStream_t st) {
+  CUtensorMap tm;
+  if (!line_tensor_map(a, G * S / 16, &tm)) return false;
+  const int nlines = (a.on ? a.on : a.L.n0 - 2) * (a.L.n1 - 2);
+  const size_t smem = RowTma<S, G, NW>::smem(flow_stage_n(a));
+  auto kern = k_sweep_rowtma<S, G, NW>;
+  const int per_block = NW * (32 / G);
+  const int grid = std::min((nlines + per_block - 1) / per_block,
+                            resident_blocks((const void*)kern, NW * 32, smem));
+  kern<<<grid, NW * 32, smem, st>>>(a, nlines, tm);
+  return true;
+}
+
+template <int S, int G>
+static bool launch_rowtma_SG(const SweepArgs& a, cudaStream_t st) {
+  switch (rowtma_nw()) {
+    case 8: return launch_rowtma_SGN<S, G, 8>(a, st);
+    case 12: return launch_rowtma_SGN<S, G, 12>(a, st);
+    case 16: return launch_rowtma_SGN<S, G, 16>(a, st);
+    default: return launch_rowtma_SGN<S, G, 20>(a, st);
+  }
+}
+
 static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
+  if (a.rw && rowtma_mode() && rowwarp_S(a.m) == 16) {
+    const bool ok = rowwarp_G(a.m) == 32 ? launch_rowtma_SG<16, 32>(a, st)
+                                         : launch_rowtma_SG<16, 16>(a, st);
+    if (ok) {
+      PBG_LAUNCH_CHECK("k_sweep_rowtma");
+      return PBG_OK;
+    }
+  }
   if (a.rw) {
     switch (rowwarp_G(a.m) * 100 + rowwarp_S(a.m)) {
       case 3216: launch_rowwarp_SG<16, 32>(a, st); break;
@@ -2116,6 +2395,11 @@ void march_axes(const pbg_march_desc* d, const Plan& plan, SweepArgs ax[3]) {
   }
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
 static bool g_profile = false;
 static double g_prof_ms[3] = {0, 0, 0};
 static long long g_prof_n[3] = {0, 0, 0};
@@ -2209,49 +2493,69 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
   if (d->initial == d->work[0]) st_idx = 0;
   else if (d->initial == d->work[1]) st_idx = 1;
   const int st0 = st_idx;
+  // LOD steps whose axis-2 sweep runs the row-warp kernel write it in place over the axis-1
+  // output (its lines are staged whole before they are stored), so the step's state stays in
+  // one buffer; optionally the axis-1 and axis-2 sweeps alternate over plane chunks so that
+  // axis 2 reads the axis-1 output (and rewrites it) while it is still in L2.
+  const bool lod_rw = plan.family <= 1 && ax[2].rw;
+  const int chunk = lod_rw ? env_int("PBG_FUSE12", 0) : 0;
+  const bool inpl = lod_rw && (chunk > 0 || env_int("PBG_INPLACE2", 0) != 0);
+  const int nplanes = g->n[0] - 2;
 
   cudaEvent_t e0, e1;
   PBG_CUDA(cudaEventCreate(&e0));
   PBG_CUDA(cudaEventCreate(&e1));
   std::vector<cudaEvent_t> kev;  // per-launch events when profiling is on
+  auto mark = [&]() {
+    if (!g_profile) return;
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    cudaEventRecord(ev, st);
+    kev.push_back(ev);
+  };
   PBG_CUDA(cudaEventRecord(e0, st));
   for (int s = 1; s <= d->nsteps; ++s) {
     const double* X = st_idx < 0 ? d->initial : d->work[st_idx];
     const int other = st_idx < 0 ? 0 : 1 - st_idx;
     double* A = d->work[other];
     double* Bf = st_idx < 0 ? d->work[1] : d->work[st_idx];
+    SweepArgs as[3];
     for (int axis = 0; axis < 3; ++axis) {
-      SweepArgs a = ax[axis];
+      SweepArgs& a = as[axis];
+      a = ax[axis];
       a.step = s;
       a.div_step = d->check_divergence ? dflag : nullptr;
       if (plan.family <= 1) {
         a.src = axis == 0 ? X : (axis == 1 ? A : Bf);
-        a.dst = axis == 0 ? A : (axis == 1 ? Bf : A);
+        a.dst = axis == 0 ? A : (axis == 1 ? Bf : (inpl ? Bf : A));
       } else {
         a.src = X;
         a.acc = A;
         a.dst = A;
       }
-      if (g_profile) {
-        cudaEvent_t ev;
-        cudaEventCreate(&ev);
-        cudaEventRecord(ev, st);
-        kev.push_back(ev);
-      }
-      rc = launch_sweep(a, axis, st);
-      if (g_profile) {
-        cudaEvent_t ev;
-        cudaEventCreate(&ev);
-        cudaEventRecord(ev, st);
-        kev.push_back(ev);
-      }
-      if (rc) {
-        cudaFreeAsync(dflag, st);
-        for (int q = 0; q < 3; ++q) release_axis(aux[q], st);
-        return rc;
-      }
     }
-    st_idx = other;
+    for (int axis = 0; axis < 3 && !rc; ++axis) {
+      mark();
+      if (chunk > 0 && axis == 1) {  // axes 1 and 2 interleaved over plane chunks
+        for (int c0 = 0; c0 < nplanes && !rc; c0 += chunk) {
+          for (int q = 1; q <= 2 && !rc; ++q) {
+            SweepArgs a = as[q];
+            a.o0 = c0;
+            a.on = std::min(chunk, nplanes - c0);
+            rc = launch_sweep(a, q, st);
+          }
+        }
+      } else if (!(chunk > 0 && axis == 2)) {
+        rc = launch_sweep(as[axis], axis, st);
+      }
+      mark();
+    }
+    if (rc) {
+      cudaFreeAsync(dflag, st);
+      for (int q = 0; q < 3; ++q) release_axis(aux[q], st);
+      return rc;
+    }
+    st_idx = inpl ? (st_idx < 0 ? 1 : st_idx) : other;
   }
   PBG_CUDA(cudaEventRecord(e1, st));
   int dstep = INT_MAX;
@@ -2280,7 +2584,8 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
   }
   // state slot after `taken` steps
   int slot;
-  if (st0 < 0) slot = (taken - 1) % 2;
+  if (inpl) slot = st0 < 0 ? 1 : st0;
+  else if (st0 < 0) slot = (taken - 1) % 2;
   else slot = (st0 + taken) % 2;
   if (steps_taken) *steps_taken = taken;
   if (result_slot) *result_slot = slot;

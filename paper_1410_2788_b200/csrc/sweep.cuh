@@ -92,6 +92,9 @@ struct SweepArgs {
   // ends[base + ends_off] instead of the field (axis 0 only).
   double* ends;
   long long ends_off;
+  // Outer-index range of a launch (axis 1 column tiles: planes i; axis 2 row-warp lines:
+  // planes i): planes o0+1 .. o0+on; on = 0 means all interior planes.
+  int o0, on;
 };
 
 

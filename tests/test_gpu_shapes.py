@@ -84,7 +84,7 @@ def test_row_warp_divergence_vs_oracle(shape):
     # step-2 and step-6 maxima trips inside the march (the row-warp sweep raises the flag);
     # the march must stop at the oracle's step and return that step's field
     p, op = problems(shape, seed=2, faces=0.0, source=500.0)
-    for v in ["LODIE2", "LODIE1"]:
+    for v in ["LODIE2", "LODIE1", "AOSIE1"]:
         amax = [np.max(np.abs(O.march(op, v, 0.2, 0.2 * k).final)) for k in (2, 6)]
         assert amax[1] > amax[0] > 0.0
         thr = 0.5 * (amax[0] + amax[1])
