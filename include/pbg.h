@@ -164,6 +164,22 @@ typedef struct pbg_march_desc {
 PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken, int32_t* diverged_step,
                       int32_t* result_slot, float* device_ms, void* stream);
 
+/* A prepared march (the reference's Stepper: schemes.py:188-262 factor once, then step):
+ * pbg_plan_create builds the per-axis tables, segment descriptors and deduplicated segment
+ * factors for d's codes / variant / dt / alpha (d->codes and d->rho must stay valid for the
+ * plan's lifetime; d->work[0] is used for setup only; synchronous).  pbg_plan_run marches
+ * nsteps from `initial` with the two work buffers (faces = Dirichlet data, as pbg_march),
+ * launching only the step kernels and synchronising once at the end; check_divergence 1 =
+ * march semantics, 0 = Stepper.step / step() (schemes.py:365-396).  Outputs as pbg_march.
+ * pbg_march == create + run + destroy.  A plan may run on any stream, one run at a time. */
+typedef struct pbg_plan pbg_plan;
+PBG_API int pbg_plan_create(const pbg_march_desc* d, pbg_plan** out, void* stream);
+PBG_API int pbg_plan_run(pbg_plan* p, const double* initial, double* work0, double* work1,
+                         int32_t nsteps, int32_t check_divergence, int32_t* steps_taken,
+                         int32_t* diverged_step, int32_t* result_slot, float* device_ms,
+                         void* stream);
+PBG_API int pbg_plan_destroy(pbg_plan* p, void* stream);
+
 /* Per-sweep-kernel timing (CUDA events around every launch inside pbg_march, on the
  * launching stream).  pbg_set_profiling(1) enables and resets the accumulators;
  * pbg_get_profile returns the summed milliseconds and launch counts per sweep axis. */
@@ -209,9 +225,9 @@ PBG_API int pbg_sweep(const pbg_grid* g, const pbg_palette* pal, const uint8_t* 
  * the global layout.  Variants: LODIE1, LODIE2, LODCN2.
  *
  * Exchange buffers (device, owned by the caller): send holds pbg_slab_exchange_elems(local)
- * doubles, recv nranks times that; after every *pack / step_a call the caller all-gathers
- * send into recv in rank order (ncclAllGather, or a device copy when all partitions live on
- * one GPU) on the same stream before the next call.
+ * doubles, recv nranks times that; after every *pack / step_a(_chunk) call the caller
+ * all-gathers the phase's part of send (pbg_slab_phase) into recv in rank order
+ * (ncclAllGather, or a device copy when all partitions live on one GPU) before step_b.
  *
  *   create            computes this rank's static responses into send  -> all-gather
  *   setup             keeps the gathered responses
@@ -222,7 +238,21 @@ PBG_API int pbg_sweep(const pbg_grid* g, const pbg_palette* pal, const uint8_t* 
  *                                       *result_slot indexes work[] as in pbg_march)
  * Results equal pbg_march on the whole grid up to reassociation (parity tests). */
 typedef struct pbg_slab pbg_slab;
+/* Doubles of the send buffer (recv: nranks times that) for a local grid. */
 PBG_API int64_t pbg_slab_exchange_elems(const pbg_grid* local);
+/* Exchange phases: which part of send travels (offset, count in doubles); the gathered
+ * blocks land rank-major at recv + nranks*offset.  SETUP: the static responses (once);
+ * HALO: the state's end planes (LODCN2, per step); STEP: chunk `chunk` of the end rows of
+ * phase A + the divergence flag (per step, one all-gather per chunk so that the exchange of
+ * chunk c overlaps phase A of chunk c+1).  Only interior lines travel (compact planes of
+ * (n1-2)*(n2-2) values).  PBG_SLAB_CHUNKS (env, default 4) sets the chunk count; it must be
+ * the same on every rank. */
+enum { PBG_SLAB_SETUP = 0, PBG_SLAB_HALO = 1, PBG_SLAB_STEP = 2 };
+PBG_API int32_t pbg_slab_nchunks(const pbg_slab* h);
+PBG_API int pbg_slab_phase(const pbg_slab* h, int32_t phase, int32_t chunk, int64_t* offset,
+                           int64_t* count);
+/* Phase A of one chunk (axis-0 lines with j in the chunk); pbg_slab_step_a = all chunks. */
+PBG_API int pbg_slab_step_a_chunk(pbg_slab* h, int32_t chunk, void* stream);
 PBG_API int pbg_slab_create(const pbg_march_desc* d, int32_t rank, int32_t nranks,
                             double* send, double* recv, pbg_slab** out, void* stream);
 PBG_API int pbg_slab_setup(pbg_slab* h, void* stream);

@@ -35,6 +35,8 @@ int validate_grid(const pbg_grid* g) {
   for (int a = 0; a < 3; ++a)
     if (g->n[a] < 3) return fail(PBG_E_INVALID, "every axis needs at least 3 nodes");
   if (g->pitch < (int64_t)g->n[2] + kOff) return fail(PBG_E_INVALID, "pitch too small");
+  if (g->pitch % 32)  // 256-byte aligned rows: the row sweeps' 16-byte and tensor copies
+    return fail(PBG_E_INVALID, "pitch must be a multiple of 32 (use pbg_layout)");
   if (!(g->h > 0)) return fail(PBG_E_INVALID, "spacing must be positive");
   return PBG_OK;
 }

@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <vector>
 
 #include "sweep.cuh"
@@ -48,15 +49,51 @@ __global__ void k_slab_add_source(double* x, const double* rho, double c, long l
     if (r != 0.0) x[t] = __dadd_rn(x[t], __dmul_rn(c, r));
   }
 }
-static long long slab_elems(const Layout& L) { return 4 * slab_plane(L) + kExchTail; }
+// Exchange layouts (doubles; every block a multiple of 32 so rank blocks stay 256-byte
+// aligned).  Only interior lines travel, in the compact order c(j, k) = (j-1)*(n2-2) + (k-1)
+// (C of them per plane):
+//   setup  [p_f | p_l | q_f | q_l] (4C)                       static responses, once
+//   halo   [state plane 1 | state plane n0-2] (pitched planes) LODCN2 only, per step
+//   step   nchunks blocks, chunk c = interior rows j in [1 + c*J, 1 + (c+1)*J):
+//          [header 32: divergence flag | g_f of the chunk's lines | g_l of them]
+//          all-gathered chunk by chunk, so the exchange of chunk c overlaps phase A of c+1.
+__host__ __device__ static long long rup32(long long n) { return (n + 31) / 32 * 32; }
+__host__ __device__ static long long compact_plane(const Layout& L) { return (long long)(L.n1 - 2) * (L.n2 - 2); }
+static int chunk_rows(const Layout& L, int nchunks) { return (L.n1 - 2 + nchunks - 1) / nchunks; }
+static int n_chunks(const Layout& L, int want) {
+  const int J = chunk_rows(L, want);
+  return (L.n1 - 2 + J - 1) / J;  // no empty chunk
+}
+__host__ __device__ static long long chunk_block(const Layout& L, int J, int c) {
+  const int rows = min(J, L.n1 - 2 - c * J);
+  return kExchTail + rup32(2LL * rows * (L.n2 - 2));
+}
+static long long setup_elems(const Layout& L) { return rup32(4 * compact_plane(L)) + kExchTail; }
+static long long halo_elems(const Layout& L) { return 2 * slab_plane(L) + kExchTail; }
+static long long step_elems(const Layout& L, int nchunks) {
+  const int J = chunk_rows(L, nchunks), nc = n_chunks(L, nchunks);
+  long long t = 0;
+  for (int c = 0; c < nc; ++c) t += chunk_block(L, J, c);
+  return t;
+}
+static long long slab_elems(const Layout& L, int nchunks) {
+  return std::max(std::max(setup_elems(L), halo_elems(L)), step_elems(L, nchunks));
+}
+static int slab_chunks_env() {
+  const char* e = getenv("PBG_SLAB_CHUNKS");
+  const int v = e && *e ? atoi(e) : 4;
+  return std::max(1, std::min(v, 64));
+}
 
-// Per line (j, k): block Thomas over the ranks' chunk end values.  recv/coef hold one
-// exchange block of E doubles per rank: planes [g_f | g_l | .. ] and [p_f | p_l | q_f | q_l].
+// Per line (j, k): block Thomas over the ranks' chunk end values.  recv holds the step
+// exchange (chunk blocks, rank-major inside each chunk), coef the gathered setup blocks.
 __global__ void k_slab_interface(const Layout L, int rank, int nranks, const double* recv,
-                                 const double* coef, long long E, double* gb, int* dflag) {
-  const long long plane = L.s0;
+                                 const double* coef, long long Es, int J, double* gb,
+                                 int* dflag) {
+  const long long plane = L.s0, C = compact_plane(L);
+  const long long B0 = chunk_block(L, J, 0);
   if (blockIdx.x == 0 && (int)threadIdx.x < nranks) {
-    const int f = *reinterpret_cast<const int*>(recv + threadIdx.x * E + 4 * plane);
+    const int f = *reinterpret_cast<const int*>(recv + threadIdx.x * B0);
     if (f != INT_MAX) atomicMin(dflag, f);
   }
   const int nj = L.n1 - 2, nk = L.n2 - 2;
@@ -65,21 +102,26 @@ __global__ void k_slab_interface(const Layout L, int rank, int nranks, const dou
        t += (long long)gridDim.x * blockDim.x) {
     const int j = 1 + (int)(t / nk), k = 1 + (int)(t % nk);
     const long long o = L.at(0, j, k);
+    const int c = (j - 1) / J;
+    const long long Bc = chunk_block(L, J, c), len = (Bc == B0 ? (long long)J * nk
+                                                                : (long long)(nj - c * J) * nk);
+    const long long local = t - (long long)c * J * nk;
+    const double* chunk = recv + (long long)nranks * c * B0;  // all earlier chunks are full
     double e[kMaxRanks], hh[kMaxRanks], cc[kMaxRanks], dd[kMaxRanks];
-    double c = 0.0, d = 0.0;
+    double cv = 0.0, d = 0.0;
     for (int r = 0; r < nranks; ++r) {
-      const double* G = recv + r * E;
-      const double* Q = coef + r * E;
-      const double gf = G[o], gl = G[plane + o];
-      const double pf = r > 0 ? Q[o] : 0.0, pl = r > 0 ? Q[plane + o] : 0.0;
-      const double qf = r + 1 < nranks ? Q[2 * plane + o] : 0.0;
-      const double ql = r + 1 < nranks ? Q[3 * plane + o] : 0.0;
+      const double* G = chunk + r * Bc + kExchTail;
+      const double* Q = coef + r * Es;
+      const double gf = G[local], gl = G[len + local];
+      const double pf = r > 0 ? Q[t] : 0.0, pl = r > 0 ? Q[C + t] : 0.0;
+      const double qf = r + 1 < nranks ? Q[2 * C + t] : 0.0;
+      const double ql = r + 1 < nranks ? Q[3 * C + t] : 0.0;
       const double inv = 1.0 / (1.0 - pf * d);
-      e[r] = (gf + pf * c) * inv;
+      e[r] = (gf + pf * cv) * inv;
       hh[r] = qf * inv;
-      const double cn = gl + pl * c + pl * d * e[r];
+      const double cn = gl + pl * cv + pl * d * e[r];
       const double dn = pl * d * hh[r] + ql;
-      cc[r] = c = cn;
+      cc[r] = cv = cn;
       dd[r] = d = dn;
     }
     double F = 0.0, Lprev = 0.0, Fnext = 0.0;
@@ -109,8 +151,13 @@ struct pbg_slab {
   double* gbB = nullptr;   // ghost values of phase B: the neighbours' chunk end values
   int* dflag = nullptr;
   int st_idx, st0, step;
-  long long plane, E;
+  long long plane, C, Es, Eh;
+  int J, nchunks;  // step exchange: chunks of J interior rows j
 };
+
+static long long chunk_offset(const pbg_slab* h, int c) {
+  return (long long)c * chunk_block(make_layout(&h->d.grid), h->J, 0);
+}
 
 static int slab_state(const pbg_slab* h, const double** X, double** A, double** Bf) {
   const pbg_march_desc* d = &h->d;
@@ -123,7 +170,25 @@ static int slab_state(const pbg_slab* h, const double** X, double** A, double** 
 
 extern "C" PBG_API int64_t pbg_slab_exchange_elems(const pbg_grid* local) {
   if (!local) return -1;
-  return slab_elems(make_layout(local));
+  return slab_elems(make_layout(local), slab_chunks_env());
+}
+
+extern "C" PBG_API int32_t pbg_slab_nchunks(const pbg_slab* h) { return h ? h->nchunks : -1; }
+
+extern "C" PBG_API int pbg_slab_phase(const pbg_slab* h, int32_t phase, int32_t chunk,
+                                      int64_t* offset, int64_t* count) {
+  if (!h || !offset || !count) return fail(PBG_E_INVALID, "null argument");
+  const Layout L = make_layout(&h->d.grid);
+  switch (phase) {
+    case PBG_SLAB_SETUP: *offset = 0; *count = h->Es; return PBG_OK;
+    case PBG_SLAB_HALO: *offset = 0; *count = h->Eh; return PBG_OK;
+    case PBG_SLAB_STEP:
+      if (chunk < 0 || chunk >= h->nchunks) return fail(PBG_E_INVALID, "chunk out of range");
+      *offset = chunk_offset(h, chunk);
+      *count = chunk_block(L, h->J, chunk);
+      return PBG_OK;
+    default: return fail(PBG_E_INVALID, "unknown exchange phase");
+  }
 }
 
 extern "C" PBG_API int pbg_slab_destroy(pbg_slab* h, void* stream) {
@@ -177,7 +242,11 @@ extern "C" PBG_API int pbg_slab_create(const pbg_march_desc* d, int32_t rank, in
   }
   const Layout L = make_layout(&d->grid);
   h->plane = slab_plane(L);
-  h->E = slab_elems(L);
+  h->C = compact_plane(L);
+  h->Es = setup_elems(L);
+  h->Eh = halo_elems(L);
+  h->J = chunk_rows(L, slab_chunks_env());
+  h->nchunks = n_chunks(L, slab_chunks_env());
   const size_t pb = h->plane * sizeof(double);
   const bool first = rank == 0, last = rank == nranks - 1;
   auto cu = [&](cudaError_t e) {
@@ -190,7 +259,7 @@ extern "C" PBG_API int pbg_slab_create(const pbg_march_desc* d, int32_t rank, in
   double* zeros = nullptr;
   double* unit = nullptr;
   const long long nelem = (long long)L.n0 * L.s0 + 64;
-  bool ok = cu(cudaMallocAsync(&h->coef, nranks * h->E * sizeof(double), st)) &&
+  bool ok = cu(cudaMallocAsync(&h->coef, nranks * h->Es * sizeof(double), st)) &&
             cu(cudaMallocAsync(&h->gbA, 2 * pb, st)) && cu(cudaMallocAsync(&h->gbB, 2 * pb, st)) &&
             cu(cudaMallocAsync(&h->dflag, sizeof(int), st)) &&
             cu(cudaMallocAsync(&zeros, nelem * sizeof(double), st)) &&
@@ -227,17 +296,13 @@ extern "C" PBG_API int pbg_slab_create(const pbg_march_desc* d, int32_t rank, in
     a.dst = zeros;
     a.bnd = unit;
     a.hi_off = h->plane;
-    a.ends = send + 2 * side * h->plane;
-    a.ends_off = h->plane;
+    a.ends = send + 2 * side * h->C;
+    a.ends_off = h->C;
     a.step = 1;
     a.div_step = nullptr;
     if (launch_sweep(a, 0, st)) ok = false;
   }
-  if (ok) {
-    const int init = INT_MAX;
-    ok = cu(cudaMemcpyAsync(send + 4 * h->plane, &init, sizeof(init), cudaMemcpyHostToDevice,
-                            st));
-  }
+
   if (ok && d->check_divergence) {
     k_faces_bad<<<148, 256, 0, st>>>(L, d->work[0], d->divergence_threshold, h->dflag,
                                      first ? 0 : 1, last ? 0 : 1);
@@ -262,7 +327,7 @@ extern "C" PBG_API int pbg_slab_create(const pbg_march_desc* d, int32_t rank, in
 extern "C" PBG_API int pbg_slab_setup(pbg_slab* h, void* stream) {
   if (!h) return fail(PBG_E_INVALID, "null slab");
   cudaStream_t st = (cudaStream_t)stream;
-  PBG_CUDA(cudaMemcpyAsync(h->coef, h->recv, h->nranks * h->E * sizeof(double),
+  PBG_CUDA(cudaMemcpyAsync(h->coef, h->recv, h->nranks * h->Es * sizeof(double),
                            cudaMemcpyDeviceToDevice, st));
   return PBG_OK;
 }
@@ -299,20 +364,24 @@ extern "C" PBG_API int pbg_slab_halo_unpack(pbg_slab* h, void* stream) {
   const int n0 = h->d.grid.n[0];
   const size_t pb = h->plane * sizeof(double);
   if (h->rank > 0)
-    PBG_CUDA(cudaMemcpyAsync(Xw, h->recv + (h->rank - 1) * h->E + h->plane, pb,
+    PBG_CUDA(cudaMemcpyAsync(Xw, h->recv + (h->rank - 1) * h->Eh + h->plane, pb,
                              cudaMemcpyDeviceToDevice, st));
   if (h->rank + 1 < h->nranks)
-    PBG_CUDA(cudaMemcpyAsync(Xw + (n0 - 1) * h->plane, h->recv + (h->rank + 1) * h->E, pb,
+    PBG_CUDA(cudaMemcpyAsync(Xw + (n0 - 1) * h->plane, h->recv + (h->rank + 1) * h->Eh, pb,
                              cudaMemcpyDeviceToDevice, st));
   return PBG_OK;
 }
 
-extern "C" PBG_API int pbg_slab_step_a(pbg_slab* h, void* stream) {
+extern "C" PBG_API int pbg_slab_step_a_chunk(pbg_slab* h, int32_t chunk, void* stream) {
   if (!h) return fail(PBG_E_INVALID, "null slab");
+  if (chunk < 0 || chunk >= h->nchunks) return fail(PBG_E_INVALID, "chunk out of range");
   cudaStream_t st = (cudaStream_t)stream;
   const double *X;
   double *A, *Bf;
   slab_state(h, &X, &A, &Bf);
+  const Layout L = make_layout(&h->d.grid);
+  const long long off = chunk_offset(h, chunk);
+  const int j0 = chunk * h->J, rows = std::min(h->J, L.n1 - 2 - j0);
   SweepArgs a = h->ax[0];
   a.step = h->step + 1;
   a.div_step = h->d.check_divergence ? h->dflag : nullptr;
@@ -320,12 +389,25 @@ extern "C" PBG_API int pbg_slab_step_a(pbg_slab* h, void* stream) {
   a.dst = A;  // not written in ends-only mode
   a.bnd = h->gbA;
   a.hi_off = h->plane;
-  a.ends = h->send;
-  a.ends_off = h->plane;
+  a.o0 = j0;  // axis-0 lines (j, k) with j in this chunk
+  a.on = rows;
+  // the kernel writes ends[c(j, k)] and ends[c(j, k) + ends_off] (compact c): shift the base
+  // so the chunk's g_f / g_l land right after its header
+  a.ends = h->send + off + kExchTail - (long long)j0 * (L.n2 - 2);
+  a.ends_off = (long long)rows * (L.n2 - 2);
   int rc = launch_sweep(a, 0, st);
   if (rc) return rc;
-  PBG_CUDA(cudaMemcpyAsync(h->send + 4 * h->plane, h->dflag, sizeof(int),
-                           cudaMemcpyDeviceToDevice, st));
+  if (chunk == 0)  // the flag after the previous step rides in chunk 0's header
+    PBG_CUDA(cudaMemcpyAsync(h->send, h->dflag, sizeof(int), cudaMemcpyDeviceToDevice, st));
+  return PBG_OK;
+}
+
+extern "C" PBG_API int pbg_slab_step_a(pbg_slab* h, void* stream) {
+  if (!h) return fail(PBG_E_INVALID, "null slab");
+  for (int c = 0; c < h->nchunks; ++c) {
+    int rc = pbg_slab_step_a_chunk(h, c, stream);
+    if (rc) return rc;
+  }
   return PBG_OK;
 }
 
@@ -336,8 +418,8 @@ extern "C" PBG_API int pbg_slab_step_b(pbg_slab* h, void* stream) {
   double *A, *Bf;
   const int other = slab_state(h, &X, &A, &Bf);
   const Layout L = make_layout(&h->d.grid);
-  k_slab_interface<<<148 * 4, 256, 0, st>>>(L, h->rank, h->nranks, h->recv, h->coef, h->E,
-                                            h->gbB, h->dflag);
+  k_slab_interface<<<148 * 4, 256, 0, st>>>(L, h->rank, h->nranks, h->recv, h->coef, h->Es,
+                                            h->J, h->gbB, h->dflag);
   PBG_LAUNCH_CHECK("k_slab_interface");
   const int s = h->step + 1;
   for (int axis = 0; axis < 3; ++axis) {
@@ -360,8 +442,8 @@ extern "C" PBG_API int pbg_slab_step_b(pbg_slab* h, void* stream) {
 
 extern "C" PBG_API int pbg_slab_flag_pack(pbg_slab* h, void* stream) {
   if (!h) return fail(PBG_E_INVALID, "null slab");
-  PBG_CUDA(cudaMemcpyAsync(h->send + 4 * h->plane, h->dflag, sizeof(int),
-                           cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  PBG_CUDA(cudaMemcpyAsync(h->send, h->dflag, sizeof(int), cudaMemcpyDeviceToDevice,
+                           (cudaStream_t)stream));
   return PBG_OK;
 }
 
@@ -372,8 +454,8 @@ extern "C" PBG_API int pbg_slab_finish(pbg_slab* h, int32_t* steps_taken,
   cudaStream_t st = (cudaStream_t)stream;
   std::vector<int> flags(h->nranks);
   for (int r = 0; r < h->nranks; ++r)
-    PBG_CUDA(cudaMemcpyAsync(&flags[r], h->recv + r * h->E + 4 * h->plane, sizeof(int),
-                             cudaMemcpyDeviceToHost, st));
+    PBG_CUDA(cudaMemcpyAsync(&flags[r], h->recv + r * chunk_block(make_layout(&h->d.grid), h->J, 0),
+                             sizeof(int), cudaMemcpyDeviceToHost, st));
   int local = INT_MAX;
   PBG_CUDA(cudaMemcpyAsync(&local, h->dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
   PBG_CUDA(cudaStreamSynchronize(st));

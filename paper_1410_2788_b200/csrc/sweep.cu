@@ -421,6 +421,12 @@ struct TileGeo {
   long long base;  // global offset of row 0 of tile line 0
 };
 
+// Slab phase A (axis-0 column tiles): the compact index (j-1)*(n2-2) + (k-1) of line (j, k)
+// in the exchanged end-row planes (only interior lines travel, no pitch padding or faces).
+__device__ __forceinline__ long long ends_index(const SweepArgs& a, const TileGeo& g, int l) {
+  return (long long)(g.outer - 1) * (a.L.n2 - 2) + (g.c0 - 1 + l);
+}
+
 template <int LB, bool RT>
 __device__ __forceinline__ TileGeo tile_geo(const SweepArgs& a, int axis, int tx, int ty,
                                             int nty) {
@@ -429,7 +435,7 @@ __device__ __forceinline__ TileGeo tile_geo(const SweepArgs& a, int axis, int tx
   g.c0 = 1 + tx * LB;
   // Row tiles walk the planes in reverse: the axis-1 sweep before them wrote the last planes
   // last, so those are still in L2 when this launch starts.
-  g.outer = RT ? nty - ty : 1 + ty;
+  g.outer = RT ? a.o0 + nty - ty : 1 + ty + a.o0;  // a.o0: first outer index of a chunk launch
   const int K = (RT ? L.n1 : L.n2) - 2;  // lines per outer index
   g.ncols = min(LB, K + 1 - g.c0);
   if (RT) {
@@ -658,7 +664,8 @@ __device__ __forceinline__ void tile_body(const SweepArgs& a, const TileGeo& g, 
     if (tid < 2 * LB) {
       const int l = tid % LB;
       const bool hi = tid >= LB;
-      if (l < ncols) a.ends[lb(l) + (hi ? a.ends_off : 0ll)] = W[sidx(hi ? m : 1, l)];
+      if (l < ncols)  // compact (j-1)*(n2-2) + (k-1) planes
+        a.ends[ends_index(a, g, l) + (hi ? a.ends_off : 0ll)] = W[sidx(hi ? m : 1, l)];
     }
     return;
   }
@@ -858,11 +865,12 @@ __device__ __forceinline__ void col_body(const SweepArgs& a, const TileGeo& g, d
   if (a.epi == EPI_SRC && cmask) fix_regs<S>(r, cmask, a.epi_coef, rr, st);
   if (!act) return;
   if (a.ends) {  // slab phase A (axis 0): only the chunk's end rows 1 and m leave the block
-    if (seg == 0) a.ends[gl] = r[0];
+    const long long ei = ends_index(a, g, threadIdx.x);
+    if (seg == 0) a.ends[ei] = r[0];
     const int jl = (m - 1) - i0;
 #pragma unroll
     for (int j = 0; j < S; ++j)
-      if (j == jl) a.ends[gl + a.ends_off] = r[j];
+      if (j == jl) a.ends[ei + a.ends_off] = r[j];
     return;
   }
   // Epilogue and store of the own rows 1..m.
@@ -935,7 +943,7 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
   constexpr int NT = LB * kSegS;
   const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
   const int tid = threadIdx.y * LB + threadIdx.x;
-  const TileGeo g = tile_geo<LB, false>(a, axis, blockIdx.x, blockIdx.y + a.o0, gridDim.y);
+  const TileGeo g = tile_geo<LB, false>(a, axis, blockIdx.x, blockIdx.y, gridDim.y);
   const int m = a.m, i0 = threadIdx.y * S;
   const bool act = threadIdx.x < g.ncols;
   const int st = g.stride;
@@ -1406,6 +1414,29 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if (wl0 * NL < nlines) issue(wl0, 0);
     if ((wl0 + stride) * NL < nlines) issue(wl0 + stride, 1);
   }
+  // descriptor words and Dirichlet fold value of warp-iteration wl's line, loaded one
+  // iteration ahead (their latency was the kernel's top stall when loaded in place)
+  auto line_of = [&](int wl, int& i, int& j) {
+    const int line = wl * NL + sub;
+    const bool v = NL == 1 || line < nlines;
+    i = v ? itop - line / K : 1;
+    j = v ? 1 + line % K : 1;
+    return v && wl * NL < nlines;
+  };
+  auto fetch = [&](int wl, ulonglong2& dd, double& bf) {
+    int i, j;
+    dd = make_ulonglong2(0ull, 0ull);
+    bf = 0.0;
+    if (line_of(wl, i, j)) {
+      dd = *reinterpret_cast<const ulonglong2*>(a.desc + 2 * (line_desc(L, i, j) * G + seg));
+      const long long bs = L.at(i, j, 0);
+      if (seg == 0) bf = a.bnd[bs];
+      else if (seg == (m - 1) / S) bf = a.bnd[bs + a.hi_off];
+    }
+  };
+  ulonglong2 ddn;
+  double bfn;
+  fetch(wl0, ddn, bfn);
   bool bad = false;
   int it = 0;
   for (int wl = wl0; wl * NL < nlines; wl += stride, ++it) {
@@ -1414,18 +1445,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const bool valid = NL == 1 || line < nlines;
     const int i = valid ? itop - line / K : 1, j = valid ? 1 + line % K : 1;
     const long long base = L.at(i, j, 0);
-    unsigned long long amask = 0ull;
-    uint32_t sbits = 0u, cmask = 0u;
-    double bfold = 0.0;
-    if (valid) {
-      const ulonglong2 dd = *reinterpret_cast<const ulonglong2*>(
-          a.desc + 2 * (line_desc(L, i, j) * G + seg));
-      amask = dd.x;
-      sbits = (uint32_t)dd.y;
-      cmask = (uint32_t)(dd.y >> 32);
-      if (seg == 0) bfold = a.bnd[base];
-      else if (seg == (m - 1) / S) bfold = a.bnd[base + a.hi_off];
-    }
+    const unsigned long long amask = ddn.x;
+    const uint32_t sbits = (uint32_t)ddn.y, cmask = (uint32_t)(ddn.y >> 32);
+    const double bfold = bfn;
+    fetch(wl + stride, ddn, bfn);
     double* W = Lb + (warp * 2 + b) * WB + sub * LD;
     mbar_wait(bar + b, (unsigned)(it >> 1) & 1u);
 
@@ -1736,7 +1759,7 @@ static int resident_blocks(const void* fn, int nthreads, size_t smem) {
 
 template <int S, int P, bool CN, int LB, bool RT>
 static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
-  const int nouter = (axis == 0 ? a.L.n1 : a.L.n0) - 2;
+  const int nouter = a.on ? a.on : (axis == 0 ? a.L.n1 : a.L.n0) - 2;
   const int nlines = (RT ? a.L.n1 : a.L.n2) - 2;
   const int ntx = (nlines + LB - 1) / LB;
   dim3 block(LB, P);
@@ -1752,7 +1775,7 @@ static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
 template <int S, int P, bool CN>
 static void launch_col(const SweepArgs& a, int axis, cudaStream_t st) {
   constexpr int LB = 16;
-  const int nouter = axis == 1 && a.on ? a.on : (axis == 0 ? a.L.n1 : a.L.n0) - 2;
+  const int nouter = a.on ? a.on : (axis == 0 ? a.L.n1 : a.L.n0) - 2;
   const int ntx = (a.L.n2 - 2 + LB - 1) / LB;
   const size_t smem =
       sizeof(double) * (kTabDoubles + P * (P + 2) + 4 * LB * P + kFlowHdr + flow_stage_n(a));
@@ -2449,62 +2472,129 @@ extern "C" PBG_API int pbg_get_profile(double axis_ms[3], int64_t launches[3]) {
   return PBG_OK;
 }
 
-extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
-                                 int32_t* diverged_step, int32_t* result_slot,
-                                 float* device_ms, void* stream) {
+// A prepared march (pbg_plan_*): the per-axis tables, segment descriptors and deduplicated
+// general-segment factors of one (problem codes, variant, dt, alpha) are built once -- the
+// reference's Stepper.__init__ (schemes.py:188-262) -- and every run only launches the step
+// kernels, with one host synchronisation at its end (reading the divergence flag).
+struct pbg_plan {
+  pbg_march_desc d;  // codes / rho pointers stay the caller's
+  Plan plan;
+  SweepArgs ax[3];
+  AxisAux aux[3];
+  bool extra = false;  // ADI / explicit Euler: march_extra per run
+  int* dflag = nullptr;
+  int* hflag = nullptr;  // pinned
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+namespace pbg {
+__global__ void k_set_int(int* p, int v) { *p = v; }
+static std::mutex g_prof_mu;
+
+static void plan_free(pbg_plan* p, cudaStream_t st) {
+  for (int q = 0; q < 3; ++q) release_axis(p->aux[q], st);
+  if (p->dflag) cudaFreeAsync(p->dflag, st);
+  if (p->hflag) cudaFreeHost(p->hflag);
+  if (p->e0) cudaEventDestroy(p->e0);
+  if (p->e1) cudaEventDestroy(p->e1);
+  delete p;
+}
+}  // namespace pbg
+
+static int check_desc(const pbg_march_desc* d) {
   if (!d) return fail(PBG_E_INVALID, "null descriptor");
   int rc = validate_grid(&d->grid);
   if (rc) return rc;
-  if (!(d->dt > 0) || !(d->alpha > 0) || d->nsteps < 1)
-    return fail(PBG_E_INVALID, "dt, alpha must be positive and nsteps >= 1");
-  if (!d->codes || !d->rho || !d->initial || !d->work[0] || !d->work[1])
-    return fail(PBG_E_INVALID, "null device buffer");
-  keep_pool_memory();
-  if (d->variant == PBG_ADI1 || d->variant == PBG_ADI2 || d->variant == PBG_EULER)
-    return march_extra(d, steps_taken, diverged_step, result_slot, device_ms,
-                       (cudaStream_t)stream);
-  Plan plan;
-  if (!plan_for(d->variant, plan))
-    return fail(PBG_E_UNSUPPORTED, "variant not supported by the device march");
-  cudaStream_t st = (cudaStream_t)stream;
-  SweepArgs ax[3];
-  march_axes(d, plan, ax);
-  const pbg_grid* g = &d->grid;
+  if (!(d->dt > 0) || !(d->alpha > 0))
+    return fail(PBG_E_INVALID, "dt, alpha must be positive");
+  if (!d->codes || !d->rho) return fail(PBG_E_INVALID, "null device buffer");
+  return PBG_OK;
+}
 
-  AxisAux aux[3];
-  for (int axis = 0; axis < 3; ++axis) {
-    rc = prepare_axis(ax[axis], axis, d->codes, aux[axis], st);
-    if (rc) {
-      for (int q = 0; q < 3; ++q) release_axis(aux[q], st);
-      return rc;
-    }
+extern "C" PBG_API int pbg_plan_create(const pbg_march_desc* d, pbg_plan** out, void* stream) {
+  if (!out) return fail(PBG_E_INVALID, "null output handle");
+  *out = nullptr;
+  int rc = check_desc(d);
+  if (rc) return rc;
+  if (!d->work[0]) return fail(PBG_E_INVALID, "null device buffer");
+  keep_pool_memory();
+  cudaStream_t st = (cudaStream_t)stream;
+  pbg_plan* p = new pbg_plan();
+  p->d = *d;
+  auto bail = [&](int code) {
+    plan_free(p, st);
+    return code;
+  };
+  if (cudaMallocHost(&p->hflag, sizeof(int)) != cudaSuccess ||
+      cudaEventCreate(&p->e0) != cudaSuccess || cudaEventCreate(&p->e1) != cudaSuccess)
+    return bail(fail(PBG_E_CUDA, "plan allocation failed"));
+  if (d->variant == PBG_ADI1 || d->variant == PBG_ADI2 || d->variant == PBG_EULER) {
+    p->extra = true;
+    *out = p;
+    return PBG_OK;
   }
-  int* dflag = nullptr;
-  PBG_CUDA(cudaMallocAsync(&dflag, sizeof(int), st));
-  const int init = INT_MAX;
-  PBG_CUDA(cudaMemcpyAsync(dflag, &init, sizeof(init), cudaMemcpyHostToDevice, st));
-  if (d->check_divergence) {
-    k_faces_bad<<<148, 256, 0, st>>>(make_layout(g), d->work[0], d->divergence_threshold,
-                                     dflag);
+  if (!plan_for(d->variant, p->plan))
+    return bail(fail(PBG_E_UNSUPPORTED, "variant not supported by the device march"));
+  march_axes(d, p->plan, p->ax);
+  for (int axis = 0; axis < 3; ++axis) {
+    rc = prepare_axis(p->ax[axis], axis, d->codes, p->aux[axis], st);
+    if (rc) return bail(rc);
+  }
+  if (cudaMallocAsync(&p->dflag, sizeof(int), st) != cudaSuccess)
+    return bail(fail(PBG_E_CUDA, "plan allocation failed"));
+  if (cudaStreamSynchronize(st) != cudaSuccess)  // the plan may run on any stream
+    return bail(fail(PBG_E_CUDA, "plan setup failed"));
+  *out = p;
+  return PBG_OK;
+}
+
+extern "C" PBG_API int pbg_plan_destroy(pbg_plan* p, void* stream) {
+  if (p) plan_free(p, (cudaStream_t)stream);
+  return PBG_OK;
+}
+
+extern "C" PBG_API int pbg_plan_run(pbg_plan* p, const double* initial, double* work0,
+                                    double* work1, int32_t nsteps, int32_t check_divergence,
+                                    int32_t* steps_taken, int32_t* diverged_step,
+                                    int32_t* result_slot, float* device_ms, void* stream) {
+  if (!p) return fail(PBG_E_INVALID, "null plan");
+  if (!initial || !work0 || !work1) return fail(PBG_E_INVALID, "null device buffer");
+  if (nsteps < 1) return fail(PBG_E_INVALID, "nsteps must be >= 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->extra) {
+    pbg_march_desc d = p->d;
+    d.initial = initial;
+    d.work[0] = work0;
+    d.work[1] = work1;
+    d.nsteps = nsteps;
+    d.check_divergence = check_divergence;
+    return march_extra(&d, steps_taken, diverged_step, result_slot, device_ms, st);
+  }
+  const pbg_grid* g = &p->d.grid;
+  const Plan& plan = p->plan;
+  double* work[2] = {work0, work1};
+  int* dflag = p->dflag;
+  int rc = PBG_OK;
+  k_set_int<<<1, 1, 0, st>>>(dflag, INT_MAX);
+  PBG_LAUNCH_CHECK("k_set_int");
+  if (check_divergence) {
+    k_faces_bad<<<148, 256, 0, st>>>(make_layout(g), work0, p->d.divergence_threshold, dflag);
     PBG_LAUNCH_CHECK("k_faces_bad");
   }
 
   int st_idx = -1;
-  if (d->initial == d->work[0]) st_idx = 0;
-  else if (d->initial == d->work[1]) st_idx = 1;
+  if (initial == work0) st_idx = 0;
+  else if (initial == work1) st_idx = 1;
   const int st0 = st_idx;
-  // LOD steps whose axis-2 sweep runs the row-warp kernel write it in place over the axis-1
-  // output (its lines are staged whole before they are stored), so the step's state stays in
-  // one buffer; optionally the axis-1 and axis-2 sweeps alternate over plane chunks so that
-  // axis 2 reads the axis-1 output (and rewrites it) while it is still in L2.
-  const bool lod_rw = plan.family <= 1 && ax[2].rw;
+  // LOD steps whose axis-2 sweep runs the row-warp kernel may write it in place over the
+  // axis-1 output (its lines are staged whole before they are stored), so the step's state
+  // stays in one buffer; PBG_FUSE12 = plane chunk of an axis-1/axis-2 interleave (measured
+  // slower: launch tails).
+  const bool lod_rw = plan.family <= 1 && p->ax[2].rw;
   const int chunk = lod_rw ? env_int("PBG_FUSE12", 0) : 0;
   const bool inpl = lod_rw && (chunk > 0 || env_int("PBG_INPLACE2", 0) != 0);
   const int nplanes = g->n[0] - 2;
 
-  cudaEvent_t e0, e1;
-  PBG_CUDA(cudaEventCreate(&e0));
-  PBG_CUDA(cudaEventCreate(&e1));
   std::vector<cudaEvent_t> kev;  // per-launch events when profiling is on
   auto mark = [&]() {
     if (!g_profile) return;
@@ -2513,18 +2603,20 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
     cudaEventRecord(ev, st);
     kev.push_back(ev);
   };
-  PBG_CUDA(cudaEventRecord(e0, st));
-  for (int s = 1; s <= d->nsteps; ++s) {
-    const double* X = st_idx < 0 ? d->initial : d->work[st_idx];
+  PBG_CUDA(cudaEventRecord(p->e0, st));
+  for (int s = 1; s <= nsteps && !rc; ++s) {
+    const double* X = st_idx < 0 ? initial : work[st_idx];
     const int other = st_idx < 0 ? 0 : 1 - st_idx;
-    double* A = d->work[other];
-    double* Bf = st_idx < 0 ? d->work[1] : d->work[st_idx];
+    double* A = work[other];
+    double* Bf = st_idx < 0 ? work[1] : work[st_idx];
     SweepArgs as[3];
     for (int axis = 0; axis < 3; ++axis) {
       SweepArgs& a = as[axis];
-      a = ax[axis];
+      a = p->ax[axis];
+      a.bnd = work0;  // faces hold the Dirichlet data
       a.step = s;
-      a.div_step = d->check_divergence ? dflag : nullptr;
+      a.div_step = check_divergence ? dflag : nullptr;
+      a.check = (axis == 2) && check_divergence;
       if (plan.family <= 1) {
         a.src = axis == 0 ? X : (axis == 1 ? A : Bf);
         a.dst = axis == 0 ? A : (axis == 1 ? Bf : (inpl ? Bf : A));
@@ -2550,33 +2642,32 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
       }
       mark();
     }
-    if (rc) {
-      cudaFreeAsync(dflag, st);
-      for (int q = 0; q < 3; ++q) release_axis(aux[q], st);
-      return rc;
-    }
     st_idx = inpl ? (st_idx < 0 ? 1 : st_idx) : other;
   }
-  PBG_CUDA(cudaEventRecord(e1, st));
-  int dstep = INT_MAX;
-  PBG_CUDA(cudaMemcpyAsync(&dstep, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  PBG_CUDA(cudaFreeAsync(dflag, st));
-  for (int q = 0; q < 3; ++q) release_axis(aux[q], st);
+  if (rc) {
+    cudaStreamSynchronize(st);
+    for (auto ev : kev) cudaEventDestroy(ev);
+    return rc;
+  }
+  PBG_CUDA(cudaEventRecord(p->e1, st));
+  PBG_CUDA(cudaMemcpyAsync(p->hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
   PBG_CUDA(cudaStreamSynchronize(st));
+  const int dstep = *p->hflag;
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  for (size_t q = 0; q + 1 < kev.size(); q += 2) {
-    float kms = 0.f;
-    cudaEventElapsedTime(&kms, kev[q], kev[q + 1]);
-    const int axis = (int)((q / 2) % 3);
-    g_prof_ms[axis] += kms;
-    g_prof_n[axis] += 1;
+  cudaEventElapsedTime(&ms, p->e0, p->e1);
+  if (!kev.empty()) {
+    std::lock_guard<std::mutex> lock(g_prof_mu);  // marches may run on several host threads
+    for (size_t q = 0; q + 1 < kev.size(); q += 2) {
+      float kms = 0.f;
+      cudaEventElapsedTime(&kms, kev[q], kev[q + 1]);
+      const int axis = (int)((q / 2) % 3);
+      g_prof_ms[axis] += kms;
+      g_prof_n[axis] += 1;
+    }
   }
   for (auto ev : kev) cudaEventDestroy(ev);
-  int taken = d->nsteps;
-  if (d->check_divergence && dstep != INT_MAX) {
+  int taken = nsteps;
+  if (check_divergence && dstep != INT_MAX) {
     taken = dstep;
     if (diverged_step) *diverged_step = dstep;
   } else if (diverged_step) {
@@ -2591,6 +2682,22 @@ extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
   if (result_slot) *result_slot = slot;
   if (device_ms) *device_ms = ms;
   return PBG_OK;
+}
+
+extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,
+                                 int32_t* diverged_step, int32_t* result_slot,
+                                 float* device_ms, void* stream) {
+  int rc = check_desc(d);
+  if (rc) return rc;
+  if (d->nsteps < 1) return fail(PBG_E_INVALID, "nsteps must be >= 1");
+  if (!d->initial || !d->work[0] || !d->work[1]) return fail(PBG_E_INVALID, "null device buffer");
+  pbg_plan* p = nullptr;
+  rc = pbg_plan_create(d, &p, stream);
+  if (rc) return rc;
+  rc = pbg_plan_run(p, d->initial, d->work[0], d->work[1], d->nsteps, d->check_divergence,
+                    steps_taken, diverged_step, result_slot, device_ms, stream);
+  pbg_plan_destroy(p, stream);
+  return rc;
 }
 
 extern "C" PBG_API int pbg_sweep(const pbg_grid* g, const pbg_palette* pal,

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import enum
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -99,6 +100,50 @@ class DeviceProblem:
                                              nat.ptr(codes), nat.stream_ptr()))
         self.codes = codes
         self.bnd = problem.boundary._device()
+        self._plans = {}  # (variant, dt, alpha, literal, threshold) -> pbg_plan, LRU
+        self._lock = threading.Lock()  # config-5 batches march one problem from two threads
+
+    _MAX_PLANS = 4
+
+    def plan(self, variant, dt, alpha, aos_literal, threshold):
+        """Prepared march (pbg_plan_create: tables, descriptors, segment factors) for this
+        problem's codes, built once and reused by every march / step with the same
+        constants -- the reference's Stepper factors once (schemes.py:188-262)."""
+        key = (nat.VARIANT_IDS[variant], float(dt), float(alpha), bool(aos_literal),
+               float(threshold))
+        with self._lock:
+            return self._plan_locked(key, aos_literal)
+
+    def _plan_locked(self, key, aos_literal):
+        h = self._plans.pop(key, None)
+        if h is None:
+            d = nat.PbgMarchDesc()
+            d.grid = self.gs
+            d.pal = self.pal
+            d.variant = key[0]
+            d.aos_literal = 1 if aos_literal else 0
+            d.dt, d.alpha, d.divergence_threshold = key[1], key[2], key[4]
+            d.nsteps, d.check_divergence = 1, 1
+            d.codes = self.codes.data_ptr()
+            d.rho = self.rho.data_ptr()
+            d.initial = d.work[0] = d.work[1] = self.bnd.data_ptr()  # setup reads none
+            out = ctypes.c_void_p()
+            nat.check(nat.lib().pbg_plan_create(ctypes.byref(d), ctypes.byref(out),
+                                                nat.stream_ptr()))
+            h = out
+            while len(self._plans) >= self._MAX_PLANS:
+                old = self._plans.pop(next(iter(self._plans)))
+                nat.lib().pbg_plan_destroy(old, nat.stream_ptr())
+        self._plans[key] = h  # most recently used last
+        return h
+
+    def __del__(self):
+        try:
+            for h in self._plans.values():
+                nat.load_library().pbg_plan_destroy(h, None)
+            self._plans.clear()
+        except Exception:
+            pass
 
     def work_pair(self):
         """Two pitched buffers whose faces hold the Dirichlet data."""
@@ -128,30 +173,18 @@ def device_problem(problem) -> DeviceProblem:
 
 
 def _run_march(problem, variant, dt, alpha, nsteps, threshold, aos_literal, check_div,
-               initial_dev=None):
+               initial_dev=None, work=None):
     v = parse_variant(variant)
     dp = device_problem(problem)
-    w0, w1 = dp.work_pair()
+    w0, w1 = work if work is not None else dp.work_pair()
     init = initial_dev if initial_dev is not None else problem.initial._device()
-    d = nat.PbgMarchDesc()
-    d.grid = dp.gs
-    d.pal = dp.pal
-    d.variant = nat.VARIANT_IDS[v.value]
-    d.aos_literal = 1 if aos_literal else 0
-    d.dt = float(dt)
-    d.alpha = float(alpha)
-    d.divergence_threshold = float(threshold)
-    d.nsteps = int(nsteps)
-    d.check_divergence = 1 if check_div else 0
-    d.codes = dp.codes.data_ptr()
-    d.rho = dp.rho.data_ptr()
-    d.initial = init.data_ptr()
-    d.work[0] = w0.data_ptr()
-    d.work[1] = w1.data_ptr()
+    h = dp.plan(v.value, dt, alpha, aos_literal, threshold)
     taken, dstep, slot = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
     ms = ctypes.c_float()
-    nat.check(nat.lib().pbg_march(ctypes.byref(d), ctypes.byref(taken), ctypes.byref(dstep),
-                                  ctypes.byref(slot), ctypes.byref(ms), nat.stream_ptr()))
+    nat.check(nat.lib().pbg_plan_run(h, nat.ptr(init), nat.ptr(w0), nat.ptr(w1), int(nsteps),
+                                     1 if check_div else 0, ctypes.byref(taken),
+                                     ctypes.byref(dstep), ctypes.byref(slot), ctypes.byref(ms),
+                                     nat.stream_ptr()))
     final = w0 if slot.value == 0 else w1
     return final, taken.value, (dstep.value or None), ms.value / 1e3
 
@@ -200,7 +233,10 @@ def step(variant, state: ScalarField, problem, dt: float, alpha: float | None = 
 
 
 class Stepper:
-    """Per-march engine (schemes.py:185-380): device problem + variant constants."""
+    """Per-march engine (schemes.py:185-380): the device plan (tables, descriptors, segment
+    factors) is prepared once here, and each .step(u) only uploads u, launches one step and
+    downloads the result.  The region maps stay device resident (nothing is materialised on
+    the host)."""
 
     def __init__(self, problem, config: MarchConfig, aos_order=(0, 1, 2)):
         self.problem = problem
@@ -210,14 +246,23 @@ class Stepper:
         self.dt = config.dt
         self.alpha = _resolve_alpha(config.alpha, problem)
         self.dta = self.dt / self.alpha
+        if sorted(aos_order) != [0, 1, 2]:
+            raise ValueError("aos_order must be a permutation of (0, 1, 2)")
         self.aos_order = aos_order
         v = self.variant.value
         self.pm = 4.0 if (v.startswith("AOS") and config.aos_nonlinear == "literal") else 1.0
-        k2 = problem.region.kappa2.data
-        if v.startswith("AOS") and config.aos_nonlinear == "exact":
-            self.decay = np.exp(-4.0 * k2 * self.dta)
-        else:
-            self.decay = np.exp(-k2 * self.dta)
+        self._literal = config.aos_nonlinear == "literal"
+        self._dp = device_problem(problem)
+        self._dp.plan(v, self.dt, self.alpha, self._literal, float("inf"))
+        self._work = self._dp.work_pair()
+
+    @property
+    def decay(self):
+        """Per-node flow decay (schemes.py:212, 264-270); materialises kappa2 on the host."""
+        k2 = self.problem.region.kappa2.data
+        if self.variant.value.startswith("AOS") and self.config.aos_nonlinear == "exact":
+            return np.exp(-4.0 * k2 * self.dta)
+        return np.exp(-k2 * self.dta)
 
     def _nl(self, u, decay, pm=1.0):
         """Flow stage with the Dirichlet faces re-applied (schemes.py:280-283)."""
@@ -230,8 +275,10 @@ class Stepper:
 
     def step(self, u: np.ndarray) -> np.ndarray:
         f = ScalarField(self.grid, u)
-        return step(self.variant, f, self.problem, self.dt, self.alpha,
-                    self.config.aos_nonlinear).data
+        final, _, _, _ = _run_march(self.problem, self.variant, self.dt, self.alpha, 1,
+                                    float("inf"), self._literal, False,
+                                    initial_dev=f._device(), work=self._work)
+        return ScalarField._from_device(self.grid, final).data
 
 
 def nonlinear_step(w, kappa2, dt: float, alpha: float, premultiplier: float = 1.0,

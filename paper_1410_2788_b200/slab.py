@@ -47,43 +47,59 @@ def slab_ranges(n0: int, nranks: int):
     return out
 
 
+SETUP, HALO, STEP = 0, 1, 2  # exchange phases (include/pbg.h PBG_SLAB_*)
+
+
 def run_slabs(parts, exchange, nsteps: int, cn: bool):
     """Drive the partitions of this process through setup, `nsteps` steps and the final flag
     agreement.  `parts` are this process's partitions (all of them for LocalExchange, one
-    for GroupExchange); each exposes create-time `send`/`recv` buffers and the phase calls."""
-    exchange.gather(parts)  # static responses (computed at creation)
+    for GroupExchange); each exposes `send`/`recv` buffers, `phase(phase, chunk)` ->
+    (offset, count) of the exchanged part of send, `nchunks`, and the phase calls.  Phase A
+    runs chunk by chunk; each chunk's all-gather is issued as soon as the chunk is done, so
+    (with an asynchronous exchange) it overlaps phase A of the next chunk."""
+    exchange.gather(parts, *parts[0].phase(SETUP, 0))  # static responses (from creation)
     for p in parts:
         p.setup()
+    nc = parts[0].nchunks
     for _ in range(nsteps):
         if cn:
             for p in parts:
                 p.halo_pack()
-            exchange.gather(parts)
+            exchange.gather(parts, *parts[0].phase(HALO, 0))
             for p in parts:
                 p.halo_unpack()
-        for p in parts:
-            p.step_a()
-        exchange.gather(parts)
+        pending = []
+        for c in range(nc):
+            for p in parts:
+                p.step_a_chunk(c)
+            pending.append(exchange.gather(parts, *parts[0].phase(STEP, c), async_op=True))
+        for w in pending:
+            if w is not None:
+                w.wait()
         for p in parts:
             p.step_b()
     for p in parts:
         p.flag_pack()
-    exchange.gather(parts)
+    exchange.gather(parts, *parts[0].phase(STEP, 0))
     return [p.finish() for p in parts]
 
 
 class LocalExchange:
-    """All partitions live in this process and share one `recv` buffer."""
+    """All partitions live in this process and share one `recv` buffer (device copies on
+    the current stream, in order)."""
 
-    def gather(self, parts):
-        E = parts[0].send.numel()
+    def gather(self, parts, offset, count, async_op=False):
         recv = parts[0].recv
+        base = len(parts) * offset
         for r, p in enumerate(parts):
-            recv[r * E:(r + 1) * E].copy_(p.send)
+            recv[base + r * count:base + (r + 1) * count].copy_(p.send[offset:offset + count])
+        return None
 
 
 class GroupExchange:
-    """One partition per process; all-gather over a torch.distributed group."""
+    """One partition per process; all-gather over a torch.distributed group (NCCL: runs on
+    the communicator's stream, ordered after the work already queued on the current stream,
+    so an async gather overlaps the kernels launched after it)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -92,13 +108,16 @@ class GroupExchange:
         self.group = group
         self.nccl = dist.get_backend(group) == "nccl"
 
-    def gather(self, parts):
+    def gather(self, parts, offset, count, async_op=False):
         (p,) = parts
+        n = self.dist.get_world_size(self.group)
+        dst = p.recv[n * offset:n * (offset + count)]
+        src = p.send[offset:offset + count]
         if self.nccl:
-            self.dist.all_gather_into_tensor(p.recv, p.send, group=self.group)
-        else:
-            n = p.recv.numel() // p.send.numel()
-            self.dist.all_gather(list(p.recv.view(n, -1).unbind(0)), p.send, group=self.group)
+            return self.dist.all_gather_into_tensor(dst, src, group=self.group,
+                                                    async_op=async_op)
+        return self.dist.all_gather(list(dst.view(n, -1).unbind(0)), src, group=self.group,
+                                    async_op=async_op)
 
 
 class DeviceSlab:
@@ -176,6 +195,19 @@ class DeviceSlab:
 
     def step_a(self):
         self._call(self.lib.pbg_slab_step_a)
+
+    def step_a_chunk(self, c):
+        nat.check(self.lib.pbg_slab_step_a_chunk(self.handle, int(c), nat.stream_ptr()))
+
+    @property
+    def nchunks(self):
+        return int(self.lib.pbg_slab_nchunks(self.handle))
+
+    def phase(self, phase, chunk):
+        off, cnt = ctypes.c_int64(), ctypes.c_int64()
+        nat.check(self.lib.pbg_slab_phase(self.handle, int(phase), int(chunk),
+                                          ctypes.byref(off), ctypes.byref(cnt)))
+        return int(off.value), int(cnt.value)
 
     def step_b(self):
         self._call(self.lib.pbg_slab_step_b)

@@ -44,6 +44,14 @@ def interface_solve(G, Q, rank, nranks):
 
 
 class NumpySlab:
+    nchunks = 1
+
+    def phase(self, phase, chunk):  # one exchange block for every phase
+        return 0, self.send.numel()
+
+    def step_a_chunk(self, c):
+        self.step_a()
+
     def __init__(self, p: O.OProblem, variant, dt, T, rank, nranks, first, stop, recv=None,
                  threshold=1e12):
         fam, mult, self.cn, _ = O.PLANS[variant]
