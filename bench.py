@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--c5-streams", action="store_true",
+                    help="config 5: one march per protein on 8 streams instead of batched")
     ap.add_argument("--mode", default=None, choices=["slab", "replicas"],
                     help="slab-sharded single grid (default for N > 1; with N = 1 it runs "
                          "the slab path as one NCCL rank) or independent replicas")
@@ -263,6 +265,27 @@ def cpu_oracle_rate(p, dp, c, nplanes=65, steps=1):
     return nint * steps / wall, nint, wall
 
 
+def c3_target(args):
+    """north_star's single-GPU target, measured in the same run: the full LODIE2 step at
+    257^3 (config 3) against the 60% mark of the 48 B/node roofline (8 TB/s nominal and the
+    measured copy bandwidth)."""
+    import torch
+
+    c, p, _ = build_problem("c3")
+    nint = (c.n - 2) ** 3
+    d, dp, keep = march_desc(p, c, args.steps)
+    run_march(d, max(3, args.warmup))
+    torch.cuda.synchronize()
+    ms = run_march(d, args.steps) / args.steps
+    peak, kind = peaks()
+    step_gbs = BYTES_LOD * nint / (ms / 1e3) / 1e9
+    return {"c3_257_lodie2": {"ms_per_step": ms, "updates_per_s": nint / (ms / 1e3),
+                              "step_GBps_48B": step_gbs, "frac_of_8TBs": step_gbs / 8000.0,
+                              "frac_of_measured": step_gbs / peak,
+                              "target_ms_60pct_of_8TBs": BYTES_LOD * nint / (0.6 * 8e12) * 1e3,
+                              "met": step_gbs / 8000.0 >= 0.6}}
+
+
 def profiled_kernels(d, nsteps):
     from paper_1410_2788_b200 import _native as nat
 
@@ -339,6 +362,9 @@ def main():
     achieved = BYTES_SWEEP * nint / (per_ms[dom] / 1e3) / 1e9
     step_gbs = BYTES_LOD * nint / (ms_max / args.steps / 1e3) / 1e9
 
+    targets = None
+    if rank == 0 and world == 1 and args.config == "c4":
+        targets = c3_target(args)
     e2e = None
     if not args.no_e2e:
         wall, h2d, d2h, ok = e2e_measure(p, c, dp, args.steps)
@@ -389,7 +415,8 @@ def main():
                          "step_GBps_48B": step_gbs, "step_frac": step_gbs / peak},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 3 * args.steps + 1,
+            "targets": targets,
+            "gpu_launches": 3 * args.steps + 2,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -416,6 +443,8 @@ def c5_main(args, world, rank, local, dist):
     torch.cuda.synchronize()
     t_asm = time.perf_counter() - t0
     variants = ("AOSIE1", "LODIE2")
+    if not args.c5_streams:
+        return c5_batched(args, world, rank, local, dist, sizes, mine, probs, t_asm, variants)
     jobs = [((i, v), probs[i][1], pb.MarchConfig(dt=probs[i][0].dt, T=probs[i][0].dt * args.steps,
                                                  variant=v)) for i in mine for v in variants]
     warm = [((k, v), p, pb.MarchConfig(dt=cfg.dt, T=cfg.dt * max(3, args.warmup), variant=v))
@@ -451,6 +480,53 @@ def c5_main(args, world, rank, local, dist):
     wall_max = float(t.item())
     n = probs[mine[0]][0].n
     total = len(sizes) * len(variants) * args.steps * (n - 2) ** 3
+    e2e = None
+    if not args.no_e2e:  # the public call from host inputs (atoms) to host results (fields)
+        from paper_1410_2788_b200.batch import run_config5
+
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        items = run_config5(rank, world, count=len(sizes), nsteps=args.steps, streams=8,
+                            group=None)
+        torch.cuda.synchronize()
+        tw = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        bad = [(it.index, it.variant) for it in items if it.diverged]
+        if bad:
+            raise RuntimeError(f"config 5 e2e marches diverged: {bad[:4]}")
+        atoms_bytes = sum(sizes[i] for i in mine) * 5 * 8
+        e2e = {"value": total / float(tw.item()), "unit": "grid-point updates/s",
+               "h2d_bytes_per_step": int(atoms_bytes / args.steps),
+               "d2h_bytes_per_step": int(len(mine) * len(variants) * n ** 3 * 8 / args.steps),
+               "note": "batch.run_config5: assembly from host atom lists, plan setup, the "
+                       "marches and the final fields downloaded (max over ranks)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import pbs_oracle as O
+        from paper_1410_2788_b200.configs import batch_config, cubic_box, kappa_bar, synthetic_atoms
+
+        cb = batch_config(0, sizes[0])
+        atoms = synthetic_atoms(cb.n_atoms, cb.ball_radius, cb.seed)
+        lo, hi = cubic_box(atoms, cb.n, cb.h)
+        op = O.protein_on_grid(O.grid_from_bounds(lo, hi, cb.h), atoms, cb.eps_m, cb.eps_s,
+                               kappa_bar(cb.ionic_strength))
+        wall = 0.0
+        ksteps = 5
+        for v in variants:
+            st = O.OStepper(op, v, cb.dt)
+            u = op.initial.copy()
+            t0 = time.perf_counter()
+            for _ in range(ksteps):
+                u = st.step(u)
+                np.max(np.abs(u))
+            wall += time.perf_counter() - t0
+        cpu = {"value": len(variants) * ksteps * (n - 2) ** 3 / wall,
+               "unit": "grid-point updates/s", "cores": 1, "kind": "port",
+               "sample": f"protein 0 ({sizes[0]} atoms, {n}^3), {ksteps} AOSIE1 + {ksteps} "
+                         "LODIE2 steps, numpy oracle port of pbsplit Stepper, one core"}
     if rank == 0:
         line = {
             "metric": "LOD/AOS grid-point updates/s (fp64), config-5 batch",
@@ -466,13 +542,142 @@ def c5_main(args, world, rank, local, dist):
                        "timing": "CUDA events: start on the default stream, joined from all 8 "
                                  "march streams at the end (per-march setup inside), max over "
                                  "ranks", "host_wall_s": round(host_wall, 4)},
-            "roofline": None, "cpu_baseline": None, "e2e": None,
-            "gpu_launches": sum(3 * r.steps_taken for r in reps.values()) * world,
+            "roofline": {"bound": "hbm", "achieved": None, "peak": peaks()[0], "unit": "GB/s",
+                         "frac": None, "traffic": None,
+                         "note": "97^3 fields (7 MB) are L2-resident: no HBM roofline "
+                                 "(SURVEY.md §8d caveat); step bytes "
+                                 f"{(48 + 64) / 2 * total / wall_max / 1e9:.0f} GB/s "
+                                 "equivalent (48 B LOD, 64 B AOS per node)"},
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": sum(3 * r.steps_taken + 2 for r in reps.values()) * world,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def c5_batched(args, world, rank, local, dist, sizes, mine, probs, t_asm, variants):
+    """Config 5 with batched launches: the rank's proteins stacked into one BatchMarch, one
+    launch per sweep for all of them; AOSIE1 then LODIE2, each `steps`
+    steps, timed with CUDA events on the launching stream."""
+    import torch
+
+    import paper_1410_2788_b200 as pb
+    from paper_1410_2788_b200.batch import BatchMarch
+
+    bm = BatchMarch([probs[i][1] for i in mine])
+    dt = probs[mine[0]][0].dt
+    for v in variants:  # warm-up (plans prepared here, as the reference's Stepper setup)
+        bm.march(pb.MarchConfig(dt=dt, T=dt * max(3, args.warmup), variant=v), keep_fields=False)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    per_variant = {}
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for v in variants:
+            reps, secs = bm.march(pb.MarchConfig(dt=dt, T=dt * args.steps, variant=v),
+                                  keep_fields=False)
+            per_variant[v] = secs
+            bad = [i for i, r in zip(mine, reps) if r.diverged or r.steps_taken != args.steps]
+            if bad:
+                raise RuntimeError(f"config 5 {v} marches diverged: {bad[:4]}")
+        ev1.record()
+        torch.cuda.synchronize()
+    wall = ev0.elapsed_time(ev1) / 1e3
+    if dist:
+        dist.barrier()
+    t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    wall_max = float(t.item())
+    n = probs[mine[0]][0].n
+    total = len(sizes) * len(variants) * args.steps * (n - 2) ** 3
+    mine_nodes = len(mine) * (n - 2) ** 3
+    e2e = None
+    if not args.no_e2e:  # the public call from host inputs (atoms) to host results (fields)
+        from paper_1410_2788_b200.batch import run_config5
+
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        items = run_config5(rank, world, count=len(sizes), nsteps=args.steps)
+        torch.cuda.synchronize()
+        tw = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        if any(it.diverged for it in items):
+            raise RuntimeError("config 5 e2e marches diverged")
+        atoms_bytes = sum(sizes[i] for i in mine) * 5 * 8
+        e2e = {"value": total / float(tw.item()), "unit": "grid-point updates/s",
+               "h2d_bytes_per_step": int(atoms_bytes / args.steps),
+               "d2h_bytes_per_step": int(len(mine) * len(variants) * n ** 3 * 8 / args.steps),
+               "note": "batch.run_config5: assembly from host atom lists, batched plan setup, "
+                       "the marches, final fields downloaded (max over ranks)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = c5_cpu_baseline(sizes, n, variants)
+    peak, kind = peaks()
+    aos_s, lod_s = per_variant["AOSIE1"], per_variant["LODIE2"]
+    lod_gbs = 48 * mine_nodes * args.steps / lod_s / 1e9
+    aos_gbs = 64 * mine_nodes * args.steps / aos_s / 1e9
+    if rank == 0:
+        line = {
+            "metric": "LOD/AOS grid-point updates/s (fp64), config-5 batch",
+            "value": total / wall_max, "unit": "grid-point updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": wall_max / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, configs.py)",
+            "config": {"workload": "c5-batch64-97", "proteins": len(sizes), "grid": [n] * 3,
+                       "variants": list(variants), "dt": 0.5,
+                       "parallelism": f"proteins round-robin over {world} rank(s); each "
+                                      "rank's proteins in one batched march (one launch per "
+                                      "sweep)", "assembly_s": round(t_asm, 3),
+                       "per_variant_ms_per_step": {v: per_variant[v] / args.steps * 1e3
+                                                   for v in variants},
+                       "l2": f"{len(mine)} x 7.3 MB fields, batch {len(mine) * 7.3:.0f} MB "
+                             "per field > L2"},
+            "roofline": {"bound": "hbm", "achieved": lod_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": lod_gbs / peak, "traffic": None, "peak_kind": kind,
+                         "kernel": "whole batched LODIE2 step (48 B/node)",
+                         "aos_step_GBps_64B": aos_gbs, "aos_frac": aos_gbs / peak},
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": (len(variants) * (3 * args.steps + 1 + len(mine))) * world,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def c5_cpu_baseline(sizes, n, variants):
+    from oracle import pbs_oracle as O
+    from paper_1410_2788_b200.configs import batch_config, cubic_box, kappa_bar, synthetic_atoms
+
+    cb = batch_config(0, sizes[0])
+    atoms = synthetic_atoms(cb.n_atoms, cb.ball_radius, cb.seed)
+    lo, hi = cubic_box(atoms, cb.n, cb.h)
+    op = O.protein_on_grid(O.grid_from_bounds(lo, hi, cb.h), atoms, cb.eps_m, cb.eps_s,
+                           kappa_bar(cb.ionic_strength))
+    wall = 0.0
+    ksteps = 5
+    for v in variants:
+        st = O.OStepper(op, v, cb.dt)
+        u = op.initial.copy()
+        t0 = time.perf_counter()
+        for _ in range(ksteps):
+            u = st.step(u)
+            np.max(np.abs(u))
+        wall += time.perf_counter() - t0
+    return {"value": len(variants) * ksteps * (n - 2) ** 3 / wall,
+            "unit": "grid-point updates/s", "cores": 1, "kind": "port",
+            "sample": f"protein 0 ({sizes[0]} atoms, {n}^3), {ksteps} AOSIE1 + {ksteps} "
+                      "LODIE2 steps, numpy oracle port of pbsplit Stepper, one core"}
 
 
 def slab_main(args, c, p, t_asm, world, rank, local, dist):

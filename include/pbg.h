@@ -180,6 +180,20 @@ PBG_API int pbg_plan_run(pbg_plan* p, const double* initial, double* work0, doub
                          void* stream);
 PBG_API int pbg_plan_destroy(pbg_plan* p, void* stream);
 
+/* Batched plans (config 5: many independent grids of one shape; SURVEY.md §8e "batched into
+ * one launch per sweep"): d->grid describes ONE grid; codes, rho, initial and work[] hold
+ * nbatch such grids batch_stride elements apart (batch_stride >= the pitched grid size and a
+ * multiple of the pitch); all grids share d->pal.  Every sweep is one launch over the lines
+ * of all grids; divergence is tracked per grid (a grid that stops is skipped by the later
+ * steps).  steps_taken / diverged_step / result_slot are arrays of nbatch.  Splitting
+ * schemes only.  pbg_plan_create == create_batch with nbatch 1. */
+PBG_API int pbg_plan_create_batch(const pbg_march_desc* d, int32_t nbatch,
+                                  int64_t batch_stride, pbg_plan** out, void* stream);
+PBG_API int pbg_plan_run_batch(pbg_plan* p, const double* initial, double* work0,
+                               double* work1, int32_t nsteps, int32_t check_divergence,
+                               int32_t* steps_taken, int32_t* diverged_step,
+                               int32_t* result_slot, float* device_ms, void* stream);
+
 /* Per-sweep-kernel timing (CUDA events around every launch inside pbg_march, on the
  * launching stream).  pbg_set_profiling(1) enables and resets the accumulators;
  * pbg_get_profile returns the summed milliseconds and launch counts per sweep axis. */

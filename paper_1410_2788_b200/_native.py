@@ -107,6 +107,11 @@ _SIGS = {
     "pbg_plan_run": ([c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, _P(c_int32),
                       _P(c_int32), _P(c_int32), _P(ctypes.c_float), c_void_p], ctypes.c_int),
     "pbg_plan_destroy": ([c_void_p, c_void_p], ctypes.c_int),
+    "pbg_plan_create_batch": ([_P(PbgMarchDesc), c_int32, c_int64, _P(c_void_p), c_void_p],
+                              ctypes.c_int),
+    "pbg_plan_run_batch": ([c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32,
+                            _P(c_int32), _P(c_int32), _P(c_int32), _P(ctypes.c_float),
+                            c_void_p], ctypes.c_int),
     "pbg_slab_exchange_elems": ([_P(PbgGrid)], c_int64),
     "pbg_slab_nchunks": ([c_void_p], c_int32),
     "pbg_slab_phase": ([c_void_p, c_int32, c_int32, _P(c_int64), _P(c_int64)], ctypes.c_int),

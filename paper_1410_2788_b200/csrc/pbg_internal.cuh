@@ -18,6 +18,10 @@ struct Layout {
   int n0, n1, n2;
   long long pitch;
   long long s0;
+  // Batched marches (config 5): nb grids of this shape, bs elements apart in every buffer
+  // (nb = 1, bs = 0 for one grid).  at() addresses grid 0; kernels add b * bs.
+  int nb;
+  long long bs;
   __host__ __device__ __forceinline__ long long at(int i, int j, int k) const {
     return (long long)i * s0 + (long long)j * pitch + k + kOff;
   }
@@ -47,6 +51,8 @@ inline Layout make_layout(const pbg_grid* g) {
   L.n2 = g->n[2];
   L.pitch = g->pitch;
   L.s0 = (long long)g->n[1] * g->pitch;
+  L.nb = 1;
+  L.bs = 0;
   return L;
 }
 

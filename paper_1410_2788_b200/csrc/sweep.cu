@@ -414,6 +414,7 @@ struct TileShape {
 
 // Where a tile sits: tile (tx, ty) of a launch with nty outer indices.
 struct TileGeo {
+  int b;        // grid of a batched march (0 otherwise); base includes b * L.bs
   int c0;       // first line of the tile (k for column tiles, j for row tiles)
   int outer;    // outer index (j for axis 0, i for axes 1 and 2)
   int ncols;    // active lines
@@ -429,9 +430,10 @@ __device__ __forceinline__ long long ends_index(const SweepArgs& a, const TileGe
 
 template <int LB, bool RT>
 __device__ __forceinline__ TileGeo tile_geo(const SweepArgs& a, int axis, int tx, int ty,
-                                            int nty) {
+                                            int nty, int b = 0) {
   const Layout& L = a.L;
   TileGeo g;
+  g.b = b;
   g.c0 = 1 + tx * LB;
   // Row tiles walk the planes in reverse: the axis-1 sweep before them wrote the last planes
   // last, so those are still in L2 when this launch starts.
@@ -448,6 +450,7 @@ __device__ __forceinline__ TileGeo tile_geo(const SweepArgs& a, int axis, int tx
     g.base = L.at(g.outer, 0, g.c0);
     g.stride = (int)L.pitch;
   }
+  g.base += (long long)b * L.bs;
   return g;
 }
 
@@ -465,7 +468,8 @@ __device__ __forceinline__ void stage_tile(const SweepArgs& a, const TileGeo& g,
   const double* gy_all = needY == 1 ? a.src : a.acc;
   if (D)
     cp_async16(D + 2 * tid,
-               a.desc + 2 * (((long long)(g.outer - 1) * kSegS + seg) * K + (g.c0 - 1 + lane)));
+               a.desc + g.b * a.dstride +
+                   2 * (((long long)(g.outer - 1) * kSegS + seg) * K + (g.c0 - 1 + lane)));
   if (RT) {
     // rows 1..m+1 of each line in 16-byte chunks (row 1 is 256-byte aligned), row 0 alone
     const int nch = (m + 1) / 2;  // full chunks; an odd last row goes alone
@@ -763,7 +767,7 @@ __device__ __forceinline__ void tile_body(const SweepArgs& a, const TileGeo& g, 
       }
     }
     if (a.check) {
-      if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicMin(a.div_step, a.step);
+      if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicMin(a.div_step + g.b, a.step);
     }
   }
 }
@@ -909,7 +913,7 @@ __device__ __forceinline__ void col_body(const SweepArgs& a, const TileGeo& g, d
       bad |= is_bad(x, a.thr);
     }
   }
-  if (a.check && bad) atomicMin(a.div_step, a.step);
+  if (a.check && bad) atomicMin(a.div_step + g.b, a.step);
 }
 
 // Stage the block's tables (uniform-segment LU tables, clean-line inverse, flow palette and
@@ -927,7 +931,8 @@ __device__ __forceinline__ void stage_tables(const SweepArgs& a, double* T, doub
 template <int kSegS>
 __device__ __forceinline__ const unsigned long long* col_desc(const SweepArgs& a,
                                                               const TileGeo& g) {
-  return a.desc + 2 * (((long long)(g.outer - 1) * kSegS + threadIdx.y) * (a.L.n2 - 2) +
+  return a.desc + g.b * a.dstride +
+         2 * (((long long)(g.outer - 1) * kSegS + threadIdx.y) * (a.L.n2 - 2) +
                        (g.c0 - 1 + threadIdx.x));
 }
 
@@ -941,9 +946,9 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
     k_sweep_col(const SweepArgs a, const int axis) {
   extern __shared__ double sm[];
   constexpr int NT = LB * kSegS;
-  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
+  const int dstep = a.div_step ? *((volatile int*)(a.div_step + blockIdx.z)) : INT_MAX;
   const int tid = threadIdx.y * LB + threadIdx.x;
-  const TileGeo g = tile_geo<LB, false>(a, axis, blockIdx.x, blockIdx.y, gridDim.y);
+  const TileGeo g = tile_geo<LB, false>(a, axis, blockIdx.x, blockIdx.y, gridDim.y, blockIdx.z);
   const int m = a.m, i0 = threadIdx.y * S;
   const bool act = threadIdx.x < g.ncols;
   const int st = g.stride;
@@ -1014,13 +1019,15 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
   if (uses_flow(a.pro, a.epi))
     for (int c = tid; c < a.fpoly_n / 2; c += NT) cp_async16(FP + kFlowHdr + 2 * c, a.fpoly + 2 * c);
   asm volatile("cp.async.commit_group;\n" ::);
-  if (dstep < a.step) {  // an earlier step diverged: nothing more to compute
+  if (a.L.nb == 1 && dstep < a.step) {  // an earlier step diverged: nothing more to compute
     cp_async_wait_all();
     return;
   }
-  const int ntiles = ntx * nty;
+  const int per = ntx * nty, ntiles = per * a.L.nb;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const TileGeo g = tile_geo<LB, RT>(a, axis, tile % ntx, tile / ntx, nty);
+    const int b = tile / per, tl = tile - b * per;
+    if (a.L.nb > 1 && a.div_step && a.div_step[b] < a.step) continue;  // grid b stopped
+    const TileGeo g = tile_geo<LB, RT>(a, axis, tl % ntx, tl / ntx, nty, b);
     stage_tile<S, kSegS, LB, RT>(a, g, W, Yt, D, needY);
     asm volatile("cp.async.commit_group;\n" ::);
     cp_async_wait_all();
@@ -1029,6 +1036,7 @@ __global__ void __launch_bounds__(LB * kSegS, LB * kSegS <= 128 ? 6 : (LB * kSeg
     tile_body<S, kSegS, CN, LB, RT>(a, g, T, Mi, W, Yt, X, D, FP, bfold);
     __syncthreads();  // the tile buffers are restaged by the next iteration
   }
+  cp_async_wait_all();  // a block whose tiles all belonged to stopped grids
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1146,60 +1154,78 @@ __device__ __forceinline__ void rw_solve(const SweepArgs& a, double (&r)[S],
 // Epilogue + coalesced store of rows 1..m of the warp's lines from the line buffer (at(p) =
 // row p): the G lanes of a line take consecutive rows (G * 8 = 128- or 256-byte runs), each
 // lane S of them; an idle sub-warp (odd line count) joins the shuffles but stores nothing.
+// Divergence test of the row-warp store pass: max|x| and a NaN/inf sentinel (x*0 is NaN
+// exactly for non-finite x), 2 fp64 operations per node instead of a compare-and-or; the
+// decision (non-finite, or max|x| above the threshold, schemes.py:417-421) is taken once per
+// thread at the end.
+struct DivAcc {
+  double mx = 0.0, nz = 0.0;
+  __device__ __forceinline__ void add(double x) {
+    mx = fmax(mx, fabs(x));
+    nz = fma(x, 0.0, nz);
+  }
+  __device__ __forceinline__ bool bad(double thr) const {
+    return !(nz == 0.0) || !(mx <= fmin(thr, 1.7976931348623157e308));
+  }
+};
+
+// Epilogue + coalesced store of rows 1..m of the warp's lines from the line buffer (at(p) =
+// row p): the G lanes of a line take consecutive rows (G * 8 = 128- or 256-byte runs), each
+// lane S of them; an idle sub-warp (odd line count) stores nothing.  Row-warp lines have
+// m + 1 = G*S rows, so only the last lane's last row (the far face) is skipped.  sbits: the
+// lane's solute bits in store order (row-warp descriptors, k_build_desc).
 template <int S, int G, typename At>
-__device__ __forceinline__ void rw_store(const SweepArgs& a, At at, bool valid, int seg, int sub,
+__device__ __forceinline__ void rw_store(const SweepArgs& a, At at, bool valid, int seg,
                                          uint32_t sbits, const double* FP, long long base,
-                                         bool& bad) {
-  constexpr unsigned FULL = 0xffffffffu;
-  const int m = a.m;
-  // epilogue + coalesced store of rows 1..m: the G lanes of a line take consecutive rows
-  // (G * 8 = 128- or 256-byte runs), each lane S of them; an idle half-warp (odd line
-  // count) joins the shuffles but stores nothing
-  {
-    double* gdst = a.dst + base;
-    if (a.epi == EPI_FLOW) {  // the tiny-argument form for almost every node, solute bits
-                              // from the lane owning the row's segment
+                                         DivAcc& acc) {
+  double* gdst = a.dst + base;
+  auto inside = [&](int q) { return q < S - 1 || seg < G - 1; };  // p <= m = G*S - 1
+  if (a.epi == EPI_FLOW) {  // the tiny-argument form for almost every node
+    constexpr int S4 = S & ~3;
 #pragma unroll
-      for (int q = 0; q < S; q += 4) {
-        double x[4];
-        uint32_t sv[4];
+    for (int q = S4; q < S; ++q) {  // rows past the last group of four
+      double x = at(1 + seg + G * q);
+      x = flow_sm(a, FP, x, (sbits >> q) & 1u, 1.0);
+      if (valid && inside(q)) {
+        gdst[1 + seg + G * q] = x;
+        acc.add(x);
+      }
+    }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int p = 1 + seg + G * (q + u);
-          x[u] = at(p);
-          sv[u] = (__shfl_sync(FULL, sbits, sub * G + (p - 1) / S) >> ((p - 1) % S)) & 1u;
-        }
-        flow_group(a, FP, x[0], x[1], x[2], x[3], sv[0], sv[1], sv[2], sv[3], 1.0);
+    for (int q = 0; q < S4; q += 4) {
+      double x[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int p = 1 + seg + G * (q + u);
-          if (valid && p <= m) {
-            gdst[p] = x[u];
-            bad |= is_bad(x[u], a.thr);
-          }
+      for (int u = 0; u < 4; ++u) x[u] = at(1 + seg + G * (q + u));
+      flow_group(a, FP, x[0], x[1], x[2], x[3], (sbits >> q) & 1u, (sbits >> (q + 1)) & 1u,
+                 (sbits >> (q + 2)) & 1u, (sbits >> (q + 3)) & 1u, 1.0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (valid && inside(q + u)) {
+          gdst[1 + seg + G * (q + u)] = x[u];
+          acc.add(x[u]);
         }
       }
-    } else if (a.epi == EPI_AOS2) {  // AOS: 0.25 * (accumulated branches + this branch),
-                                     // read and written in place, same rounding as tiles
-      const double* gy = a.acc + base;
+    }
+  } else if (a.epi == EPI_AOS2) {  // AOS: 0.25 * (accumulated branches + this branch),
+                                   // read and written in place, same rounding as tiles
+    const double* gy = a.acc + base;
 #pragma unroll
-      for (int q = 0; q < S; ++q) {
-        const int p = 1 + seg + G * q;
-        if (valid && p <= m) {
-          const double x = __dmul_rn(0.25, __dadd_rn(gy[p], at(p)));
-          gdst[p] = x;
-          if (a.check) bad |= is_bad(x, a.thr);
-        }
+    for (int q = 0; q < S; ++q) {
+      const int p = 1 + seg + G * q;
+      if (valid && inside(q)) {
+        const double x = __dmul_rn(0.25, __dadd_rn(gy[p], at(p)));
+        gdst[p] = x;
+        if (a.check) acc.add(x);
       }
-    } else {
+    }
+  } else {
 #pragma unroll
-      for (int q = 0; q < S; ++q) {
-        const int p = 1 + seg + G * q;
-        if (valid && p <= m) {
-          const double x = at(p);
-          gdst[p] = x;
-          if (a.check) bad |= is_bad(x, a.thr);
-        }
+    for (int q = 0; q < S; ++q) {
+      const int p = 1 + seg + G * q;
+      if (valid && inside(q)) {
+        const double x = at(p);
+        gdst[p] = x;
+        if (a.check) acc.add(x);
       }
     }
   }
@@ -1228,20 +1254,24 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
   asm volatile("cp.async.commit_group;\n" ::);
   cp_async_wait_all();
   __syncthreads();
-  if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
+  if (a.L.nb == 1 && dstep < a.step) return;  // an earlier step diverged: nothing more to compute
 
   const Layout& L = a.L;
   const int m = a.m, K = L.n1 - 2, i0 = seg * S;
   const int itop = a.on ? a.o0 + a.on : L.n0 - 2;  // planes itop, itop-1, ... (reverse)
   double* W = Wb + warp * RW::WD + sub * RW::LW;          // this lane's line
   double* sR = Wb + warp * RW::WD + NL * RW::LW + sub * RW::RW;
-  bool bad = false;
+  DivAcc acc;
+  const int nlp = nlines / L.nb;  // lines per grid (batched marches: nb grids)
   for (int wl = blockIdx.x * kRWarps + warp; wl * NL < nlines; wl += gridDim.x * kRWarps) {
     const int line = wl * NL + sub;
-    const bool valid = NL == 1 || line < nlines;  // NL == 1: the loop condition
+    const int b = line < nlines ? line / nlp : 0, ln = line - b * nlp;
+    // NL == 1: the loop condition; batched: grids that stopped at an earlier step are skipped
+    const bool valid = (NL == 1 || line < nlines) &&
+                       (L.nb == 1 || !a.div_step || a.div_step[b] >= a.step);
     // planes in reverse (the axis-1 sweep before this one wrote the last planes last)
-    const int i = valid ? itop - line / K : 1, j = valid ? 1 + line % K : 1;
-    const long long base = L.at(i, j, 0);
+    const int i = valid ? itop - ln / K : 1, j = valid ? 1 + ln % K : 1;
+    const long long base = L.at(i, j, 0) + (long long)b * L.bs;
     unsigned long long amask = 0ull;
     uint32_t sbits = 0u, cmask = 0u;
     double bfold = 0.0;
@@ -1254,7 +1284,7 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
         cp_async16(W + RW::pos(2 * c + 1), gsrc + 2 * c);
       }
       const ulonglong2 dd = *reinterpret_cast<const ulonglong2*>(
-          a.desc + 2 * (line_desc(L, i, j) * G + seg));
+          a.desc + b * a.dstride + 2 * (line_desc(L, i, j) * G + seg));
       amask = dd.x;
       sbits = (uint32_t)dd.y;
       cmask = (uint32_t)(dd.y >> 32);
@@ -1265,7 +1295,8 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
     {  // the warp's next lines towards L2 while this one is solved (LODIE1 c4: 533 -> 498 us)
       const int nl = (wl + gridDim.x * kRWarps) * NL + sub;
       if (nl < nlines) {
-        const double* np = a.src + L.at(itop - nl / K, 1 + nl % K, 0) + 1;
+        const int nb2 = nl / nlp, nn = nl - nb2 * nlp;
+        const double* np = a.src + L.at(itop - nn / K, 1 + nn % K, 0) + (long long)nb2 * L.bs + 1;
         for (int c = seg; c < G * S / 16; c += G)  // 128-byte lines
           asm volatile("prefetch.global.L2 [%0];" ::"l"(np + 16 * c));
       }
@@ -1289,11 +1320,15 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
     }
     __syncwarp();
 
-    rw_store<S, G>(a, [&](int p) { return W[RW::pos(p)]; }, valid, seg, sub, sbits, FP, base,
-                   bad);
+    rw_store<S, G>(a, [&](int p) { return W[RW::pos(p)]; }, valid, seg, sbits, FP, base, acc);
+    if (L.nb > 1 && a.check) {  // batched: the line's own grid (lines of a warp may differ)
+      if (acc.bad(a.thr)) atomicMin(a.div_step + b, a.step);
+      acc = DivAcc();
+    }
     __syncwarp();  // the line buffers are restaged by the next lines
   }
-  if (a.check && __any_sync(FULL, bad) && lane == 0) atomicMin(a.div_step, a.step);
+  if (L.nb == 1 && a.check && __any_sync(FULL, acc.bad(a.thr)) && lane == 0)
+    atomicMin(a.div_step, a.step);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1386,7 +1421,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   cp_async_wait_all();
   __syncthreads();
-  if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
+  if (a.L.nb == 1 && dstep < a.step) return;  // an earlier step diverged: nothing more to compute
 
   const Layout& L = a.L;
   const int m = a.m, K = L.n1 - 2;
@@ -1396,6 +1431,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const int stride = gridDim.x * NW;
   const int wl0 = blockIdx.x * NW + warp;
   // lane 0: one tensor copy per valid line of warp-iteration wl into buffer b
+  const int nlp = nlines / L.nb;  // lines per grid (batched marches: nb grids)
+  const long long grid_lines = L.bs / L.pitch;  // tensor-map lines between grids
   auto issue = [&](int wl, int b) {
     int nv = 0;
 #pragma unroll
@@ -1405,8 +1442,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
     for (int l = 0; l < NL; ++l) {
       const int line = wl * NL + l;
       if (line < nlines) {
-        const int i = itop - line / K, j = 1 + line % K;
-        tma_load_3d(Lb + (warp * 2 + b) * WB + l * LD, &tm, 0, 0, i * L.n1 + j, bar + b);
+        const int gb = line / nlp, ln = line - gb * nlp;
+        const int i = itop - ln / K, j = 1 + ln % K;
+        tma_load_3d(Lb + (warp * 2 + b) * WB + l * LD, &tm, 0, 0,
+                    (int)(gb * grid_lines) + i * L.n1 + j, bar + b);
       }
     }
   };
@@ -1416,20 +1455,23 @@ __global__ void __launch_bounds__(NW * 32, 1)
   }
   // descriptor words and Dirichlet fold value of warp-iteration wl's line, loaded one
   // iteration ahead (their latency was the kernel's top stall when loaded in place)
-  auto line_of = [&](int wl, int& i, int& j) {
+  auto line_of = [&](int wl, int& i, int& j, int& gb) {
     const int line = wl * NL + sub;
     const bool v = NL == 1 || line < nlines;
-    i = v ? itop - line / K : 1;
-    j = v ? 1 + line % K : 1;
+    gb = v ? line / nlp : 0;
+    const int ln = line - gb * nlp;
+    i = v ? itop - ln / K : 1;
+    j = v ? 1 + ln % K : 1;
     return v && wl * NL < nlines;
   };
   auto fetch = [&](int wl, ulonglong2& dd, double& bf) {
-    int i, j;
+    int i, j, gb;
     dd = make_ulonglong2(0ull, 0ull);
     bf = 0.0;
-    if (line_of(wl, i, j)) {
-      dd = *reinterpret_cast<const ulonglong2*>(a.desc + 2 * (line_desc(L, i, j) * G + seg));
-      const long long bs = L.at(i, j, 0);
+    if (line_of(wl, i, j, gb)) {
+      dd = *reinterpret_cast<const ulonglong2*>(a.desc + gb * a.dstride +
+                                                2 * (line_desc(L, i, j) * G + seg));
+      const long long bs = L.at(i, j, 0) + gb * L.bs;
       if (seg == 0) bf = a.bnd[bs];
       else if (seg == (m - 1) / S) bf = a.bnd[bs + a.hi_off];
     }
@@ -1437,14 +1479,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
   ulonglong2 ddn;
   double bfn;
   fetch(wl0, ddn, bfn);
-  bool bad = false;
+  DivAcc acc;
   int it = 0;
   for (int wl = wl0; wl * NL < nlines; wl += stride, ++it) {
     const int b = it & 1;
-    const int line = wl * NL + sub;
-    const bool valid = NL == 1 || line < nlines;
-    const int i = valid ? itop - line / K : 1, j = valid ? 1 + line % K : 1;
-    const long long base = L.at(i, j, 0);
+    int i, j, gb;
+    const bool inl = line_of(wl, i, j, gb);
+    // batched: grids that stopped at an earlier step are skipped (their copy still lands)
+    const bool valid = inl && (L.nb == 1 || !a.div_step || a.div_step[gb] >= a.step);
+    const long long base = L.at(i, j, 0) + gb * L.bs;
     const unsigned long long amask = ddn.x;
     const uint32_t sbits = (uint32_t)ddn.y, cmask = (uint32_t)(ddn.y >> 32);
     const double bfold = bfn;
@@ -1469,14 +1512,18 @@ __global__ void __launch_bounds__(NW * 32, 1)
             make_double2(r[q], r[q + 1]);
     }
     __syncwarp();
-    rw_store<S, G>(a, [&](int p) { return W[swz(p - 1)]; }, valid, seg, sub, sbits, FP, base,
-                   bad);
+    rw_store<S, G>(a, [&](int p) { return W[swz(p - 1)]; }, valid, seg, sbits, FP, base, acc);
+    if (L.nb > 1 && a.check) {  // batched: the line's own grid (lines of a warp may differ)
+      if (acc.bad(a.thr)) atomicMin(a.div_step + gb, a.step);
+      acc = DivAcc();
+    }
     // the buffer's generic-proxy reads/writes are ordered before the next tensor copy into it
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0 && (wl + 2 * stride) * NL < nlines) issue(wl + 2 * stride, b);
   }
-  if (a.check && __any_sync(FULL, bad) && lane == 0) atomicMin(a.div_step, a.step);
+  if (L.nb == 1 && a.check && __any_sync(FULL, acc.bad(a.thr)) && lane == 0)
+    atomicMin(a.div_step, a.step);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1517,10 +1564,16 @@ __global__ void k_build_desc(const Layout L, int axis, int S, int P, int lm,
       const uint32_t c = codes[base + p * stride];
       w0 |= (unsigned long long)((c >> sh) & 1u) << j;
       if (j < S && p <= m) {
-        w1 |= (unsigned long long)(c & 1u) << j;
+        if (!lm) w1 |= (unsigned long long)(c & 1u) << j;
         w1 |= (unsigned long long)((c >> 4) & 1u) << (32 + j);
       }
     }
+    if (lm)  // row-warp store pass: lane `seg` stores rows 1 + seg + P*q, q = 0..S-1; its
+             // solute bits in that order (no per-node shuffle in the LODIE2 flow epilogue)
+      for (int q = 0; q < S; ++q) {
+        const int p = 1 + seg + P * q;
+        if (p <= m) w1 |= (unsigned long long)(codes[base + p * stride] & 1u) << q;
+      }
     desc[2 * t] = w0;
     desc[2 * t + 1] = w1;
   }
@@ -1702,7 +1755,13 @@ static int rowwarp_G(int m) {
   if (m + 1 == 512) return 32;  // S = 16 (c4: 734 -> 645 us with the LODIE2 flow)
   if (m + 1 == 256) return 16;  // S = 16 (c3: 100 -> 95 us; two lines per warp)
   if (m + 1 == 128) return 16;  // S = 8  (c2: 25 -> 22 us)
-  if (m + 1 == 96) return 8;    // S = 12, four lines per warp (c5 97^3 lines)
+  if (m + 1 == 96) {            // c5 97^3 lines: S = 12, four lines per warp, or (PBG_RW96G)
+    static const int g = [] {   // S = 6, two lines per warp
+      const char* e = getenv("PBG_RW96G");
+      return e && atoi(e) == 16 ? 16 : 8;
+    }();
+    return g;
+  }
   return 0;
 }
 static int rowwarp_S(int m) {
@@ -1766,7 +1825,8 @@ static void launch_strided_SCL(const SweepArgs& a, int axis, cudaStream_t st) {
   const size_t smem = strided_smem<LB, RT>(S, P, epi_needs(a.epi) != 0, flow_stage_n(a));
   auto kern = k_sweep_strided<S, P, CN, LB, RT>;
   // persistent blocks: as many as fit at once (the tables are staged once per block)
-  const int grid = std::min(ntx * nouter, resident_blocks((const void*)kern, LB * P, smem));
+  const int grid =
+      std::min(ntx * nouter * a.L.nb, resident_blocks((const void*)kern, LB * P, smem));
   kern<<<grid, block, smem, st>>>(a, axis, ntx, nouter);
 }
 
@@ -1781,7 +1841,7 @@ static void launch_col(const SweepArgs& a, int axis, cudaStream_t st) {
       sizeof(double) * (kTabDoubles + P * (P + 2) + 4 * LB * P + kFlowHdr + flow_stage_n(a));
   auto kern = k_sweep_col<S, P, CN, LB>;
   resident_blocks((const void*)kern, LB * P, smem);  // shared-memory limit, once
-  kern<<<dim3(ntx, nouter), dim3(LB, P), smem, st>>>(a, axis);
+  kern<<<dim3(ntx, nouter, a.L.nb), dim3(LB, P), smem, st>>>(a, axis);
 }
 
 // Row tiles of 16 lines for lines of <= 256 rows (256 threads per block: fewer duplicated
@@ -1833,7 +1893,7 @@ static void launch_strided_SP(const SweepArgs& a, int axis, cudaStream_t st) {
 
 template <int S, int G>
 static void launch_rowwarp_SG(const SweepArgs& a, cudaStream_t st) {
-  const int nlines = (a.on ? a.on : a.L.n0 - 2) * (a.L.n1 - 2);
+  const int nlines = (a.on ? a.on : a.L.n0 - 2) * (a.L.n1 - 2) * a.L.nb;
   const size_t smem = rowwarp_smem(S, G, flow_stage_n(a));
   auto kern = k_sweep_rowwarp<S, G>;
   const int per_block = kRWarps * (32 / G);
@@ -1881,7 +1941,8 @@ static bool line_tensor_map(const SweepArgs& a, int box_chunks, CUtensorMap* tm)
   if (!fn) return false;
   const Layout& L = a.L;
   cuuint64_t dims[3] = {16, (cuuint64_t)((L.pitch - kOff - 1) / 16),
-                        (cuuint64_t)L.n0 * (cuuint64_t)L.n1};
+                        L.nb > 1 ? (cuuint64_t)L.nb * (cuuint64_t)(L.bs / L.pitch)
+                                 : (cuuint64_t)L.n0 * (cuuint64_t)L.n1};
   cuuint64_t strides[2] = {128, (cuuint64_t)L.pitch * sizeof(double)};
   cuuint32_t box[3] = {16, (cuuint32_t)box_chunks, 1};
   cuuint32_t es[3] = {1, 1, 1};
@@ -1894,7 +1955,7 @@ template <int S, int G, int NW>
 static bool launch_rowtma_SGN(const SweepArgs& a, cudaStream_t st) {
   CUtensorMap tm;
   if (!line_tensor_map(a, G * S / 16, &tm)) return false;
-  const int nlines = (a.on ? a.on : a.L.n0 - 2) * (a.L.n1 - 2);
+  const int nlines = (a.on ? a.on : a.L.n0 - 2) * (a.L.n1 - 2) * a.L.nb;
   const size_t smem = RowTma<S, G, NW>::smem(flow_stage_n(a));
   auto kern = k_sweep_rowtma<S, G, NW>;
   const int per_block = NW * (32 / G);
@@ -1915,7 +1976,10 @@ static bool launch_rowtma_SG(const SweepArgs& a, cudaStream_t st) {
 }
 
 static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
-  if (a.rw && rowtma_mode() && rowwarp_S(a.m) == 16) {
+  // TMA staging measured faster for 256-row lines (c3), slower for 512-row lines (c4:
+  // 1.62 vs 1.59 ms/step; profiles/rowtma_ab_r02.txt); PBG_ROWTMA=0/1/2: off / auto / on.
+  if (a.rw && rowwarp_S(a.m) == 16 &&
+      (rowtma_mode() == 2 || (rowtma_mode() == 1 && rowwarp_G(a.m) == 16))) {
     const bool ok = rowwarp_G(a.m) == 32 ? launch_rowtma_SG<16, 32>(a, st)
                                          : launch_rowtma_SG<16, 16>(a, st);
     if (ok) {
@@ -1929,6 +1993,7 @@ static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
       case 1616: launch_rowwarp_SG<16, 16>(a, st); break;
       case 1608: launch_rowwarp_SG<8, 16>(a, st); break;
       case 812: launch_rowwarp_SG<12, 8>(a, st); break;
+      case 1606: launch_rowwarp_SG<6, 16>(a, st); break;
       default: return fail(PBG_E_UNSUPPORTED, "row-warp sweep without a segment length");
     }
     PBG_LAUNCH_CHECK("k_sweep_rowwarp");
@@ -2219,11 +2284,16 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
   PBG_CUDA(cudaMemcpyAsync(aux.buf, host.data(), host.size() * sizeof(double),
                            cudaMemcpyHostToDevice, st));
   const long long nseg = desc_segments(a.L, axis, P);
-  // +64 words of slack: tiles past the last interior column read (unused) descriptors
-  PBG_CUDA(cudaMallocAsync(&aux.desc, (2 * nseg + 64) * sizeof(unsigned long long), st));
-  k_build_desc<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, codes,
-                                         aux.desc);
-  PBG_LAUNCH_CHECK("k_build_desc");
+  // +64 words of slack: tiles past the last interior column read (unused) descriptors; a
+  // batched march keeps one such block per grid (a.dstride words apart)
+  const int nb = a.L.nb;
+  a.dstride = 2 * nseg + 64;
+  PBG_CUDA(cudaMallocAsync(&aux.desc, nb * a.dstride * sizeof(unsigned long long), st));
+  for (int b = 0; b < nb; ++b) {
+    k_build_desc<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, codes + b * a.L.bs,
+                                           aux.desc + b * a.dstride);
+    PBG_LAUNCH_CHECK("k_build_desc");
+  }
   if (S <= kDedupMaxS) {
     const int nw = 1 << (key_bits(S) - 5);
     unsigned* bitmap = nullptr;
@@ -2236,8 +2306,11 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
     PBG_CUDA(cudaMallocAsync(&base, (size_t)nw * sizeof(int), st));
     PBG_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
     PBG_CUDA(cudaMemsetAsync(bitmap, 0, (size_t)nw * sizeof(unsigned), st));
-    k_mark_keys<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, aux.desc, bitmap);
-    PBG_LAUNCH_CHECK("k_mark_keys");
+    for (int b = 0; b < nb; ++b) {
+      k_mark_keys<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, aux.desc + b * a.dstride,
+                                           bitmap);
+      PBG_LAUNCH_CHECK("k_mark_keys");
+    }
     k_popc_words<<<(nw + 255) / 256, 256, 0, st>>>(bitmap, nw, cnt);
     PBG_LAUNCH_CHECK("k_popc_words");
     cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, base, nw, st);
@@ -2251,8 +2324,11 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
     if (ndist > 0) {
       k_key_factors<<<(nw + 255) / 256, 256, 0, st>>>(a.co, S, bitmap, base, nw, aux.gfac);
       PBG_LAUNCH_CHECK("k_key_factors");
-      k_assign_slots<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, aux.desc, bitmap, base);
-      PBG_LAUNCH_CHECK("k_assign_slots");
+      for (int b = 0; b < nb; ++b) {
+        k_assign_slots<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, aux.desc + b * a.dstride,
+                                                bitmap, base);
+        PBG_LAUNCH_CHECK("k_assign_slots");
+      }
     }
     PBG_CUDA(cudaFreeAsync(bitmap, st));
     PBG_CUDA(cudaFreeAsync(cnt, st));
@@ -2262,18 +2338,22 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
     int* counter = nullptr;
     PBG_CUDA(cudaMallocAsync(&counter, sizeof(int), st));
     PBG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-    k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, a.co, 0,
-                                            aux.desc, counter, nullptr);
-    PBG_LAUNCH_CHECK("k_seg_factors");
+    for (int b = 0; b < nb; ++b) {
+      k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, a.co, 0,
+                                              aux.desc + b * a.dstride, counter, nullptr);
+      PBG_LAUNCH_CHECK("k_seg_factors");
+    }
     int ngen = 0;
     PBG_CUDA(cudaMemcpyAsync(&ngen, counter, sizeof(int), cudaMemcpyDeviceToHost, st));
     PBG_CUDA(cudaStreamSynchronize(st));  // also: the host staging vector dies here
     PBG_CUDA(cudaMallocAsync(&aux.gfac, ((size_t)ngen + 1) * 5 * kTabRows * sizeof(double), st));
     if (ngen > 0) {
       PBG_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-      k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, a.co, 1,
-                                             aux.desc, counter, aux.gfac);
-      PBG_LAUNCH_CHECK("k_seg_factors");
+      for (int b = 0; b < nb; ++b) {
+        k_seg_factors<<<148 * 8, 256, 0, st>>>(a.L, axis, S, P, lm, a.co, 1,
+                                               aux.desc + b * a.dstride, counter, aux.gfac);
+        PBG_LAUNCH_CHECK("k_seg_factors");
+      }
     }
     PBG_CUDA(cudaFreeAsync(counter, st));
   }
@@ -2478,6 +2558,8 @@ extern "C" PBG_API int pbg_get_profile(double axis_ms[3], int64_t launches[3]) {
 // kernels, with one host synchronisation at its end (reading the divergence flag).
 struct pbg_plan {
   pbg_march_desc d;  // codes / rho pointers stay the caller's
+  int nb = 1;        // batched march: nb grids, bs elements apart in every buffer
+  long long bs = 0;
   Plan plan;
   SweepArgs ax[3];
   AxisAux aux[3];
@@ -2488,7 +2570,9 @@ struct pbg_plan {
 };
 
 namespace pbg {
-__global__ void k_set_int(int* p, int v) { *p = v; }
+__global__ void k_set_int(int* p, int n, int v) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) p[t] = v;
+}
 static std::mutex g_prof_mu;
 
 static void plan_free(pbg_plan* p, cudaStream_t st) {
@@ -2511,21 +2595,33 @@ static int check_desc(const pbg_march_desc* d) {
   return PBG_OK;
 }
 
-extern "C" PBG_API int pbg_plan_create(const pbg_march_desc* d, pbg_plan** out, void* stream) {
+extern "C" PBG_API int pbg_plan_create_batch(const pbg_march_desc* d, int32_t nbatch,
+                                             int64_t batch_stride, pbg_plan** out,
+                                             void* stream) {
   if (!out) return fail(PBG_E_INVALID, "null output handle");
   *out = nullptr;
   int rc = check_desc(d);
   if (rc) return rc;
+  if (nbatch < 1) return fail(PBG_E_INVALID, "nbatch must be >= 1");
+  const Layout L0 = make_layout(&d->grid);
+  if (nbatch > 1 && (batch_stride < L0.n0 * L0.s0 || batch_stride % L0.pitch))
+    return fail(PBG_E_INVALID,
+                "batch_stride must cover one pitched grid and be a multiple of the pitch");
+  if (nbatch > 1 &&
+      (d->variant == PBG_ADI1 || d->variant == PBG_ADI2 || d->variant == PBG_EULER))
+    return fail(PBG_E_UNSUPPORTED, "batched marches support the splitting schemes");
   if (!d->work[0]) return fail(PBG_E_INVALID, "null device buffer");
   keep_pool_memory();
   cudaStream_t st = (cudaStream_t)stream;
   pbg_plan* p = new pbg_plan();
   p->d = *d;
+  p->nb = nbatch;
+  p->bs = nbatch > 1 ? batch_stride : 0;
   auto bail = [&](int code) {
     plan_free(p, st);
     return code;
   };
-  if (cudaMallocHost(&p->hflag, sizeof(int)) != cudaSuccess ||
+  if (cudaMallocHost(&p->hflag, nbatch * sizeof(int)) != cudaSuccess ||
       cudaEventCreate(&p->e0) != cudaSuccess || cudaEventCreate(&p->e1) != cudaSuccess)
     return bail(fail(PBG_E_CUDA, "plan allocation failed"));
   if (d->variant == PBG_ADI1 || d->variant == PBG_ADI2 || d->variant == PBG_EULER) {
@@ -2537,10 +2633,12 @@ extern "C" PBG_API int pbg_plan_create(const pbg_march_desc* d, pbg_plan** out, 
     return bail(fail(PBG_E_UNSUPPORTED, "variant not supported by the device march"));
   march_axes(d, p->plan, p->ax);
   for (int axis = 0; axis < 3; ++axis) {
+    p->ax[axis].L.nb = p->nb;
+    p->ax[axis].L.bs = p->bs;
     rc = prepare_axis(p->ax[axis], axis, d->codes, p->aux[axis], st);
     if (rc) return bail(rc);
   }
-  if (cudaMallocAsync(&p->dflag, sizeof(int), st) != cudaSuccess)
+  if (cudaMallocAsync(&p->dflag, p->nb * sizeof(int), st) != cudaSuccess)
     return bail(fail(PBG_E_CUDA, "plan allocation failed"));
   if (cudaStreamSynchronize(st) != cudaSuccess)  // the plan may run on any stream
     return bail(fail(PBG_E_CUDA, "plan setup failed"));
@@ -2548,15 +2646,20 @@ extern "C" PBG_API int pbg_plan_create(const pbg_march_desc* d, pbg_plan** out, 
   return PBG_OK;
 }
 
+extern "C" PBG_API int pbg_plan_create(const pbg_march_desc* d, pbg_plan** out, void* stream) {
+  return pbg_plan_create_batch(d, 1, 0, out, stream);
+}
+
 extern "C" PBG_API int pbg_plan_destroy(pbg_plan* p, void* stream) {
   if (p) plan_free(p, (cudaStream_t)stream);
   return PBG_OK;
 }
 
-extern "C" PBG_API int pbg_plan_run(pbg_plan* p, const double* initial, double* work0,
-                                    double* work1, int32_t nsteps, int32_t check_divergence,
-                                    int32_t* steps_taken, int32_t* diverged_step,
-                                    int32_t* result_slot, float* device_ms, void* stream) {
+extern "C" PBG_API int pbg_plan_run_batch(pbg_plan* p, const double* initial, double* work0,
+                                          double* work1, int32_t nsteps,
+                                          int32_t check_divergence, int32_t* steps_taken,
+                                          int32_t* diverged_step, int32_t* result_slot,
+                                          float* device_ms, void* stream) {
   if (!p) return fail(PBG_E_INVALID, "null plan");
   if (!initial || !work0 || !work1) return fail(PBG_E_INVALID, "null device buffer");
   if (nsteps < 1) return fail(PBG_E_INVALID, "nsteps must be >= 1");
@@ -2575,11 +2678,15 @@ extern "C" PBG_API int pbg_plan_run(pbg_plan* p, const double* initial, double* 
   double* work[2] = {work0, work1};
   int* dflag = p->dflag;
   int rc = PBG_OK;
-  k_set_int<<<1, 1, 0, st>>>(dflag, INT_MAX);
+  const int nb = p->nb;
+  k_set_int<<<1, 256, 0, st>>>(dflag, nb, INT_MAX);
   PBG_LAUNCH_CHECK("k_set_int");
   if (check_divergence) {
-    k_faces_bad<<<148, 256, 0, st>>>(make_layout(g), work0, p->d.divergence_threshold, dflag);
-    PBG_LAUNCH_CHECK("k_faces_bad");
+    for (int b = 0; b < nb; ++b) {
+      k_faces_bad<<<148, 256, 0, st>>>(make_layout(g), work0 + b * p->bs,
+                                       p->d.divergence_threshold, dflag + b);
+      PBG_LAUNCH_CHECK("k_faces_bad");
+    }
   }
 
   int st_idx = -1;
@@ -2592,7 +2699,14 @@ extern "C" PBG_API int pbg_plan_run(pbg_plan* p, const double* initial, double* 
   // slower: launch tails).
   const bool lod_rw = plan.family <= 1 && p->ax[2].rw;
   const int chunk = lod_rw ? env_int("PBG_FUSE12", 0) : 0;
-  const bool inpl = lod_rw && (chunk > 0 || env_int("PBG_INPLACE2", 0) != 0);
+  // LOD sweeps in place on one state buffer when a field is about the L2 size or smaller
+  // (c3 257^3: 216 -> 211 us/step, the next sweep re-reads what the previous one left in L2);
+  // at 513^3 (8.7x L2) in place measured 2-4% slower, so the ping-pong stays there.
+  // PBG_INPLACE=0/1 forces either (profiles/inplace_ab_r02.txt).
+  const double field_mb = (double)nb * g->n[0] * g->n[1] * g->pitch * 8.0 / 1e6;
+  const bool inpl_all =
+      plan.family <= 1 && env_int("PBG_INPLACE", field_mb <= 256.0 ? 1 : 0) != 0;
+  const bool inpl = inpl_all || (lod_rw && (chunk > 0 || env_int("PBG_INPLACE2", 0) != 0));
   const int nplanes = g->n[0] - 2;
 
   std::vector<cudaEvent_t> kev;  // per-launch events when profiling is on
@@ -2620,6 +2734,10 @@ extern "C" PBG_API int pbg_plan_run(pbg_plan* p, const double* initial, double* 
       if (plan.family <= 1) {
         a.src = axis == 0 ? X : (axis == 1 ? A : Bf);
         a.dst = axis == 0 ? A : (axis == 1 ? Bf : (inpl ? Bf : A));
+        if (inpl_all) {  // every sweep in place on the state buffer (one field per step)
+          a.src = axis == 0 ? X : Bf;
+          a.dst = Bf;
+        }
       } else {
         a.src = X;
         a.acc = A;
@@ -2650,9 +2768,8 @@ extern "C" PBG_API int pbg_plan_run(pbg_plan* p, const double* initial, double* 
     return rc;
   }
   PBG_CUDA(cudaEventRecord(p->e1, st));
-  PBG_CUDA(cudaMemcpyAsync(p->hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PBG_CUDA(cudaMemcpyAsync(p->hflag, dflag, nb * sizeof(int), cudaMemcpyDeviceToHost, st));
   PBG_CUDA(cudaStreamSynchronize(st));
-  const int dstep = *p->hflag;
   float ms = 0.f;
   cudaEventElapsedTime(&ms, p->e0, p->e1);
   if (!kev.empty()) {
@@ -2666,22 +2783,33 @@ extern "C" PBG_API int pbg_plan_run(pbg_plan* p, const double* initial, double* 
     }
   }
   for (auto ev : kev) cudaEventDestroy(ev);
-  int taken = nsteps;
-  if (check_divergence && dstep != INT_MAX) {
-    taken = dstep;
-    if (diverged_step) *diverged_step = dstep;
-  } else if (diverged_step) {
-    *diverged_step = 0;
+  for (int b = 0; b < nb; ++b) {  // per grid: steps taken, divergence, state slot
+    const int dstep = p->hflag[b];
+    int taken = nsteps;
+    if (check_divergence && dstep != INT_MAX) {
+      taken = dstep;
+      if (diverged_step) diverged_step[b] = dstep;
+    } else if (diverged_step) {
+      diverged_step[b] = 0;
+    }
+    int slot;
+    if (inpl) slot = st0 < 0 ? 1 : st0;
+    else if (st0 < 0) slot = (taken - 1) % 2;
+    else slot = (st0 + taken) % 2;
+    if (steps_taken) steps_taken[b] = taken;
+    if (result_slot) result_slot[b] = slot;
   }
-  // state slot after `taken` steps
-  int slot;
-  if (inpl) slot = st0 < 0 ? 1 : st0;
-  else if (st0 < 0) slot = (taken - 1) % 2;
-  else slot = (st0 + taken) % 2;
-  if (steps_taken) *steps_taken = taken;
-  if (result_slot) *result_slot = slot;
   if (device_ms) *device_ms = ms;
   return PBG_OK;
+}
+
+extern "C" PBG_API int pbg_plan_run(pbg_plan* p, const double* initial, double* work0,
+                                    double* work1, int32_t nsteps, int32_t check_divergence,
+                                    int32_t* steps_taken, int32_t* diverged_step,
+                                    int32_t* result_slot, float* device_ms, void* stream) {
+  if (p && p->nb != 1) return fail(PBG_E_INVALID, "batched plan: use pbg_plan_run_batch");
+  return pbg_plan_run_batch(p, initial, work0, work1, nsteps, check_divergence, steps_taken,
+                            diverged_step, result_slot, device_ms, stream);
 }
 
 extern "C" PBG_API int pbg_march(const pbg_march_desc* d, int32_t* steps_taken,

@@ -95,6 +95,9 @@ struct SweepArgs {
   // Outer-index range of a launch (axis 1 column tiles: planes i; axis 2 row-warp lines:
   // planes i): planes o0+1 .. o0+on; on = 0 means all interior planes.
   int o0, on;
+  // Batched marches: descriptor words per grid (desc + b * dstride is grid b's block);
+  // div_step holds one flag per grid.
+  long long dstride;
 };
 
 
