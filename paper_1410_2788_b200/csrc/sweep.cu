@@ -96,14 +96,28 @@ __device__ __forceinline__ void flow_group(const SweepArgs& a, const double* FP,
                                            uint32_t s1, uint32_t s2, uint32_t s3, double pm) {
   const double x0 = flow_tiny(w0, a.ftiny), x1 = flow_tiny(w1, a.ftiny);
   const double x2 = flow_tiny(w2, a.ftiny), x3 = flow_tiny(w3, a.ftiny);
-  auto fin = [&](double& w, double x, uint32_t s) {
-    if (s || !a.fsmall_on || !(fabs(w) <= kFTinyX)) w = flow_sm(a, FP, w, s, pm);
-    else w = pm != 1.0 ? pm * x : x;
-  };
-  fin(w0, x0, s0);
-  fin(w1, x1, s1);
-  fin(w2, x2, s2);
-  fin(w3, x3, s3);
+  auto slow = [&](double w, uint32_t s) { return s || !a.fsmall_on || !(fabs(w) <= kFTinyX); };
+  const unsigned need = (slow(w0, s0) ? 1u : 0u) | (slow(w1, s1) ? 2u : 0u) |
+                        (slow(w2, s2) ? 4u : 0u) | (slow(w3, s3) ? 8u : 0u);
+  const double in0 = w0, in1 = w1, in2 = w2, in3 = w3;
+  w0 = pm != 1.0 ? pm * x0 : x0;
+  w1 = pm != 1.0 ? pm * x1 : x1;
+  w2 = pm != 1.0 ? pm * x2 : x2;
+  w3 = pm != 1.0 ? pm * x3 : x3;
+  if (!need) return;
+  // the others one at a time through ONE inlined copy of flow_sm (a per-node copy made the
+  // row kernels' code 4x larger and their instruction fetch a top stall)
+#pragma unroll 1
+  for (unsigned m = need; m; m &= m - 1) {
+    const int u = __ffs(m) - 1;
+    const double w = u == 0 ? in0 : (u == 1 ? in1 : (u == 2 ? in2 : in3));
+    const uint32_t s = u == 0 ? s0 : (u == 1 ? s1 : (u == 2 ? s2 : s3));
+    const double r = flow_sm(a, FP, w, s, pm);
+    if (u == 0) w0 = r;
+    else if (u == 1) w1 = r;
+    else if (u == 2) w2 = r;
+    else w3 = r;
+  }
 }
 
 __host__ __device__ __forceinline__ bool uses_flow(int pro, int epi) {
@@ -1191,7 +1205,7 @@ __device__ __forceinline__ void rw_store(const SweepArgs& a, At at, bool valid, 
         acc.add(x);
       }
     }
-#pragma unroll
+#pragma unroll 1
     for (int q = 0; q < S4; q += 4) {
       double x[4];
 #pragma unroll
@@ -1231,7 +1245,7 @@ __device__ __forceinline__ void rw_store(const SweepArgs& a, At at, bool valid, 
   }
 }
 
-template <int S, int G>
+template <int S, int G, bool BATCH>
 __global__ void __launch_bounds__(kRWarps * 32, 3)
     k_sweep_rowwarp(const SweepArgs a, const int nlines) {
   extern __shared__ double sm[];
@@ -1262,13 +1276,13 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
   double* W = Wb + warp * RW::WD + sub * RW::LW;          // this lane's line
   double* sR = Wb + warp * RW::WD + NL * RW::LW + sub * RW::RW;
   DivAcc acc;
-  const int nlp = nlines / L.nb;  // lines per grid (batched marches: nb grids)
+  const int nlp = BATCH ? nlines / L.nb : nlines;  // lines per grid (batched: nb grids)
   for (int wl = blockIdx.x * kRWarps + warp; wl * NL < nlines; wl += gridDim.x * kRWarps) {
     const int line = wl * NL + sub;
-    const int b = line < nlines ? line / nlp : 0, ln = line - b * nlp;
+    const int b = BATCH && line < nlines ? line / nlp : 0, ln = line - b * nlp;
     // NL == 1: the loop condition; batched: grids that stopped at an earlier step are skipped
     const bool valid = (NL == 1 || line < nlines) &&
-                       (L.nb == 1 || !a.div_step || a.div_step[b] >= a.step);
+                       (!BATCH || !a.div_step || a.div_step[b] >= a.step);
     // planes in reverse (the axis-1 sweep before this one wrote the last planes last)
     const int i = valid ? itop - ln / K : 1, j = valid ? 1 + ln % K : 1;
     const long long base = L.at(i, j, 0) + (long long)b * L.bs;
@@ -1295,7 +1309,7 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
     {  // the warp's next lines towards L2 while this one is solved (LODIE1 c4: 533 -> 498 us)
       const int nl = (wl + gridDim.x * kRWarps) * NL + sub;
       if (nl < nlines) {
-        const int nb2 = nl / nlp, nn = nl - nb2 * nlp;
+        const int nb2 = BATCH ? nl / nlp : 0, nn = nl - nb2 * nlp;
         const double* np = a.src + L.at(itop - nn / K, 1 + nn % K, 0) + (long long)nb2 * L.bs + 1;
         for (int c = seg; c < G * S / 16; c += G)  // 128-byte lines
           asm volatile("prefetch.global.L2 [%0];" ::"l"(np + 16 * c));
@@ -1321,13 +1335,13 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
     __syncwarp();
 
     rw_store<S, G>(a, [&](int p) { return W[RW::pos(p)]; }, valid, seg, sbits, FP, base, acc);
-    if (L.nb > 1 && a.check) {  // batched: the line's own grid (lines of a warp may differ)
+    if (BATCH && a.check) {  // batched: the line's own grid (lines of a warp may differ)
       if (acc.bad(a.thr)) atomicMin(a.div_step + b, a.step);
       acc = DivAcc();
     }
     __syncwarp();  // the line buffers are restaged by the next lines
   }
-  if (L.nb == 1 && a.check && __any_sync(FULL, acc.bad(a.thr)) && lane == 0)
+  if (!BATCH && a.check && __any_sync(FULL, acc.bad(a.thr)) && lane == 0)
     atomicMin(a.div_step, a.step);
 }
 
@@ -1391,7 +1405,7 @@ struct RowTma {
   }
 };
 
-template <int S, int G, int NW>
+template <int S, int G, int NW, bool BATCH>
 __global__ void __launch_bounds__(NW * 32, 1)
     k_sweep_rowtma(const SweepArgs a, const int nlines, const __grid_constant__ CUtensorMap tm) {
   static_assert(S == 16, "one 128-byte chunk per segment");
@@ -1431,8 +1445,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const int stride = gridDim.x * NW;
   const int wl0 = blockIdx.x * NW + warp;
   // lane 0: one tensor copy per valid line of warp-iteration wl into buffer b
-  const int nlp = nlines / L.nb;  // lines per grid (batched marches: nb grids)
-  const long long grid_lines = L.bs / L.pitch;  // tensor-map lines between grids
+  const int nlp = BATCH ? nlines / L.nb : nlines;  // lines per grid (batched: nb grids)
+  const long long grid_lines = BATCH ? L.bs / L.pitch : 0;  // tensor-map lines between grids
   auto issue = [&](int wl, int b) {
     int nv = 0;
 #pragma unroll
@@ -1442,7 +1456,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     for (int l = 0; l < NL; ++l) {
       const int line = wl * NL + l;
       if (line < nlines) {
-        const int gb = line / nlp, ln = line - gb * nlp;
+        const int gb = BATCH ? line / nlp : 0, ln = line - gb * nlp;
         const int i = itop - ln / K, j = 1 + ln % K;
         tma_load_3d(Lb + (warp * 2 + b) * WB + l * LD, &tm, 0, 0,
                     (int)(gb * grid_lines) + i * L.n1 + j, bar + b);
@@ -1458,7 +1472,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   auto line_of = [&](int wl, int& i, int& j, int& gb) {
     const int line = wl * NL + sub;
     const bool v = NL == 1 || line < nlines;
-    gb = v ? line / nlp : 0;
+    gb = BATCH && v ? line / nlp : 0;
     const int ln = line - gb * nlp;
     i = v ? itop - ln / K : 1;
     j = v ? 1 + ln % K : 1;
@@ -1486,7 +1500,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     int i, j, gb;
     const bool inl = line_of(wl, i, j, gb);
     // batched: grids that stopped at an earlier step are skipped (their copy still lands)
-    const bool valid = inl && (L.nb == 1 || !a.div_step || a.div_step[gb] >= a.step);
+    const bool valid = inl && (!BATCH || !a.div_step || a.div_step[gb] >= a.step);
     const long long base = L.at(i, j, 0) + gb * L.bs;
     const unsigned long long amask = ddn.x;
     const uint32_t sbits = (uint32_t)ddn.y, cmask = (uint32_t)(ddn.y >> 32);
@@ -1513,7 +1527,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
     __syncwarp();
     rw_store<S, G>(a, [&](int p) { return W[swz(p - 1)]; }, valid, seg, sbits, FP, base, acc);
-    if (L.nb > 1 && a.check) {  // batched: the line's own grid (lines of a warp may differ)
+    if (BATCH && a.check) {  // batched: the line's own grid (lines of a warp may differ)
       if (acc.bad(a.thr)) atomicMin(a.div_step + gb, a.step);
       acc = DivAcc();
     }
@@ -1522,7 +1536,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     __syncwarp();
     if (lane == 0 && (wl + 2 * stride) * NL < nlines) issue(wl + 2 * stride, b);
   }
-  if (L.nb == 1 && a.check && __any_sync(FULL, acc.bad(a.thr)) && lane == 0)
+  if (!BATCH && a.check && __any_sync(FULL, acc.bad(a.thr)) && lane == 0)
     atomicMin(a.div_step, a.step);
 }
 
@@ -1895,7 +1909,7 @@ template <int S, int G>
 static void launch_rowwarp_SG(const SweepArgs& a, cudaStream_t st) {
   const int nlines = (a.on ? a.on : a.L.n0 - 2) * (a.L.n1 - 2) * a.L.nb;
   const size_t smem = rowwarp_smem(S, G, flow_stage_n(a));
-  auto kern = k_sweep_rowwarp<S, G>;
+  auto kern = a.L.nb > 1 ? k_sweep_rowwarp<S, G, true> : k_sweep_rowwarp<S, G, false>;
   const int per_block = kRWarps * (32 / G);
   const int grid = std::min((nlines + per_block - 1) / per_block,
                             resident_blocks((const void*)kern, kRWarps * 32, smem));
@@ -1957,7 +1971,7 @@ static bool launch_rowtma_SGN(const SweepArgs& a, cudaStream_t st) {
   if (!line_tensor_map(a, G * S / 16, &tm)) return false;
   const int nlines = (a.on ? a.on : a.L.n0 - 2) * (a.L.n1 - 2) * a.L.nb;
   const size_t smem = RowTma<S, G, NW>::smem(flow_stage_n(a));
-  auto kern = k_sweep_rowtma<S, G, NW>;
+  auto kern = a.L.nb > 1 ? k_sweep_rowtma<S, G, NW, true> : k_sweep_rowtma<S, G, NW, false>;
   const int per_block = NW * (32 / G);
   const int grid = std::min((nlines + per_block - 1) / per_block,
                             resident_blocks((const void*)kern, NW * 32, smem));
@@ -1967,12 +1981,9 @@ static bool launch_rowtma_SGN(const SweepArgs& a, cudaStream_t st) {
 
 template <int S, int G>
 static bool launch_rowtma_SG(const SweepArgs& a, cudaStream_t st) {
-  switch (rowtma_nw()) {
-    case 8: return launch_rowtma_SGN<S, G, 8>(a, st);
-    case 12: return launch_rowtma_SGN<S, G, 12>(a, st);
-    case 16: return launch_rowtma_SGN<S, G, 16>(a, st);
-    default: return launch_rowtma_SGN<S, G, 20>(a, st);
-  }
+  // 20 warps per block measured best (8 / 12 / 16: +7..19%, profiles/rowtma_ab_r02.txt)
+  if (rowtma_nw() == 16) return launch_rowtma_SGN<S, G, 16>(a, st);
+  return launch_rowtma_SGN<S, G, 20>(a, st);
 }
 
 static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
