@@ -96,9 +96,10 @@ __device__ __forceinline__ void flow_group(const SweepArgs& a, const double* FP,
                                            uint32_t s1, uint32_t s2, uint32_t s3, double pm) {
   const double x0 = flow_tiny(w0, a.ftiny), x1 = flow_tiny(w1, a.ftiny);
   const double x2 = flow_tiny(w2, a.ftiny), x3 = flow_tiny(w3, a.ftiny);
-  auto slow = [&](double w, uint32_t s) { return s || !a.fsmall_on || !(fabs(w) <= kFTinyX); };
-  const unsigned need = (slow(w0, s0) ? 1u : 0u) | (slow(w1, s1) ? 2u : 0u) |
-                        (slow(w2, s2) ? 4u : 0u) | (slow(w3, s3) ? 8u : 0u);
+  // branch-free: solute palette, |w| above the tiny range (NaN included), no small form
+  const unsigned big = (fabs(w0) <= kFTinyX ? 0u : 1u) | (fabs(w1) <= kFTinyX ? 0u : 2u) |
+                       (fabs(w2) <= kFTinyX ? 0u : 4u) | (fabs(w3) <= kFTinyX ? 0u : 8u);
+  const unsigned need = a.fsmall_on ? (big | s0 | (s1 << 1) | (s2 << 2) | (s3 << 3)) : 15u;
   const double in0 = w0, in1 = w1, in2 = w2, in3 = w3;
   w0 = pm != 1.0 ? pm * x0 : x0;
   w1 = pm != 1.0 ? pm * x1 : x1;
@@ -1168,19 +1169,15 @@ __device__ __forceinline__ void rw_solve(const SweepArgs& a, double (&r)[S],
 // Epilogue + coalesced store of rows 1..m of the warp's lines from the line buffer (at(p) =
 // row p): the G lanes of a line take consecutive rows (G * 8 = 128- or 256-byte runs), each
 // lane S of them; an idle sub-warp (odd line count) joins the shuffles but stores nothing.
-// Divergence test of the row-warp store pass: max|x| and a NaN/inf sentinel (x*0 is NaN
-// exactly for non-finite x), 2 fp64 operations per node instead of a compare-and-or; the
-// decision (non-finite, or max|x| above the threshold, schemes.py:417-421) is taken once per
-// thread at the end.
+// Divergence test of the row-warp store pass (non-finite, or |x| above the threshold,
+// schemes.py:417-421): one compare with the hoisted clamped threshold per node (an fmax
+// accumulator measured 9% of the kernel's instructions: fp64 fmax is a compare-select chain).
 struct DivAcc {
-  double mx = 0.0, nz = 0.0;
-  __device__ __forceinline__ void add(double x) {
-    mx = fmax(mx, fabs(x));
-    nz = fma(x, 0.0, nz);
-  }
-  __device__ __forceinline__ bool bad(double thr) const {
-    return !(nz == 0.0) || !(mx <= fmin(thr, 1.7976931348623157e308));
-  }
+  double thr;       // threshold clamped to DBL_MAX: +-inf and NaN fail the one comparison
+  bool b = false;
+  __device__ __forceinline__ explicit DivAcc(double t) : thr(fmin(t, 1.7976931348623157e308)) {}
+  __device__ __forceinline__ void add(double x) { b |= !(fabs(x) <= thr); }
+  __device__ __forceinline__ bool bad(double) const { return b; }
 };
 
 // Epilogue + coalesced store of rows 1..m of the warp's lines from the line buffer (at(p) =
@@ -1275,7 +1272,7 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
   const int itop = a.on ? a.o0 + a.on : L.n0 - 2;  // planes itop, itop-1, ... (reverse)
   double* W = Wb + warp * RW::WD + sub * RW::LW;          // this lane's line
   double* sR = Wb + warp * RW::WD + NL * RW::LW + sub * RW::RW;
-  DivAcc acc;
+  DivAcc acc(a.thr);
   const int nlp = BATCH ? nlines / L.nb : nlines;  // lines per grid (batched: nb grids)
   for (int wl = blockIdx.x * kRWarps + warp; wl * NL < nlines; wl += gridDim.x * kRWarps) {
     const int line = wl * NL + sub;
@@ -1334,10 +1331,16 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
     }
     __syncwarp();
 
-    rw_store<S, G>(a, [&](int p) { return W[RW::pos(p)]; }, valid, seg, sbits, FP, base, acc);
+    if (G % S == 0) {  // rows 1 + seg + G*k sit at pos(1 + seg) + k*(G + 2G/S): no division
+      const int p0 = RW::pos(1 + seg);
+      rw_store<S, G>(a, [&](int p) { return W[p0 + ((p - 1 - seg) / G) * (G + 2 * G / S)]; },
+                     valid, seg, sbits, FP, base, acc);
+    } else {
+      rw_store<S, G>(a, [&](int p) { return W[RW::pos(p)]; }, valid, seg, sbits, FP, base, acc);
+    }
     if (BATCH && a.check) {  // batched: the line's own grid (lines of a warp may differ)
       if (acc.bad(a.thr)) atomicMin(a.div_step + b, a.step);
-      acc = DivAcc();
+      acc = DivAcc(a.thr);
     }
     __syncwarp();  // the line buffers are restaged by the next lines
   }
@@ -1493,7 +1496,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   ulonglong2 ddn;
   double bfn;
   fetch(wl0, ddn, bfn);
-  DivAcc acc;
+  DivAcc acc(a.thr);
   int it = 0;
   for (int wl = wl0; wl * NL < nlines; wl += stride, ++it) {
     const int b = it & 1;
@@ -1529,7 +1532,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     rw_store<S, G>(a, [&](int p) { return W[swz(p - 1)]; }, valid, seg, sbits, FP, base, acc);
     if (BATCH && a.check) {  // batched: the line's own grid (lines of a warp may differ)
       if (acc.bad(a.thr)) atomicMin(a.div_step + gb, a.step);
-      acc = DivAcc();
+      acc = DivAcc(a.thr);
     }
     // the buffer's generic-proxy reads/writes are ordered before the next tensor copy into it
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
