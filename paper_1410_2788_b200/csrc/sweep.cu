@@ -121,6 +121,48 @@ __device__ __forceinline__ void flow_group(const SweepArgs& a, const double* FP,
   }
 }
 
+// pm * flow of four independent nodes in place, the small-argument polynomial (|w| <= 2: all
+// solvent nodes of the protein configs) for all of them, branch-free with the identity of an
+// ion-free solute palette selected per node; flow_sm only for the rare others (|w| > 2, NaN,
+// a solute palette with ions, no small form).  Seven more DFMA per node than the tiny tier
+// but no divergent fallback near the molecule (k_sweep_rowlean: the lanes of a warp sit 16
+// rows apart on the same line).
+__device__ __forceinline__ void flow_group_small(const SweepArgs& a, const double* FP,
+                                                 double& w0, double& w1, double& w2, double& w3,
+                                                 uint32_t s0, uint32_t s1, uint32_t s2,
+                                                 uint32_t s3, double pm) {
+  const double x0 = flow_small(w0, a.fsmall), x1 = flow_small(w1, a.fsmall);
+  const double x2 = flow_small(w2, a.fsmall), x3 = flow_small(w3, a.fsmall);
+  const unsigned big = (fabs(w0) <= kFSmallX ? 0u : 1u) | (fabs(w1) <= kFSmallX ? 0u : 2u) |
+                       (fabs(w2) <= kFSmallX ? 0u : 4u) | (fabs(w3) <= kFSmallX ? 0u : 8u);
+  const unsigned sol = s0 | (s1 << 1) | (s2 << 2) | (s3 << 3);
+  const bool sol_id = a.decay1 >= 1.0;  // launch-uniform
+  const unsigned need = a.fsmall_on ? (sol_id ? (big & ~sol) : (big | sol)) : 15u;
+  const double in0 = w0, in1 = w1, in2 = w2, in3 = w3;
+  w0 = (sol_id && s0) ? w0 : x0;
+  w1 = (sol_id && s1) ? w1 : x1;
+  w2 = (sol_id && s2) ? w2 : x2;
+  w3 = (sol_id && s3) ? w3 : x3;
+  if (pm != 1.0) {
+    w0 *= pm;
+    w1 *= pm;
+    w2 *= pm;
+    w3 *= pm;
+  }
+  if (!need) return;
+#pragma unroll 1
+  for (unsigned m = need; m; m &= m - 1) {
+    const int u = __ffs(m) - 1;
+    const double w = u == 0 ? in0 : (u == 1 ? in1 : (u == 2 ? in2 : in3));
+    const uint32_t s = u == 0 ? s0 : (u == 1 ? s1 : (u == 2 ? s2 : s3));
+    const double r = flow_sm(a, FP, w, s, pm);
+    if (u == 0) w0 = r;
+    else if (u == 1) w1 = r;
+    else if (u == 2) w2 = r;
+    else w3 = r;
+  }
+}
+
 __host__ __device__ __forceinline__ bool uses_flow(int pro, int epi) {
   return pro == PRO_FLOW || epi == EPI_FLOW || epi == EPI_AOS0;
 }
@@ -1544,11 +1586,468 @@ __global__ void __launch_bounds__(NW * 32, 1)
 }
 
 // ---------------------------------------------------------------------------------------
+// Row sweeps (axis 2), TMA in and TMA out: every warp owns three line buffers in shared
+// memory.  A line arrives by one tensor copy (128-byte swizzle, mbarrier), lane `seg` takes
+// its 16 rows into registers, the line is solved inside the warp (rw_solve), the LODIE2 flow
+// and the divergence test run on those registers, the rows go back to the same buffer and one
+// tensor store writes the line out.  The lanes never address global memory for the field, no
+// transposing store pass, no per-node predicates: the far face row m+1 travels with the line
+// and is written back unchanged.  Copies of the lines two iterations ahead are in flight while
+// a line is solved; the store of a buffer has a whole iteration to drain before the buffer is
+// refilled.  One block of NW warps per SM, so every lane may keep its rows and the flow's
+// temporaries in up to 128 registers.  Lines of 16 x G rows (m + 1 = 256, 512), single grid,
+// LOD epilogues (store, LODIE1 source, LODIE2 flow); source and destination faces must agree
+// (march buffers, or in place).  Descriptors: line-major, solute bits in row order (lm = 2).
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, int c0, int c1, int c2,
+                                             const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+          reinterpret_cast<unsigned long long>(tm)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int G, int NW>
+struct RowLean {
+  static constexpr int S = 16, NL = 32 / G, LD = G * S, WB = NL * LD, NB = 3;
+  static constexpr size_t lines_bytes = (size_t)NW * NB * WB * sizeof(double);
+  static constexpr size_t smem(int fpoly_n) {
+    return 1024 + lines_bytes +
+           sizeof(double) * (G * (G + 2) + NW * NL * (G + 2) + kFlowHdr + fpoly_n + 2) +
+           sizeof(unsigned long long) * NW * NB;
+  }
+};
+
+template <int G, int NW, int FLOWK>
+__global__ void __launch_bounds__(NW * 32, 1)
+    k_sweep_rowlean(const SweepArgs a, const int nlines, const __grid_constant__ CUtensorMap tms,
+                    const __grid_constant__ CUtensorMap tmd) {
+  extern __shared__ unsigned char smraw[];
+  using RL = RowLean<G, NW>;
+  constexpr int S = RL::S, NL = RL::NL, LD = RL::LD, WB = RL::WB, NB = RL::NB;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int NT = NW * 32;
+  constexpr bool FLOW = FLOWK != 0, FSM = FLOWK == 2;  // flow epilogue and its form (launch)
+  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sub = lane / G, seg = lane % G;
+  double* Lb = reinterpret_cast<double*>(
+      smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u));  // 1024-aligned line buffers
+  double* Mi = Lb + NW * NB * WB;        // G x (G + 2)
+  double* sRb = Mi + G * (G + 2);        // NW * NL * (G + 2)
+  double* FP = sRb + NW * NL * (G + 2);  // flow tables at FP + kFlowHdr
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(
+      FP + kFlowHdr + (FLOW ? a.fpoly_n + (a.fpoly_n & 1) : 0));
+  if (a.static_ok)
+    for (int c = tid; c < G * (G + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
+  if (FLOW)
+    for (int c = tid; c < a.fpoly_n / 2; c += NT) cp_async16(FP + kFlowHdr + 2 * c, a.fpoly + 2 * c);
+  asm volatile("cp.async.commit_group;\n" ::);
+  if (tid < NW * NB) mbar_init(bars + tid, NL);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  cp_async_wait_all();
+  __syncthreads();
+  if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
+
+  const Layout& L = a.L;
+  const int m = a.m, K = L.n1 - 2;
+  const int itop = a.on ? a.o0 + a.on : L.n0 - 2;  // planes itop, itop-1, ... (reverse)
+  double* sR = sRb + (warp * NL + sub) * (G + 2);
+  unsigned long long* bar = bars + warp * NB;
+  double* Wq = Lb + warp * NB * WB + sub * LD;  // buffer b of this lane's line: Wq + b * WB
+  // Line cursor of this lane: line = (warp-iteration) * NL + sub walks by `dl` lines per
+  // iteration; (i, j) follow without divisions.
+  const int dl = gridDim.x * NW * NL, dq = dl / K, dr = dl - dq * K;
+  int line = (blockIdx.x * NW + warp) * NL + sub;
+  int ci = itop - line / K, cj = 1 + line % K;
+  auto advance = [&](int& ln, int& i, int& j) {
+    ln += dl;
+    i -= dq;
+    j += dr;
+    if (j > K) {
+      j -= K;
+      i -= 1;
+    }
+  };
+  // seg == 0 lanes: tensor copy of line (i, j) into buffer b (every sub-line arrives once per
+  // phase, a line past the end with no bytes)
+  auto issue = [&](int ln, int i, int j, int b) {
+    if (ln < nlines) {
+      mbar_expect_tx(bar + b, (unsigned)(LD * sizeof(double)));
+      tma_load_3d(Wq + b * WB, &tms, 0, 0, i * L.n1 + j, bar + b);
+    } else {
+      mbar_arrive(bar + b);
+    }
+  };
+  // descriptor words and low-face fold value of a line, fetched one iteration ahead
+  auto fetch = [&](int ln, int i, int j, ulonglong2& dd, double& bf) {
+    dd = make_ulonglong2(0ull, 0ull);
+    bf = 0.0;
+    if (ln < nlines) {
+      dd = *reinterpret_cast<const ulonglong2*>(a.desc + 2 * (line_desc(L, i, j) * G + seg));
+      const long long bs = L.at(i, j, 0);
+      if (seg == 0) bf = a.bnd[bs];
+      else if (seg == G - 1) bf = a.bnd[bs + a.hi_off];
+    }
+  };
+  int l1 = line, i1 = ci, j1 = cj;  // one iteration ahead
+  advance(l1, i1, j1);
+  int l2 = l1, i2 = i1, j2 = j1;    // two iterations ahead
+  advance(l2, i2, j2);
+  if (seg == 0) {
+    issue(line, ci, cj, 0);
+    issue(l1, i1, j1, 1);
+  }
+  ulonglong2 ddn;
+  double bfn;
+  fetch(line, ci, cj, ddn, bfn);
+  const double thrc = fmin(a.thr, 1.7976931348623157e308);
+  const int thrH = thrc >= 0.0 ? __double2hiint(thrc) : -1;
+  bool bad = false;
+  // swizzled offsets of the lane's eight 16-byte units inside its 128-byte chunk
+  const int x7 = seg & 7;
+  int it = 0;
+  for (int w0 = blockIdx.x * NW + warp; w0 * NL < nlines; w0 += gridDim.x * NW, ++it) {
+    const int b = it % NB;
+    const bool valid = line < nlines;
+    const long long base = L.at(valid ? ci : 1, valid ? cj : 1, 0);
+    const unsigned long long amask = ddn.x;
+    const uint32_t sbits = (uint32_t)ddn.y, cmask = (uint32_t)(ddn.y >> 32);
+    const double bfold = bfn;
+    fetch(l1, i1, j1, ddn, bfn);
+    double* W = Wq + b * WB + seg * 16;  // this lane's chunk
+    mbar_wait(bar + b, (unsigned)(it / NB) & 1u);
+
+    double r[S];
+#pragma unroll
+    for (int q = 0; q < S; q += 2) {
+      const double2 v = valid ? *reinterpret_cast<const double2*>(W + (((q >> 1) ^ x7) << 1))
+                              : make_double2(0.0, 0.0);
+      r[q] = v.x;
+      r[q + 1] = v.y;
+    }
+    const double face = r[S - 1];  // last lane: row m + 1, written back unchanged
+    rw_solve<S, G>(a, r, amask, cmask, bfold, valid, seg, a.tab, Mi, sR, base);
+    unsigned need = 0u;  // FLOWK == 3: rows whose flow is evaluated from the buffer below
+    if (FLOWK == 3) {
+      // Flow on the lane's 16 rows, eight interleaved Horner chains at a time, the tier chosen
+      // per warp and half (no divergence): the tiny-argument polynomial when every row of the
+      // warp's half is solvent with |w| <= 0.5 (the far field, most of the grid), else the
+      // small-argument polynomial (|w| <= 2) with the solute rows keeping w.  Rows outside
+      // both (|w| > 2, NaN, a solute palette with ions, no small form) are redone from the
+      // buffer below (need).
+      const unsigned force = a.fsmall_on ? sbits : 0xffffu;
+      const unsigned ident = a.decay1 >= 1.0 ? sbits : 0u;  // ion-free solute: w is final
+#pragma unroll
+      for (int h = 0; h < S; h += 8) {
+        bool tiny = ((force >> h) & 0xffu) == 0u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) tiny = tiny && fabs(r[h + u]) <= kFTinyX;
+        double t[8], p[8];
+        if (__all_sync(FULL, tiny)) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            t[u] = fma(r[h + u], r[h + u], -0.5 * kFTinyX * kFTinyX);
+            p[u] = a.ftiny[kFTinyN - 1];
+          }
+#pragma unroll
+          for (int c = kFTinyN - 2; c >= 0; --c)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) p[u] = fma(p[u], t[u], a.ftiny[c]);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) r[h + u] *= p[u];
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            t[u] = fma(r[h + u], r[h + u], -0.5 * kFSmallX * kFSmallX);
+            p[u] = a.fsmall[kFSmallN - 1];
+          }
+#pragma unroll
+          for (int c = kFSmallN - 2; c >= 0; --c)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) p[u] = fma(p[u], t[u], a.fsmall[c]);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const bool keep = !(fabs(r[h + u]) <= kFSmallX) || ((force >> (h + u)) & 1u);
+            need |= keep ? (1u << (h + u)) : 0u;
+            r[h + u] = keep ? r[h + u] : r[h + u] * p[u];
+          }
+        }
+      }
+      need &= ~ident;
+      if (seg == G - 1) need &= 0x7fffu;  // the face row
+    } else if (FLOW) {
+#pragma unroll
+      for (int q = 0; q < S; q += 4)
+        if (FSM)
+          flow_group_small(a, FP, r[q], r[q + 1], r[q + 2], r[q + 3], (sbits >> q) & 1u,
+                           (sbits >> (q + 1)) & 1u, (sbits >> (q + 2)) & 1u,
+                           (sbits >> (q + 3)) & 1u, 1.0);
+        else
+          flow_group(a, FP, r[q], r[q + 1], r[q + 2], r[q + 3], (sbits >> q) & 1u,
+                     (sbits >> (q + 1)) & 1u, (sbits >> (q + 2)) & 1u, (sbits >> (q + 3)) & 1u,
+                     1.0);
+    }
+    if (seg == G - 1) r[S - 1] = 0.0;
+    // divergence test (schemes.py:417-421) on the high words: |x| > thr for sure when the
+    // high word is above the threshold's, undecided only when equal (exact compare then)
+    int mx = 0;
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+      if (!((need >> q) & 1u)) mx = max(mx, __double2hiint(r[q]) & 0x7fffffff);
+    if (mx >= thrH) {
+      if (mx > thrH) {
+        bad = true;
+      } else {
+#pragma unroll
+        for (int q = 0; q < S; ++q) bad |= !(fabs(r[q]) <= thrc);
+      }
+    }
+    if (seg == G - 1) r[S - 1] = face;
+    if (valid) {
+#pragma unroll
+      for (int q = 0; q < S; q += 2)
+        *reinterpret_cast<double2*>(W + (((q >> 1) ^ x7) << 1)) = make_double2(r[q], r[q + 1]);
+    }
+    if (FLOWK == 3 && valid) {  // the other rows, one at a time, in the buffer
+#pragma unroll 1
+      for (unsigned nm = need; nm; nm &= nm - 1) {
+        const int u = __ffs(nm) - 1;
+        double* slot = W + ((((u >> 1) ^ x7) << 1) | (u & 1));
+        const double x = flow_sm(a, FP, *slot, (sbits >> u) & 1u, 1.0);
+        *slot = x;
+        bad |= !(fabs(x) <= thrc);
+      }
+    }
+    // the lanes' writes are ordered before the tensor store reads the buffer
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (seg == 0) {
+      if (valid) tma_store_3d(&tmd, 0, 0, ci * L.n1 + cj, Wq + b * WB);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      // the buffer refilled next was stored one iteration ago: all but the newest group done
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      if ((w0 + 2 * gridDim.x * NW) * NL < nlines) issue(l2, i2, j2, (it + 2) % NB);
+    }
+    line = l1; ci = i1; cj = j1;
+    l1 = l2; i1 = i2; j1 = j2;
+    advance(l2, i2, j2);
+  }
+  if (seg == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (a.check && __any_sync(FULL, bad) && lane == 0) atomicMin(a.div_step, a.step);
+}
+
+// ---------------------------------------------------------------------------------------
+// Fused axis-1 + axis-2 sweeps of a LOD step (schemes.py:301-311, order 0 -> 1 -> 2 kept).
+// The lines of both families lie inside one i-plane, so one persistent launch runs the
+// axis-1 column tiles of plane p and, a few planes later, the axis-2 lines of plane p, which
+// read the axis-1 output from L2 and store in place over it: the intermediate field never
+// travels to HBM and back (step traffic 48 -> 32 B per node).  Blocks take work items from
+// one global queue (atomic counter, the next item claimed while the current one runs).  The
+// queue order IS the dependency order -- `lag` planes of column tiles, then for every plane
+// its line groups followed by the column tiles of plane p + lag -- and an item only ever
+// waits for earlier items, all of which are held by running blocks, so the launch cannot
+// deadlock whatever the number of resident blocks.  A column tile publishes its plane with a
+// fence + counter increment; a line group spins (one thread, acquire loads) until its plane's
+// counter reaches the tiles per plane.  Both sweeps use the kernels' own bodies: col_body
+// (register-direct column tiles) and the row-warp line solve (rw_solve / rw_store), with the
+// reduced-system scratch of the one and the line buffers of the other sharing shared memory.
+// Requires square planes and equal axis coefficients (one table set, P = G separators).
+struct FuseCtl {
+  int* q;      // q[0] next item, q[1] blocks that left, q[2 + p] finished column tiles of plane p
+  int np;      // interior planes
+  int n1, n2;  // items per plane: axis-1 column tiles, axis-2 line groups
+  int lag;     // planes of column tiles queued ahead of the line groups (1 <= lag <= np)
+};
+
+template <int S, int P, int LB, int G>
+struct Fused12 {
+  static constexpr int NT = LB * P, NW = NT / 32;
+  using RW = RowWarp<S, G>;
+  static constexpr int XD = 4 * NT, WD = NW * RW::WD;
+  static constexpr int UD = ((XD > WD ? XD : WD) + 1) & ~1;  // scratch union, doubles
+  static constexpr size_t smem(int fpoly_n) {
+    return sizeof(double) * (kTabDoubles + P * (P + 2) + UD + kFlowHdr + fpoly_n + 2);
+  }
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int S, int P, int LB, int G>
+__global__ void __launch_bounds__(LB * P, 3)
+    k_sweep_fused12(const SweepArgs a1, const SweepArgs a2, const FuseCtl c) {
+  static_assert(P == G, "one reduced-system shape for both axes");
+  extern __shared__ double sm[];
+  using F = Fused12<S, P, LB, G>;
+  using RW = RowWarp<S, G>;
+  constexpr int NT = F::NT, NW = F::NW, NL = RW::NL;
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ int s_item;
+  const int tid = threadIdx.y * LB + threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int dstep = a2.div_step ? *((volatile int*)a2.div_step) : INT_MAX;
+  double* T = sm;
+  double* Mi = T + kTabDoubles;
+  double* U = Mi + P * (P + 2);  // column tiles: reduced-system scratch; line groups: buffers
+  double* FP = U + F::UD;
+  stage_tables<P>(a2, T, Mi, FP, tid, NT);
+  asm volatile("cp.async.commit_group;\n" ::);
+  if (dstep < a2.step) {  // an earlier step diverged: nothing more to compute
+    cp_async_wait_all();
+    return;
+  }
+  if (tid == 0) s_item = atomicAdd(c.q, 1);
+  cp_async_wait_all();
+  __syncthreads();
+
+  const Layout& L = a2.L;
+  const int K = L.n1 - 2;  // lines per plane (either family: square planes)
+  const int nitems = c.np * (c.n1 + c.n2), per = c.n1 + c.n2;
+  const int head = c.lag * c.n1, full = c.np - c.lag;
+  const int sub = lane / G, seg = lane % G;
+  double* W = U + warp * RW::WD + sub * RW::LW;  // this lane's line buffer
+  double* sR = U + warp * RW::WD + NL * RW::LW + sub * RW::RW;
+  DivAcc acc(a2.thr);
+  int item = s_item;
+  while (item < nitems) {
+    int nxt = 0;
+    if (tid == 0) nxt = atomicAdd(c.q, 1);  // claimed now, taken up when this item is done
+    int kind, plane, si;  // kind 1: column tile si of plane, 2: line group si of plane
+    if (item < head) {
+      kind = 1;
+      plane = item / c.n1;
+      si = item - plane * c.n1;
+    } else {
+      const int r = item - head;
+      if (r < full * per) {
+        const int grp = r / per, w = r - grp * per;
+        kind = w < c.n2 ? 2 : 1;
+        plane = w < c.n2 ? grp : grp + c.lag;
+        si = w < c.n2 ? w : w - c.n2;
+      } else {
+        const int r2 = r - full * per;
+        kind = 2;
+        plane = full + r2 / c.n2;
+        si = r2 % c.n2;
+      }
+    }
+    if (kind == 1) {  // ---- axis-1 column tile (as k_sweep_col) ----
+      TileGeo g;
+      g.b = 0;
+      g.c0 = 1 + si * LB;
+      g.outer = plane + 1;
+      g.ncols = min(LB, (L.n2 - 2) + 1 - g.c0);
+      g.base = L.at(g.outer, 0, g.c0);
+      g.stride = (int)L.pitch;
+      const int m = a1.m, i0 = threadIdx.y * S, st = g.stride;
+      const bool act = (int)threadIdx.x < g.ncols;
+      const long long gl = g.base + threadIdx.x;
+      unsigned long long amask = 0ull;
+      if (act) amask = *col_desc<P>(a1, g);
+      double r[S];
+      const double* srow = a1.src + gl + (long long)(i0 + 1) * st;
+      if (act && i0 + S <= m + 1) {
+#pragma unroll
+        for (int j = 0; j < S; ++j) r[j] = srow[j * st];
+      } else {
+#pragma unroll
+        for (int j = 0; j < S; ++j) r[j] = (act && i0 + 1 + j <= m + 1) ? srow[j * st] : 0.0;
+      }
+      double bfold = 0.0;
+      if (act) {
+        if (threadIdx.y == 0) bfold = a1.bnd[gl];
+        else if ((int)threadIdx.y == (m - 1) / S) bfold = a1.bnd[gl + a1.hi_off];
+      }
+      col_body<S, P, false, LB>(a1, g, r, 0.0, 0.0, amask, 0ull, bfold, T, Mi, U, FP);
+      if (tid == 0) s_item = nxt;
+      __syncthreads();  // every store of the tile is issued; the scratch is free again
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(c.q + 2 + plane, 1);
+      }
+    } else {  // ---- axis-2 line group: NW warps x NL lines of plane `plane` ----
+      if (tid == 0) {
+        const int* d = c.q + 2 + plane;
+        while (ld_acquire(d) < c.n1) __nanosleep(64);
+      }
+      __syncthreads();
+      const int m = a2.m;
+      const int ln = (si * NW + warp) * NL + sub;
+      const bool valid = ln < K;
+      const int i = plane + 1, j = valid ? 1 + ln : 1;
+      const long long base = L.at(i, j, 0);
+      unsigned long long amask = 0ull;
+      uint32_t sbits = 0u, cmask = 0u;
+      double bfold = 0.0;
+      if (valid) {
+        const double* gsrc = a2.src + base + 1;
+#pragma unroll
+        for (int q = 0; q < S / 2; ++q) {
+          const int ch = seg + G * q;  // chunk: rows 2ch+1, 2ch+2 (one segment, S even)
+          cp_async16(W + RW::pos(2 * ch + 1), gsrc + 2 * ch);
+        }
+        const ulonglong2 dd = *reinterpret_cast<const ulonglong2*>(
+            a2.desc + 2 * (line_desc(L, i, j) * G + seg));
+        amask = dd.x;
+        sbits = (uint32_t)dd.y;
+        cmask = (uint32_t)(dd.y >> 32);
+        if (seg == 0) bfold = a2.bnd[base];
+        else if (seg == (m - 1) / S) bfold = a2.bnd[base + a2.hi_off];
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+      cp_async_wait_all();
+      __syncwarp();
+      double r[S];
+#pragma unroll
+      for (int q = 0; q < S; q += 2) {
+        const double2 v = valid ? *reinterpret_cast<const double2*>(W + 2 + seg * RW::SP + q)
+                                : make_double2(0.0, 0.0);
+        r[q] = v.x;
+        r[q + 1] = v.y;
+      }
+      rw_solve<S, G>(a2, r, amask, cmask, bfold, valid, seg, T, Mi, sR, base);
+      if (valid) {
+#pragma unroll
+        for (int q = 0; q < S; q += 2)
+          *reinterpret_cast<double2*>(W + 2 + seg * RW::SP + q) = make_double2(r[q], r[q + 1]);
+      }
+      __syncwarp();
+      if (G % S == 0) {
+        const int p0 = RW::pos(1 + seg);
+        rw_store<S, G>(a2, [&](int p) { return W[p0 + ((p - 1 - seg) / G) * (G + 2 * G / S)]; },
+                       valid, seg, sbits, FP, base, acc);
+      } else {
+        rw_store<S, G>(a2, [&](int p) { return W[RW::pos(p)]; }, valid, seg, sbits, FP, base,
+                       acc);
+      }
+      if (tid == 0) s_item = nxt;
+      __syncthreads();  // line buffers and the item slot are reused
+    }
+    item = s_item;
+  }
+  if (a2.check && __any_sync(FULL, acc.bad(a2.thr)) && lane == 0)
+    atomicMin(a2.div_step, a2.step);
+  // The last block to leave resets the queue for the next launch.
+  __syncthreads();
+  if (tid == 0) s_item = atomicAdd(c.q + 1, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (s_item)
+    for (int t = tid; t < 2 + c.np; t += NT) c.q[t] = 0;
+}
+
+// ---------------------------------------------------------------------------------------
 // Segment descriptors, built once per march and axis from the 1-byte node codes:
 //   word 0: bit j = eps bit (axis) of the node of row i0+j, j = 0..S (zero past node m+1)
 //   word 1: bits 0..S-1 solute bit of the nodes of rows i0..i0+S-1; bits 32.. charged bits
 // Layout: ((outer-1)*P + seg)*K + (line-1); line-major ((outer-1)*K + line-1)*P + seg for the
-// row-warp sweeps (lm).
+// row-warp sweeps (lm = 1: solute bits in the store-pass order of k_sweep_rowwarp / rowtma;
+// lm = 2: in row order, k_sweep_rowlean).
 __global__ void k_build_desc(const Layout L, int axis, int S, int P, int lm,
                              const uint8_t* __restrict__ codes,
                              unsigned long long* __restrict__ desc) {
@@ -1581,11 +2080,11 @@ __global__ void k_build_desc(const Layout L, int axis, int S, int P, int lm,
       const uint32_t c = codes[base + p * stride];
       w0 |= (unsigned long long)((c >> sh) & 1u) << j;
       if (j < S && p <= m) {
-        if (!lm) w1 |= (unsigned long long)(c & 1u) << j;
+        if (lm != 1) w1 |= (unsigned long long)(c & 1u) << j;
         w1 |= (unsigned long long)((c >> 4) & 1u) << (32 + j);
       }
     }
-    if (lm)  // row-warp store pass: lane `seg` stores rows 1 + seg + P*q, q = 0..S-1; its
+    if (lm == 1)  // row-warp store pass: lane `seg` stores rows 1 + seg + P*q, q = 0..S-1; its
              // solute bits in that order (no per-node shuffle in the LODIE2 flow epilogue)
       for (int q = 0; q < S; ++q) {
         const int p = 1 + seg + P * q;
@@ -1785,6 +2284,15 @@ static int rowwarp_S(int m) {
   const int G = rowwarp_G(m);
   return G ? (m + 1) / G : 0;
 }
+// PBG_FUSED12=1: axis-1 and axis-2 sweeps of a LOD step in one launch (k_sweep_fused12).
+static bool fused12_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PBG_FUSED12");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 static bool rowwarp_ok(const SweepArgs& a, int axis) {
   static const bool on = [] {
     const char* e = getenv("PBG_ROWWARP");
@@ -1953,7 +2461,8 @@ static EncodeTiled encode_tiled() {
 
 // Tensor map of the axis-2 lines of a field: (16 doubles, chunk, line) with the line index
 // i*n1 + j, based at row 1 (k = 1, 256-byte aligned), 128-byte swizzle.
-static bool line_tensor_map(const SweepArgs& a, int box_chunks, CUtensorMap* tm) {
+static bool line_tensor_map(const SweepArgs& a, int box_chunks, CUtensorMap* tm,
+                            const double* field = nullptr) {
   EncodeTiled fn = encode_tiled();
   if (!fn) return false;
   const Layout& L = a.L;
@@ -1963,7 +2472,8 @@ static bool line_tensor_map(const SweepArgs& a, int box_chunks, CUtensorMap* tm)
   cuuint64_t strides[2] = {128, (cuuint64_t)L.pitch * sizeof(double)};
   cuuint32_t box[3] = {16, (cuuint32_t)box_chunks, 1};
   cuuint32_t es[3] = {1, 1, 1};
-  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)(a.src + kOff + 1), dims, strides,
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)((field ? field : a.src) + kOff + 1),
+            dims, strides,
             box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -1989,7 +2499,64 @@ static bool launch_rowtma_SG(const SweepArgs& a, cudaStream_t st) {
   return launch_rowtma_SGN<S, G, 20>(a, st);
 }
 
+// TMA-in / TMA-out row sweeps (k_sweep_rowlean): the default for 256- and 512-row lines of a
+// single grid with the LOD epilogues; PBG_ROWLEAN=0 keeps k_sweep_rowwarp / k_sweep_rowtma,
+// PBG_ROWLEAN_NW = warps per block (16 or 12).
+static bool rowlean_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PBG_ROWLEAN");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+static bool rowlean_ok(const SweepArgs& a) {
+  return rowlean_enabled() && a.L.nb == 1 && rowwarp_S(a.m) == 16 &&
+         (a.epi == EPI_STORE || a.epi == EPI_FLOW || a.epi == EPI_SRC);
+}
+
+template <int G, int NW>
+static bool launch_rowlean_GN(const SweepArgs& a, cudaStream_t st) {
+  CUtensorMap tms, tmd;
+  if (!line_tensor_map(a, G, &tms, a.src) || !line_tensor_map(a, G, &tmd, a.dst)) return false;
+  const int nlines = (a.on ? a.on : a.L.n0 - 2) * (a.L.n1 - 2);
+  const bool flow = a.epi == EPI_FLOW;
+  const size_t smem = RowLean<G, NW>::smem(flow ? a.fpoly_n : 0);
+  // PBG_FLOWK: 3 = tiny tier on all 16 rows at once, the others from the buffer (default);
+  // 2 = small form for all rows; 1 = flow_group (tiny tier + per-node fallback), as elsewhere
+  static const int fsm = [] {
+    const char* e = getenv("PBG_FLOWK");
+    const int v = e && *e ? atoi(e) : 3;
+    return v == 1 ? 0 : v;
+  }();
+  auto kern = !flow ? k_sweep_rowlean<G, NW, 0>
+                    : (fsm == 3 ? k_sweep_rowlean<G, NW, 3>
+                                : (fsm ? k_sweep_rowlean<G, NW, 2> : k_sweep_rowlean<G, NW, 1>));
+  const int per_block = NW * (32 / G);
+  const int grid = std::min((nlines + per_block - 1) / per_block,
+                            resident_blocks((const void*)kern, NW * 32, smem));
+  kern<<<grid, NW * 32, smem, st>>>(a, nlines, tms, tmd);
+  return true;
+}
+
+template <int G>
+static bool launch_rowlean_G(const SweepArgs& a, cudaStream_t st) {
+  static const int nw = [] {
+    const char* e = getenv("PBG_ROWLEAN_NW");
+    return e && *e ? atoi(e) : 16;
+  }();
+  if (nw == 12) return launch_rowlean_GN<G, 12>(a, st);
+  return launch_rowlean_GN<G, 16>(a, st);
+}
+
 static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
+  if (a.rw == 2) {
+    if (!a.faces_ok && a.src != a.dst)
+      return fail(PBG_E_INVALID, "row sweep: source and destination faces must agree");
+    const bool ok = rowwarp_G(a.m) == 32 ? launch_rowlean_G<32>(a, st) : launch_rowlean_G<16>(a, st);
+    if (!ok) return fail(PBG_E_CUDA, "tensor map encoding failed");
+    PBG_LAUNCH_CHECK("k_sweep_rowlean");
+    return PBG_OK;
+  }
   // TMA staging measured faster for 256-row lines (c3), slower for 512-row lines (c4:
   // 1.62 vs 1.59 ms/step; profiles/rowtma_ab_r02.txt); PBG_ROWTMA=0/1/2: off / auto / on.
   if (a.rw && rowwarp_S(a.m) == 16 &&
@@ -2028,6 +2595,59 @@ static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
     return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 1024)");
   }
   PBG_LAUNCH_CHECK("k_sweep_strided");
+  return PBG_OK;
+}
+
+
+// Fused axis-1 + axis-2 launch (k_sweep_fused12): LOD steps on square planes whose two axes
+// share their coefficient tables and whose axis-2 sweep is a row-warp sweep with as many
+// separators per line as the axis-1 column tiles (n1 = n2 = 257: 16 x 16; 513: 32 x 16).
+// Measured slower than the separate launches (c3 265 vs 208 us/step, c4 1.97 vs 1.50 ms,
+// profiles/fused12_ab_r02.txt: three blocks of 8 warps per SM, one work item at a time each,
+// hide less latency than the separate kernels' free-running warps), so PBG_FUSED12=1 only
+// selects it for comparison.
+static int fused12_shape(const SweepArgs& a1, const SweepArgs& a2) {
+  if (!fused12_enabled() || a2.rw != 1 || a1.cn || a2.cn || a1.L.nb != 1 || a1.L.n1 != a1.L.n2) return 0;
+  if (a1.pro != PRO_NONE || a1.epi != EPI_STORE || a1.has_extra || a1.ends || a1.check) return 0;
+  if (memcmp(&a1.co, &a2.co, sizeof(AxisCoef)) || memcmp(a1.tmid, a2.tmid, sizeof(a1.tmid)) ||
+      a1.static_ok != a2.static_ok)
+    return 0;
+  const int P = seg_P(1, a1.m), S = seg_S(a1.m, P);
+  if (P != rowwarp_G(a2.m) || S != rowwarp_S(a2.m) || S != 16) return 0;
+  return P == 16 || P == 32 ? P : 0;
+}
+
+template <int S, int P, int LB, int G>
+static void launch_fused12_T(const SweepArgs& a1, const SweepArgs& a2, int* q, cudaStream_t st) {
+  using F = Fused12<S, P, LB, G>;
+  const size_t smem = F::smem(flow_stage_n(a2));
+  auto kern = k_sweep_fused12<S, P, LB, G>;
+  const int resident = resident_blocks((const void*)kern, F::NT, smem);
+  FuseCtl c;
+  c.q = q;
+  c.np = a1.L.n0 - 2;
+  c.n1 = (a1.L.n2 - 2 + LB - 1) / LB;
+  c.n2 = (a2.L.n1 - 2 + F::NW * (32 / G) - 1) / (F::NW * (32 / G));
+  // every column tile of plane p is claimed at least `resident` items before the line groups
+  // of plane p, so those rarely have to wait
+  static const int lag_env = [] {
+    const char* e = getenv("PBG_FUSED12_LAG");
+    return e && *e ? atoi(e) : 0;
+  }();
+  const int lag = lag_env > 0 ? lag_env : resident / (c.n1 + c.n2) + 2;
+  c.lag = std::max(1, std::min(lag, c.np));
+  const int grid = std::min(c.np * (c.n1 + c.n2), resident);
+  kern<<<grid, dim3(LB, P), smem, st>>>(a1, a2, c);
+}
+
+static int launch_fused12(const SweepArgs& a1, const SweepArgs& a2, int* q, cudaStream_t st) {
+  if (!a2.fpoly) return fail(PBG_E_CUDA, "flow table allocation failed");
+  switch (fused12_shape(a1, a2)) {
+    case 16: launch_fused12_T<16, 16, 16, 16>(a1, a2, q, st); break;
+    case 32: launch_fused12_T<16, 32, 8, 32>(a1, a2, q, st); break;
+    default: return fail(PBG_E_UNSUPPORTED, "fused axis-1/axis-2 sweep: unsupported shape");
+  }
+  PBG_LAUNCH_CHECK("k_sweep_fused12");
   return PBG_OK;
 }
 
@@ -2285,6 +2905,7 @@ static long long desc_segments(const Layout& L, int axis, int P) {
 int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
                         cudaStream_t st) {
   a.rw = rowwarp_ok(a, axis) ? 1 : 0;
+  if (a.rw && a.faces_ok && rowlean_ok(a) && !fused12_enabled()) a.rw = 2;
   const int P = a.rw ? rowwarp_G(a.m) : seg_P(axis, a.m);
   const int S = a.rw ? rowwarp_S(a.m) : seg_S(a.m, P);
   const int lm = a.rw;
@@ -2460,6 +3081,9 @@ void march_axes(const pbg_march_desc* d, const Plan& plan, SweepArgs ax[3]) {
     dec_aos[b] = d->aos_literal ? std::exp(-k2 * dta) : std::exp(-4.0 * k2 * dta);
   }
   const double aos_pm = d->aos_literal ? 4.0 : 1.0;
+  // No ions anywhere (the vacuum marches of the energy pipeline): the LOD flow is the identity
+  // (_apply_flow returns w for decay >= 1, schemes.py:88-103), so those steps carry no flow stage.
+  const bool flow_id = dec_lod[0] >= 1.0 && dec_lod[1] >= 1.0;
 
   for (int axis = 0; axis < 3; ++axis) {
     SweepArgs a = base_args(g, &d->pal, axis, factor);
@@ -2471,7 +3095,7 @@ void march_axes(const pbg_march_desc* d, const Plan& plan, SweepArgs ax[3]) {
     a.thr = d->divergence_threshold;
     switch (plan.family) {
       case 0:  // LODIE1 / LODCN1: flow -> sweeps -> + dta*rho
-        if (axis == 0) {
+        if (axis == 0 && !flow_id) {
           a.pro = PRO_FLOW;
           set_decays(a, dec_lod[0], dec_lod[1]);
         }
@@ -2485,7 +3109,7 @@ void march_axes(const pbg_march_desc* d, const Plan& plan, SweepArgs ax[3]) {
           a.pro = PRO_SRC;
           a.pro_coef = dta;
         }
-        if (axis == 2) {
+        if (axis == 2 && !flow_id) {
           a.epi = EPI_FLOW;
           set_decays(a, dec_lod[0], dec_lod[1]);
         }
@@ -2580,6 +3204,7 @@ struct pbg_plan {
   bool extra = false;  // ADI / explicit Euler: march_extra per run
   int* dflag = nullptr;
   int* hflag = nullptr;  // pinned
+  int* fq = nullptr;     // work queue of the fused axis-1/axis-2 launch (zero between launches)
   cudaEvent_t e0 = nullptr, e1 = nullptr;
 };
 
@@ -2592,6 +3217,7 @@ static std::mutex g_prof_mu;
 static void plan_free(pbg_plan* p, cudaStream_t st) {
   for (int q = 0; q < 3; ++q) release_axis(p->aux[q], st);
   if (p->dflag) cudaFreeAsync(p->dflag, st);
+  if (p->fq) cudaFreeAsync(p->fq, st);
   if (p->hflag) cudaFreeHost(p->hflag);
   if (p->e0) cudaEventDestroy(p->e0);
   if (p->e1) cudaEventDestroy(p->e1);
@@ -2649,11 +3275,18 @@ extern "C" PBG_API int pbg_plan_create_batch(const pbg_march_desc* d, int32_t nb
   for (int axis = 0; axis < 3; ++axis) {
     p->ax[axis].L.nb = p->nb;
     p->ax[axis].L.bs = p->bs;
+    p->ax[axis].faces_ok = 1;  // both work buffers' faces hold the Dirichlet data (pbg.h)
     rc = prepare_axis(p->ax[axis], axis, d->codes, p->aux[axis], st);
     if (rc) return bail(rc);
   }
   if (cudaMallocAsync(&p->dflag, p->nb * sizeof(int), st) != cudaSuccess)
     return bail(fail(PBG_E_CUDA, "plan allocation failed"));
+  if (p->plan.family <= 1 && fused12_shape(p->ax[1], p->ax[2])) {
+    const size_t qb = (size_t)(2 + d->grid.n[0]) * sizeof(int);
+    if (cudaMallocAsync(&p->fq, qb, st) != cudaSuccess ||
+        cudaMemsetAsync(p->fq, 0, qb, st) != cudaSuccess)
+      return bail(fail(PBG_E_CUDA, "plan allocation failed"));
+  }
   if (cudaStreamSynchronize(st) != cudaSuccess)  // the plan may run on any stream
     return bail(fail(PBG_E_CUDA, "plan setup failed"));
   *out = p;
@@ -2720,7 +3353,11 @@ extern "C" PBG_API int pbg_plan_run_batch(pbg_plan* p, const double* initial, do
   const double field_mb = (double)nb * g->n[0] * g->n[1] * g->pitch * 8.0 / 1e6;
   const bool inpl_all =
       plan.family <= 1 && env_int("PBG_INPLACE", field_mb <= 256.0 ? 1 : 0) != 0;
-  const bool inpl = inpl_all || (lod_rw && (chunk > 0 || env_int("PBG_INPLACE2", 0) != 0));
+  // One launch for the axis-1 and axis-2 sweeps (k_sweep_fused12), axis 2 in place over the
+  // axis-1 output while it is still in L2.
+  const bool fused = p->fq != nullptr && chunk == 0;
+  const bool inpl =
+      inpl_all || fused || (lod_rw && (chunk > 0 || env_int("PBG_INPLACE2", 0) != 0));
   const int nplanes = g->n[0] - 2;
 
   std::vector<cudaEvent_t> kev;  // per-launch events when profiling is on
@@ -2769,6 +3406,8 @@ extern "C" PBG_API int pbg_plan_run_batch(pbg_plan* p, const double* initial, do
             rc = launch_sweep(a, q, st);
           }
         }
+      } else if (fused && axis >= 1) {
+        if (axis == 1) rc = launch_fused12(as[1], as[2], p->fq, st);
       } else if (!(chunk > 0 && axis == 2)) {
         rc = launch_sweep(as[axis], axis, st);
       }

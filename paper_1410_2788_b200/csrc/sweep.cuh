@@ -79,8 +79,13 @@ struct SweepArgs {
   const double* fpoly;
   int foff[2];
   int fpoly_n;
-  // Axis 2 runs the row-warp kernel (line-major descriptors, P = 32), set by prepare_axis.
+  // Axis 2 runs a row-warp kernel (line-major descriptors, P = lanes per line), set by
+  // prepare_axis: 1 = k_sweep_rowwarp / k_sweep_rowtma (solute bits in store-pass order),
+  // 2 = k_sweep_rowlean (solute bits in row order).
   int rw;
+  // The far faces (k = n2 - 1) of src and dst hold the same values (march work buffers, or
+  // src == dst): k_sweep_rowlean writes the face row back with the line.
+  int faces_ok;
   // Small-argument flow of palette 0 (pbg_internal.cuh flow_small), when decay0 < 1.
   int fsmall_on;
   double fsmall[kFSmallN];

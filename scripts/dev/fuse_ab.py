@@ -22,7 +22,15 @@ for _ in range(3):
     rep = pb.march(p, pb.MarchConfig(dt=c.dt, T=c.dt * 20, variant=v))
     best = min(best, rep.wall_time / rep.steps_taken)
 u = rep.final.data
-print(json.dumps({"us": best * 1e6, "sha": hashlib.sha256(u.tobytes()).hexdigest()[:16]}))
+from paper_1410_2788_b200 import _native as nat
+lib = nat.lib()
+lib.pbg_set_profiling(1)
+pb.march(p, pb.MarchConfig(dt=c.dt, T=c.dt * 20, variant=v))
+ms = (ctypes.c_double * 3)(); n = (ctypes.c_int64 * 3)()
+lib.pbg_get_profile(ms, n)
+lib.pbg_set_profiling(0)
+ax = [round(1e3 * ms[q] / max(1, n[q]), 1) for q in range(3)]
+print(json.dumps({"us": round(best * 1e6, 1), "axes_us": ax, "sha": hashlib.sha256(u.tobytes()).hexdigest()[:16]}))
 '''.replace("ROOT", repr(ROOT))
 # usage: fuse_ab.py CONFIGS VARIANTS ENVS_JSON, e.g. c3,c4 LODIE2 '[{}, {"PBG_ROWTMA": "0"}]'
 keys = sys.argv[1].split(",") if len(sys.argv) > 1 else ["c3", "c4"]
