@@ -406,8 +406,10 @@ def main():
                          "kernel": ["k_sweep_col axis 0 (register-direct column tiles, "
                                     "+ source)",
                                     "k_sweep_col axis 1 (register-direct column tiles)",
-                                    ({513: "k_sweep_rowwarp axis 2 (one line per warp, + flow)",
-                                      257: "k_sweep_rowwarp axis 2 (two lines per warp, + flow)",
+                                    ({513: "k_sweep_rowlean axis 2 (TMA in / TMA out, one line per "
+                                           "warp, + flow)",
+                                      257: "k_sweep_rowlean axis 2 (TMA in / TMA out, two lines per "
+                                           "warp, + flow)",
                                       129: "k_sweep_rowwarp axis 2 (two lines per warp, + flow)",
                                       97: "k_sweep_rowwarp axis 2 (four lines per warp, + flow)"}
                                      .get(c.n, "k_sweep_strided axis 2 (row tiles, + flow)"))][dom],

@@ -234,6 +234,7 @@ extern "C" PBG_API int pbg_slab_create(const pbg_march_desc* d, int32_t rank, in
   h->recv = recv;
   march_axes(d, plan, h->ax);
   for (int axis = 0; axis < 3; ++axis) {
+    h->ax[axis].faces_ok = 1;  // both work buffers' faces hold the Dirichlet data (pbg.h)
     rc = prepare_axis(h->ax[axis], axis, d->codes, h->aux[axis], st);
     if (rc) {
       pbg_slab_destroy(h, stream);

@@ -62,6 +62,12 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Which second tile the epilogue needs: 0 none, 1 the raw field (AOS0), 2 the accumulator.
 __host__ __device__ __forceinline__ int epi_needs(int epi) {
   return epi == EPI_AOS0 ? 1
@@ -850,6 +856,18 @@ __device__ __forceinline__ void fix_regs(double (&r)[S], unsigned cmask, double 
   }
 }
 
+// Next row of a strided line: the pointer advances by one 64-bit add per row (two integer
+// instructions); left to itself the compiler rebuilds every row address from j * stride with
+// uniform multiplies, sign extensions and carries (~5.5 instructions per row, 24% of the
+// column kernels' instructions, profiles/ncu_r02b).  The empty asm keeps the running pointer
+// opaque.
+template <typename T>
+__device__ __forceinline__ T* next_row(T* p, long long st) {
+  p += st;
+  asm volatile("" : "+l"(p));
+  return p;
+}
+
 // Per-tile work of the column kernels once the thread's rows are in registers: r[j] = row
 // i0+1+j of the line (rows past m+1 zero), wl / wr = raw rows i0 and i0+S+1 (CN only).
 // Prologue, CN explicit half, folds, elimination, reduced system (block-wide barriers: every
@@ -940,8 +958,12 @@ __device__ __forceinline__ void col_body(const SweepArgs& a, const TileGeo& g, d
   bool bad = false;
   if ((epi == EPI_STORE || epi == EPI_SRC || epi == EPI_MAOS0) && !a.check) {
     if (i0 + S <= m) {  // whole segment inside the line: no per-row predicates
+      double* dp = drow;
 #pragma unroll
-      for (int j = 0; j < S; ++j) drow[j * st] = r[j];
+      for (int j = 0; j < S; ++j) {
+        *dp = r[j];
+        if (j + 1 < S) dp = next_row(dp, st);
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < S; ++j)
@@ -1024,8 +1046,12 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
   double r[S];
   const double* srow = a.src + gl + (long long)(i0 + 1) * st;
   if (act && i0 + S <= m + 1) {  // whole segment inside rows 1..m+1: no per-row predicates
+    const double* sp = srow;
 #pragma unroll
-    for (int j = 0; j < S; ++j) r[j] = srow[j * st];
+    for (int j = 0; j < S; ++j) {
+      r[j] = *sp;
+      if (j + 1 < S) sp = next_row(sp, st);
+    }
   } else {
 #pragma unroll
     for (int j = 0; j < S; ++j) r[j] = (act && i0 + 1 + j <= m + 1) ? srow[j * st] : 0.0;
@@ -1040,15 +1066,177 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
     if (threadIdx.y == 0) bfold = a.bnd[gl];
     else if ((int)threadIdx.y == (m - 1) / S) bfold = a.bnd[gl + a.hi_off];
   }
-  double* T = sm;
-  double* Mi = T + kTabDoubles;
+  // The uniform-segment tables stay in global memory (7.7 KB, L1-resident): only warps
+  // with a non-solvent or general segment read them, the dominant kind comes from the
+  // kernel parameters, and staging them per block cost 7% of the kernel's instructions.
+  double* Mi = sm;
   double* X = Mi + kSegS * (kSegS + 2);
   double* FP = X + 4 * NT;
-  stage_tables<kSegS>(a, T, Mi, FP, tid, NT);
+  if (a.static_ok)
+    for (int c = tid; c < kSegS * (kSegS + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
+  if (uses_flow(a.pro, a.epi))
+    for (int c = tid; c < a.fpoly_n / 2; c += NT) cp_async16(FP + kFlowHdr + 2 * c, a.fpoly + 2 * c);
   cp_async_wait_all();
   __syncthreads();
   if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
-  col_body<S, kSegS, CN, LB>(a, g, r, wl, wr, amask, w1, bfold, T, Mi, X, FP);
+  col_body<S, kSegS, CN, LB>(a, g, r, wl, wr, amask, w1, bfold, a.tab, Mi, X, FP);
+}
+
+// ---------------------------------------------------------------------------------------
+// Fused axis-0 + axis-1 column sweeps of a LOD step (schemes.py:301-311, order kept).  The
+// lines of both families lie inside a k-slab (a group of adjacent k columns, all i and j),
+// and a slab of 16-64 columns is a few tens of MB: one persistent launch runs the axis-0
+// tiles of slab x and, `lag` slabs later, the axis-1 tiles of slab x, which find the axis-0
+// output in L2 and store in place over it, so that the intermediate field never travels to
+// HBM and back.  Both parts are the register-direct column tile of k_sweep_col (same block
+// shape, same 64 registers, four blocks per SM), so the fusion costs no occupancy.  Blocks
+// take items from a global queue whose order is the dependency order (an item only waits
+// for earlier items, all held by running blocks: no deadlock); an axis-0 tile publishes its
+// slab with a fence + counter increment, an axis-1 tile spins (one thread, acquire loads)
+// until its slab's counter reaches the tiles per slab.  Within a slab the tiles run with the
+// column group fastest, so concurrently running tiles read adjacent 128-byte row chunks.
+struct Fuse01Ctl {
+  int* q;       // q[0] next item, q[1] blocks that left, q[2 + x] finished axis-0 tiles of slab x
+  int nslab;    // slabs
+  int tw;       // column groups (of LB columns) per slab
+  int ntx;      // column groups in all
+  int n0i, n1i; // outer indices: axis-0 tiles per column group (n1 - 2), axis-1 (n0 - 2)
+  int lag;      // slabs of axis-0 tiles queued ahead of the axis-1 tiles (1 <= lag <= nslab)
+};
+
+template <int S, int kSegS, int LB>
+__device__ __forceinline__ void col_tile_run(const SweepArgs& a, int axis, int tx, int outer,
+                                             const double* Mi, double* X, const double* FP) {
+  TileGeo g;
+  g.b = 0;
+  g.c0 = 1 + tx * LB;
+  g.outer = outer;
+  g.ncols = min(LB, (a.L.n2 - 2) + 1 - g.c0);
+  if (axis == 0) {
+    g.base = a.L.at(0, outer, g.c0);
+    g.stride = (int)a.L.s0;
+  } else {
+    g.base = a.L.at(outer, 0, g.c0);
+    g.stride = (int)a.L.pitch;
+  }
+  const int m = a.m, i0 = threadIdx.y * S, st = g.stride;
+  const bool act = (int)threadIdx.x < g.ncols;
+  const long long gl = g.base + threadIdx.x;
+  unsigned long long amask = 0ull, w1 = 0ull;
+  if (act) {
+    const unsigned long long* dp = col_desc<kSegS>(a, g);
+    if (a.pro != PRO_NONE || a.has_extra || a.epi != EPI_STORE) {
+      const ulonglong2 dd = *reinterpret_cast<const ulonglong2*>(dp);
+      amask = dd.x;
+      w1 = dd.y;
+    } else {
+      amask = *dp;
+    }
+  }
+  double r[S];
+  const double* srow = a.src + gl + (long long)(i0 + 1) * st;
+  if (act && i0 + S <= m + 1) {
+    const double* sp = srow;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      r[j] = *sp;
+      if (j + 1 < S) sp = next_row(sp, st);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < S; ++j) r[j] = (act && i0 + 1 + j <= m + 1) ? srow[j * st] : 0.0;
+  }
+  double bfold = 0.0;
+  if (act) {
+    if (threadIdx.y == 0) bfold = a.bnd[gl];
+    else if ((int)threadIdx.y == (m - 1) / S) bfold = a.bnd[gl + a.hi_off];
+  }
+  col_body<S, kSegS, false, LB>(a, g, r, 0.0, 0.0, amask, w1, bfold, a.tab, Mi, X, FP);
+}
+
+template <int S, int kSegS, int LB>
+__global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
+    k_sweep_fused01(const SweepArgs a0, const SweepArgs a1, const Fuse01Ctl c) {
+  extern __shared__ double sm[];
+  constexpr int NT = LB * kSegS, MD = kSegS * (kSegS + 2);
+  __shared__ int s_item;
+  const int tid = threadIdx.y * LB + threadIdx.x;
+  const int dstep = a0.div_step ? *((volatile int*)a0.div_step) : INT_MAX;
+  double* Mi0 = sm;
+  double* Mi1 = Mi0 + MD;
+  double* X = Mi1 + MD;
+  double* FP = X + 4 * NT;
+  if (a0.static_ok)
+    for (int t = tid; t < MD / 2; t += NT) cp_async16(Mi0 + 2 * t, a0.minv + 2 * t);
+  if (a1.static_ok)
+    for (int t = tid; t < MD / 2; t += NT) cp_async16(Mi1 + 2 * t, a1.minv + 2 * t);
+  if (uses_flow(a0.pro, a0.epi))
+    for (int t = tid; t < a0.fpoly_n / 2; t += NT) cp_async16(FP + kFlowHdr + 2 * t, a0.fpoly + 2 * t);
+  if (dstep < a0.step) {  // an earlier step diverged: nothing more to compute
+    cp_async_wait_all();
+    return;
+  }
+  if (tid == 0) s_item = atomicAdd(c.q, 1);
+  cp_async_wait_all();
+  __syncthreads();
+
+  const int per0 = c.tw * c.n0i, per1 = c.tw * c.n1i, per = per0 + per1;
+  const int nitems = c.nslab * per;  // laid out as if every slab had c.tw column groups
+  const int head = c.lag * per0, full = c.nslab - c.lag;
+  int item = s_item;
+  while (item < nitems) {
+    int nxt = 0;
+    if (tid == 0) nxt = atomicAdd(c.q, 1);  // claimed now, taken up when this item is done
+    // queue order: axis-0 tiles of slabs 0..lag-1, then for slab x: its axis-1 tiles, the
+    // axis-0 tiles of slab x+lag.  The last slab may be narrower: the queue is laid out as if
+    // every slab had c.tw groups and items of missing groups are skipped.
+    int kind, slab, w;
+    if (item < head) {
+      kind = 0;
+      slab = item / per0;
+      w = item - slab * per0;
+    } else {
+      const int r = item - head;
+      if (r < full * per) {
+        const int grp = r / per, v = r - grp * per;
+        kind = v < per1 ? 1 : 0;
+        slab = v < per1 ? grp : grp + c.lag;
+        w = v < per1 ? v : v - per1;
+      } else {
+        const int r2 = r - full * per;
+        kind = 1;
+        slab = full + r2 / per1;
+        w = r2 - (slab - full) * per1;
+      }
+    }
+    const int outer = 1 + w / c.tw, tx = slab * c.tw + (w - (outer - 1) * c.tw);
+    const bool exists = tx < c.ntx;
+    if (kind == 0) {
+      if (exists) col_tile_run<S, kSegS, LB>(a0, 0, tx, outer, Mi0, X, FP);
+      if (tid == 0) s_item = nxt;
+      __syncthreads();  // every store of the tile is issued; the scratch is free again
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(c.q + 2 + slab, 1);
+      }
+    } else {
+      if (tid == 0) {
+        const int* d = c.q + 2 + slab;
+        while (ld_acquire(d) < per0) __nanosleep(64);
+      }
+      __syncthreads();
+      if (exists) col_tile_run<S, kSegS, LB>(a1, 1, tx, outer, Mi1, X, FP);
+      if (tid == 0) s_item = nxt;
+      __syncthreads();
+    }
+    item = s_item;
+  }
+  // The last block to leave resets the queue for the next launch.
+  __syncthreads();
+  if (tid == 0) s_item = atomicAdd(c.q + 1, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (s_item)
+    for (int t = tid; t < 2 + c.nslab; t += NT) c.q[t] = 0;
 }
 
 // Staged-tile kernel: block (x = column / row group, y = outer index).  Serves the row
@@ -1610,24 +1798,25 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int G, int NW>
+template <int G, int NW, int NB_>
 struct RowLean {
-  static constexpr int S = 16, NL = 32 / G, LD = G * S, WB = NL * LD, NB = 3;
+  static constexpr int S = 16, NL = 32 / G, LD = G * S, WB = NL * LD, NB = NB_;
   static constexpr size_t lines_bytes = (size_t)NW * NB * WB * sizeof(double);
   static constexpr size_t smem(int fpoly_n) {
     return 1024 + lines_bytes +
-           sizeof(double) * (G * (G + 2) + NW * NL * (G + 2) + kFlowHdr + fpoly_n + 2) +
+           sizeof(double) * (kTabDoubles + G * (G + 2) + NW * NL * (G + 2) + kFlowHdr + fpoly_n + 2) +
            sizeof(unsigned long long) * NW * NB;
   }
 };
 
-template <int G, int NW, int FLOWK>
+template <int G, int NW, int NB_, int FLOWK>
 __global__ void __launch_bounds__(NW * 32, 1)
     k_sweep_rowlean(const SweepArgs a, const int nlines, const __grid_constant__ CUtensorMap tms,
                     const __grid_constant__ CUtensorMap tmd) {
   extern __shared__ unsigned char smraw[];
-  using RL = RowLean<G, NW>;
+  using RL = RowLean<G, NW, NB_>;
   constexpr int S = RL::S, NL = RL::NL, LD = RL::LD, WB = RL::WB, NB = RL::NB;
+  static_assert(NB == 2 || NB == 3, "two or three line buffers per warp");
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int NT = NW * 32;
   constexpr bool FLOW = FLOWK != 0, FSM = FLOWK == 2;  // flow epilogue and its form (launch)
@@ -1636,11 +1825,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const int sub = lane / G, seg = lane % G;
   double* Lb = reinterpret_cast<double*>(
       smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u));  // 1024-aligned line buffers
-  double* Mi = Lb + NW * NB * WB;        // G x (G + 2)
+  double* T = Lb + NW * NB * WB;         // uniform-segment tables
+  double* Mi = T + kTabDoubles;          // G x (G + 2)
   double* sRb = Mi + G * (G + 2);        // NW * NL * (G + 2)
   double* FP = sRb + NW * NL * (G + 2);  // flow tables at FP + kFlowHdr
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(
       FP + kFlowHdr + (FLOW ? a.fpoly_n + (a.fpoly_n & 1) : 0));
+  for (int c = tid; c < kTabDoubles / 2; c += NT) cp_async16(T + 2 * c, a.tab + 2 * c);
   if (a.static_ok)
     for (int c = tid; c < G * (G + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
   if (FLOW)
@@ -1687,10 +1878,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
     dd = make_ulonglong2(0ull, 0ull);
     bf = 0.0;
     if (ln < nlines) {
-      dd = *reinterpret_cast<const ulonglong2*>(a.desc + 2 * (line_desc(L, i, j) * G + seg));
-      const long long bs = L.at(i, j, 0);
-      if (seg == 0) bf = a.bnd[bs];
-      else if (seg == G - 1) bf = a.bnd[bs + a.hi_off];
+      // 32-bit line arithmetic: (i, j) is line i*n1 + j of the field, pitch doubles each
+      dd = *reinterpret_cast<const ulonglong2*>(
+          a.desc + 2 * (long long)(((i - 1) * K + (j - 1)) * G + seg));
+      const double* bp = a.bnd + (long long)(i * L.n1 + j) * L.pitch + kOff;
+      if (seg == 0) bf = bp[0];
+      else if (seg == G - 1) bf = bp[a.hi_off];
     }
   };
   int l1 = line, i1 = ci, j1 = cj;  // one iteration ahead
@@ -1713,7 +1906,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   for (int w0 = blockIdx.x * NW + warp; w0 * NL < nlines; w0 += gridDim.x * NW, ++it) {
     const int b = it % NB;
     const bool valid = line < nlines;
-    const long long base = L.at(valid ? ci : 1, valid ? cj : 1, 0);
+    const long long base = (long long)(valid ? ci * L.n1 + cj : 0) * L.pitch + kOff;
     const unsigned long long amask = ddn.x;
     const uint32_t sbits = (uint32_t)ddn.y, cmask = (uint32_t)(ddn.y >> 32);
     const double bfold = bfn;
@@ -1724,14 +1917,16 @@ __global__ void __launch_bounds__(NW * 32, 1)
     double r[S];
 #pragma unroll
     for (int q = 0; q < S; q += 2) {
-      const double2 v = valid ? *reinterpret_cast<const double2*>(W + (((q >> 1) ^ x7) << 1))
-                              : make_double2(0.0, 0.0);
+      // (an idle sub-line of the last iteration solves whatever its buffer holds; nothing
+      // of it is stored or tested)
+      const double2 v = *reinterpret_cast<const double2*>(W + (((q >> 1) ^ x7) << 1));
       r[q] = v.x;
       r[q + 1] = v.y;
     }
     const double face = r[S - 1];  // last lane: row m + 1, written back unchanged
-    rw_solve<S, G>(a, r, amask, cmask, bfold, valid, seg, a.tab, Mi, sR, base);
+    rw_solve<S, G>(a, r, amask, cmask, bfold, valid, seg, T, Mi, sR, base);
     unsigned need = 0u;  // FLOWK == 3: rows whose flow is evaluated from the buffer below
+    int mx = 0;  // divergence test: largest high word of |x| over the lane's final rows
     if (FLOWK == 3) {
       // Flow on the lane's 16 rows, eight interleaved Horner chains at a time, the tier chosen
       // per warp and half (no divergence): the tiny-argument polynomial when every row of the
@@ -1758,7 +1953,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
             for (int u = 0; u < 8; ++u) p[u] = fma(p[u], t[u], a.ftiny[c]);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) r[h + u] *= p[u];
+          for (int u = 0; u < 8; ++u) {
+            r[h + u] *= p[u];
+            mx = max(mx, __double2hiint(r[h + u]) & 0x7fffffff);
+          }
         } else {
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
@@ -1774,6 +1972,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
             const bool keep = !(fabs(r[h + u]) <= kFSmallX) || ((force >> (h + u)) & 1u);
             need |= keep ? (1u << (h + u)) : 0u;
             r[h + u] = keep ? r[h + u] : r[h + u] * p[u];
+            // final unless it is redone from the buffer (tested there)
+            if (!keep || ((ident >> (h + u)) & 1u))
+              mx = max(mx, __double2hiint(r[h + u]) & 0x7fffffff);
           }
         }
       }
@@ -1794,16 +1995,17 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if (seg == G - 1) r[S - 1] = 0.0;
     // divergence test (schemes.py:417-421) on the high words: |x| > thr for sure when the
     // high word is above the threshold's, undecided only when equal (exact compare then)
-    int mx = 0;
+    if (FLOWK != 3) {  // (FLOWK == 3 tests its rows where the flow leaves them)
 #pragma unroll
-    for (int q = 0; q < S; ++q)
-      if (!((need >> q) & 1u)) mx = max(mx, __double2hiint(r[q]) & 0x7fffffff);
-    if (mx >= thrH) {
+      for (int q = 0; q < S; ++q)
+        if (!((need >> q) & 1u)) mx = max(mx, __double2hiint(r[q]) & 0x7fffffff);
+    }
+    if (mx >= thrH && valid) {
       if (mx > thrH) {
         bad = true;
       } else {
 #pragma unroll
-        for (int q = 0; q < S; ++q) bad |= !(fabs(r[q]) <= thrc);
+        for (int q = 0; q < S; ++q) bad |= !((need >> q) & 1u) && !(fabs(r[q]) <= thrc);
       }
     }
     if (seg == G - 1) r[S - 1] = face;
@@ -1828,8 +2030,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if (seg == 0) {
       if (valid) tma_store_3d(&tmd, 0, 0, ci * L.n1 + cj, Wq + b * WB);
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      // the buffer refilled next was stored one iteration ago: all but the newest group done
-      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      // the buffer refilled next was stored one iteration ago (three buffers: all but the
+      // newest group done) or just now (two buffers)
+      if (NB == 3) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       if ((w0 + 2 * gridDim.x * NW) * NL < nlines) issue(l2, i2, j2, (it + 2) % NB);
     }
     line = l1; ci = i1; cj = j1;
@@ -1873,12 +2077,6 @@ struct Fused12 {
     return sizeof(double) * (kTabDoubles + P * (P + 2) + UD + kFlowHdr + fpoly_n + 2);
   }
 };
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 template <int S, int P, int LB, int G>
 __global__ void __launch_bounds__(LB * P, 3)
@@ -2250,6 +2448,11 @@ __global__ void k_seg_factors(const Layout L, int axis, int S, int P, int lm, Ax
 // ---------------------------------------------------------------------------------------
 // Host-side launch helpers.
 
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
 static int seg_S(int m, int P) {
   if (P == 16) return m <= 256 ? 16 : 0;  // instantiated: P = 8 with any S, 16/32 with 16/32
   if (P == 32) return m <= 512 ? 16 : (m <= 1024 ? 32 : 0);
@@ -2362,8 +2565,7 @@ static void launch_col(const SweepArgs& a, int axis, cudaStream_t st) {
   constexpr int LB = 16;
   const int nouter = a.on ? a.on : (axis == 0 ? a.L.n1 : a.L.n0) - 2;
   const int ntx = (a.L.n2 - 2 + LB - 1) / LB;
-  const size_t smem =
-      sizeof(double) * (kTabDoubles + P * (P + 2) + 4 * LB * P + kFlowHdr + flow_stage_n(a));
+  const size_t smem = sizeof(double) * (P * (P + 2) + 4 * LB * P + kFlowHdr + flow_stage_n(a));
   auto kern = k_sweep_col<S, P, CN, LB>;
   resident_blocks((const void*)kern, LB * P, smem);  // shared-memory limit, once
   kern<<<dim3(ntx, nouter, a.L.nb), dim3(LB, P), smem, st>>>(a, axis);
@@ -2501,7 +2703,7 @@ static bool launch_rowtma_SG(const SweepArgs& a, cudaStream_t st) {
 
 // TMA-in / TMA-out row sweeps (k_sweep_rowlean): the default for 256- and 512-row lines of a
 // single grid with the LOD epilogues; PBG_ROWLEAN=0 keeps k_sweep_rowwarp / k_sweep_rowtma,
-// PBG_ROWLEAN_NW = warps per block (16 or 12).
+// PBG_ROWLEAN_NW = warps per block (16; 12, 20, 24 for comparison).
 static bool rowlean_enabled() {
   static const bool on = [] {
     const char* e = getenv("PBG_ROWLEAN");
@@ -2514,23 +2716,24 @@ static bool rowlean_ok(const SweepArgs& a) {
          (a.epi == EPI_STORE || a.epi == EPI_FLOW || a.epi == EPI_SRC);
 }
 
-template <int G, int NW>
+template <int G, int NW, int NB>
 static bool launch_rowlean_GN(const SweepArgs& a, cudaStream_t st) {
   CUtensorMap tms, tmd;
   if (!line_tensor_map(a, G, &tms, a.src) || !line_tensor_map(a, G, &tmd, a.dst)) return false;
   const int nlines = (a.on ? a.on : a.L.n0 - 2) * (a.L.n1 - 2);
   const bool flow = a.epi == EPI_FLOW;
-  const size_t smem = RowLean<G, NW>::smem(flow ? a.fpoly_n : 0);
-  // PBG_FLOWK: 3 = tiny tier on all 16 rows at once, the others from the buffer (default);
-  // 2 = small form for all rows; 1 = flow_group (tiny tier + per-node fallback), as elsewhere
+  const size_t smem = RowLean<G, NW, NB>::smem(flow ? a.fpoly_n : 0);
+  // PBG_FLOWK: 3 = per-warp tier choice on all 16 rows (default); 2 = small form for all
+  // rows; 1 = flow_group (tiny tier + per-node fallback), as the other kernels
   static const int fsm = [] {
     const char* e = getenv("PBG_FLOWK");
     const int v = e && *e ? atoi(e) : 3;
     return v == 1 ? 0 : v;
   }();
-  auto kern = !flow ? k_sweep_rowlean<G, NW, 0>
-                    : (fsm == 3 ? k_sweep_rowlean<G, NW, 3>
-                                : (fsm ? k_sweep_rowlean<G, NW, 2> : k_sweep_rowlean<G, NW, 1>));
+  auto kern = !flow ? k_sweep_rowlean<G, NW, NB, 0>
+                    : (fsm == 3 ? k_sweep_rowlean<G, NW, NB, 3>
+                                : (fsm ? k_sweep_rowlean<G, NW, NB, 2>
+                                       : k_sweep_rowlean<G, NW, NB, 1>));
   const int per_block = NW * (32 / G);
   const int grid = std::min((nlines + per_block - 1) / per_block,
                             resident_blocks((const void*)kern, NW * 32, smem));
@@ -2544,8 +2747,11 @@ static bool launch_rowlean_G(const SweepArgs& a, cudaStream_t st) {
     const char* e = getenv("PBG_ROWLEAN_NW");
     return e && *e ? atoi(e) : 16;
   }();
-  if (nw == 12) return launch_rowlean_GN<G, 12>(a, st);
-  return launch_rowlean_GN<G, 16>(a, st);
+  if (nw == 12) return launch_rowlean_GN<G, 12, 3>(a, st);
+  if (nw == 20) return launch_rowlean_GN<G, 20, 2>(a, st);
+  if (nw == 24) return launch_rowlean_GN<G, 24, 2>(a, st);
+  if (nw == 162) return launch_rowlean_GN<G, 16, 2>(a, st);
+  return launch_rowlean_GN<G, 16, 3>(a, st);
 }
 
 static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
@@ -2651,6 +2857,58 @@ static int launch_fused12(const SweepArgs& a1, const SweepArgs& a2, int* q, cuda
   return PBG_OK;
 }
 
+
+// Fused axis-0 + axis-1 launch (k_sweep_fused01): LOD steps of a single grid whose first two
+// axes use the same segmentation.  Measured slower than the separate launches (c3 126-129 vs
+// 124 us for the two sweeps, c4 1119 vs 982 us, profiles/fused01_ab_r02.txt: the column tiles
+// are not bound by DRAM latency, and the slab order costs DRAM locality), so PBG_FUSED01=1
+// only selects it for comparison; PBG_FUSED01_TW = column groups per slab, PBG_FUSED01_LAG =
+// slabs of lead.
+static bool fused01_ok(const SweepArgs& a0, const SweepArgs& a1) {
+  static const bool on = env_int("PBG_FUSED01", 0) != 0;
+  if (!on || !col_enabled() || a0.cn || a1.cn || a0.L.nb != 1 || a0.ends || a1.ends) return false;
+  if (a0.epi != EPI_STORE || a0.has_extra || a0.check) return false;
+  if (a1.pro != PRO_NONE || a1.epi != EPI_STORE || a1.has_extra || a1.check) return false;
+  const int P0 = seg_P(0, a0.m), P1 = seg_P(1, a1.m);
+  if (P0 != P1 || seg_S(a0.m, P0) != 16 || seg_S(a1.m, P1) != 16) return false;
+  return P0 == 16 || P0 == 32;
+}
+
+template <int S, int P>
+static void launch_fused01_T(const SweepArgs& a0, const SweepArgs& a1, int* q, cudaStream_t st) {
+  constexpr int LB = 16;
+  const size_t smem =
+      sizeof(double) * (2 * P * (P + 2) + 4 * LB * P + kFlowHdr + flow_stage_n(a0));
+  auto kern = k_sweep_fused01<S, P, LB>;
+  const int resident = resident_blocks((const void*)kern, LB * P, smem);
+  static const int tw_env = env_int("PBG_FUSED01_TW", 0), lag_env = env_int("PBG_FUSED01_LAG", 0);
+  Fuse01Ctl c;
+  c.q = q;
+  c.ntx = (a0.L.n2 - 2 + LB - 1) / LB;
+  c.n0i = a0.L.n1 - 2;
+  c.n1i = a0.L.n0 - 2;
+  // slabs of at most ~18 MB: the axis-0 output of `lag` + 1 slabs and the in-place axis-1
+  // output of the slab before them stay in L2 together
+  const double group_mb = (double)a0.L.n0 * a0.L.n1 * LB * 8.0 / 1e6;
+  c.tw = tw_env > 0 ? tw_env : std::max(1, std::min(4, (int)(18.0 / group_mb)));
+  c.tw = std::min(c.tw, c.ntx);
+  c.nslab = (c.ntx + c.tw - 1) / c.tw;
+  // every axis-0 tile of slab x is claimed at least `resident` items before the axis-1 tiles
+  // of slab x
+  const int per0 = c.tw * c.n0i;
+  const int lag = lag_env > 0 ? lag_env : (resident + per0 - 1) / per0 + 1;
+  c.lag = std::max(1, std::min(lag, c.nslab));
+  const int grid = std::min(c.nslab * c.tw * (c.n0i + c.n1i), resident);
+  kern<<<grid, dim3(LB, P), smem, st>>>(a0, a1, c);
+}
+
+static int launch_fused01(const SweepArgs& a0, const SweepArgs& a1, int* q, cudaStream_t st) {
+  if (!a0.fpoly) return fail(PBG_E_CUDA, "flow table allocation failed");
+  if (seg_P(0, a0.m) == 16) launch_fused01_T<16, 16>(a0, a1, q, st);
+  else launch_fused01_T<16, 32>(a0, a1, q, st);
+  PBG_LAUNCH_CHECK("k_sweep_fused01");
+  return PBG_OK;
+}
 
 // Tridiagonal row tables for one axis: f = factor / h^2 (tridiag.py:165, 179-181, 199-202).
 static AxisCoef make_axis_coef(const double eps[2], double factor, double h) {
@@ -3136,11 +3394,6 @@ void march_axes(const pbg_march_desc* d, const Plan& plan, SweepArgs ax[3]) {
   }
 }
 
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e && *e ? atoi(e) : dflt;
-}
-
 static bool g_profile = false;
 static double g_prof_ms[3] = {0, 0, 0};
 static long long g_prof_n[3] = {0, 0, 0};
@@ -3205,6 +3458,7 @@ struct pbg_plan {
   int* dflag = nullptr;
   int* hflag = nullptr;  // pinned
   int* fq = nullptr;     // work queue of the fused axis-1/axis-2 launch (zero between launches)
+  int* fq01 = nullptr;   // work queue of the fused axis-0/axis-1 launch
   cudaEvent_t e0 = nullptr, e1 = nullptr;
 };
 
@@ -3218,6 +3472,7 @@ static void plan_free(pbg_plan* p, cudaStream_t st) {
   for (int q = 0; q < 3; ++q) release_axis(p->aux[q], st);
   if (p->dflag) cudaFreeAsync(p->dflag, st);
   if (p->fq) cudaFreeAsync(p->fq, st);
+  if (p->fq01) cudaFreeAsync(p->fq01, st);
   if (p->hflag) cudaFreeHost(p->hflag);
   if (p->e0) cudaEventDestroy(p->e0);
   if (p->e1) cudaEventDestroy(p->e1);
@@ -3281,6 +3536,12 @@ extern "C" PBG_API int pbg_plan_create_batch(const pbg_march_desc* d, int32_t nb
   }
   if (cudaMallocAsync(&p->dflag, p->nb * sizeof(int), st) != cudaSuccess)
     return bail(fail(PBG_E_CUDA, "plan allocation failed"));
+  if (p->plan.family <= 1 && fused01_ok(p->ax[0], p->ax[1])) {
+    const size_t qb = (size_t)(2 + d->grid.n[2]) * sizeof(int);
+    if (cudaMallocAsync(&p->fq01, qb, st) != cudaSuccess ||
+        cudaMemsetAsync(p->fq01, 0, qb, st) != cudaSuccess)
+      return bail(fail(PBG_E_CUDA, "plan allocation failed"));
+  }
   if (p->plan.family <= 1 && fused12_shape(p->ax[1], p->ax[2])) {
     const size_t qb = (size_t)(2 + d->grid.n[0]) * sizeof(int);
     if (cudaMallocAsync(&p->fq, qb, st) != cudaSuccess ||
@@ -3356,6 +3617,9 @@ extern "C" PBG_API int pbg_plan_run_batch(pbg_plan* p, const double* initial, do
   // One launch for the axis-1 and axis-2 sweeps (k_sweep_fused12), axis 2 in place over the
   // axis-1 output while it is still in L2.
   const bool fused = p->fq != nullptr && chunk == 0;
+  // One launch for the axis-0 and axis-1 sweeps (k_sweep_fused01), axis 1 in place over the
+  // axis-0 output while it is still in L2; the axis-2 sweep then runs in place too.
+  const bool fused01 = p->fq01 != nullptr && chunk == 0 && !fused;
   const bool inpl =
       inpl_all || fused || (lod_rw && (chunk > 0 || env_int("PBG_INPLACE2", 0) != 0));
   const int nplanes = g->n[0] - 2;
@@ -3388,6 +3652,9 @@ extern "C" PBG_API int pbg_plan_run_batch(pbg_plan* p, const double* initial, do
         if (inpl_all) {  // every sweep in place on the state buffer (one field per step)
           a.src = axis == 0 ? X : Bf;
           a.dst = Bf;
+        } else if (fused01) {  // axis 0 into the other buffer, axes 1 and 2 in place there
+          a.src = axis == 0 ? X : A;
+          a.dst = A;
         }
       } else {
         a.src = X;
@@ -3406,6 +3673,8 @@ extern "C" PBG_API int pbg_plan_run_batch(pbg_plan* p, const double* initial, do
             rc = launch_sweep(a, q, st);
           }
         }
+      } else if (fused01 && axis <= 1) {
+        if (axis == 0) rc = launch_fused01(as[0], as[1], p->fq01, st);
       } else if (fused && axis >= 1) {
         if (axis == 1) rc = launch_fused12(as[1], as[2], p->fq, st);
       } else if (!(chunk > 0 && axis == 2)) {
