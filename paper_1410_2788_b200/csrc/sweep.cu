@@ -872,11 +872,16 @@ __device__ __forceinline__ T* next_row(T* p, long long st) {
 // i0+1+j of the line (rows past m+1 zero), wl / wr = raw rows i0 and i0+S+1 (CN only).
 // Prologue, CN explicit half, folds, elimination, reduced system (block-wide barriers: every
 // thread of the block calls this), reconstruction, epilogue and the store of rows 1..m.
-template <int S, int kSegS, bool CN, int LB>
+// MODE 1 ("plain"): no flow and no accumulator operand anywhere (prologue none / source,
+// epilogue store / source / MAOS first branch, no divergence test) -- the LOD column sweeps,
+// compiled without the other stages so that those do not cost the common path registers.
+// MODE 2: the AOS first branch with its grouped flow epilogue.  MODE 0: everything else.
+template <int S, int kSegS, bool CN, int LB, int MODE = 0>
 __device__ __forceinline__ void col_body(const SweepArgs& a, const TileGeo& g, double (&r)[S],
                                          double wl, double wr, unsigned long long amask,
                                          unsigned long long w1, double bfold, const double* T,
                                          const double* Mi, double* X, const double* FP) {
+  constexpr bool PLAIN = MODE == 1;
   const int lane = threadIdx.x, seg = threadIdx.y;
   const int m = a.m, i0 = seg * S;
   const bool act = lane < g.ncols;
@@ -885,7 +890,7 @@ __device__ __forceinline__ void col_body(const SweepArgs& a, const TileGeo& g, d
   const uint32_t sbits = (uint32_t)w1, cmask = (uint32_t)(w1 >> 32);
   const double* rr = a.rho + gl + (long long)(i0 + 1) * st;  // source of row j: rr[j * st]
   // Prologue on the own rows: w = pm*flow(u) or w = u + dta*rho (charged nodes).
-  if (a.pro == PRO_FLOW) {
+  if (!PLAIN && a.pro == PRO_FLOW) {
     const double pm = a.pm;
 #pragma unroll
     for (int j = 0; j < S; ++j)
@@ -956,7 +961,7 @@ __device__ __forceinline__ void col_body(const SweepArgs& a, const TileGeo& g, d
   double* drow = a.dst + gl + (long long)(i0 + 1) * st;
   const int epi = a.epi;
   bool bad = false;
-  if ((epi == EPI_STORE || epi == EPI_SRC || epi == EPI_MAOS0) && !a.check) {
+  if (PLAIN || ((epi == EPI_STORE || epi == EPI_SRC || epi == EPI_MAOS0) && !a.check)) {
     if (i0 + S <= m) {  // whole segment inside the line: no per-row predicates
       double* dp = drow;
 #pragma unroll
@@ -968,6 +973,27 @@ __device__ __forceinline__ void col_body(const SweepArgs& a, const TileGeo& g, d
 #pragma unroll
       for (int j = 0; j < S; ++j)
         if (i0 + 1 + j <= m) drow[j * st] = r[j];
+    }
+  } else if (MODE == 2 && epi == EPI_AOS0) {
+    // AOS first branch: pm * flow(u) + b0 (schemes.py:313-323), the flow of four rows at a
+    // time (tiny-argument tier interleaved and branch-free, the others one by one) instead of
+    // sixteen inlined per-node tier selections
+    const double* yrow = a.src + gl + (long long)(i0 + 1) * st;
+    const double pm = a.pm;
+#pragma unroll
+    for (int q = 0; q < S; q += 4) {
+      double y[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) y[u] = i0 + 1 + q + u <= m ? yrow[(q + u) * st] : 0.0;
+      flow_group(a, FP, y[0], y[1], y[2], y[3], (sbits >> q) & 1u, (sbits >> (q + 1)) & 1u,
+                 (sbits >> (q + 2)) & 1u, (sbits >> (q + 3)) & 1u, pm);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i0 + 1 + q + u > m) continue;
+        const double x = __dadd_rn(y[u], r[q + u]);
+        drow[(q + u) * st] = x;
+        bad |= is_bad(x, a.thr);
+      }
     }
   } else {
     const double* yrow = (epi == EPI_AOS0 ? a.src : a.acc) + gl + (long long)(i0 + 1) * st;
@@ -992,7 +1018,7 @@ __device__ __forceinline__ void col_body(const SweepArgs& a, const TileGeo& g, d
       bad |= is_bad(x, a.thr);
     }
   }
-  if (a.check && bad) atomicMin(a.div_step + g.b, a.step);
+  if (!PLAIN && a.check && bad) atomicMin(a.div_step + g.b, a.step);
 }
 
 // Stage the block's tables (uniform-segment LU tables, clean-line inverse, flow palette and
@@ -1020,9 +1046,10 @@ __device__ __forceinline__ const unsigned long long* col_desc(const SweepArgs& a
 // chunks of 16 adjacent columns -- eliminates, joins the block-wide reduced system, and
 // stores its rows back from registers.  Shared memory holds only the tables and the
 // reduced-system scratch.  Block (LB columns, kSegS segments), grid (column groups, outer).
-template <int S, int kSegS, bool CN, int LB>
+template <int S, int kSegS, bool CN, int LB, int MODE>
 __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
     k_sweep_col(const SweepArgs a, const int axis) {
+  constexpr bool PLAIN = MODE == 1;
   extern __shared__ double sm[];
   constexpr int NT = LB * kSegS;
   const int dstep = a.div_step ? *((volatile int*)(a.div_step + blockIdx.z)) : INT_MAX;
@@ -1066,6 +1093,15 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
     if (threadIdx.y == 0) bfold = a.bnd[gl];
     else if ((int)threadIdx.y == (m - 1) / S) bfold = a.bnd[gl + a.hi_off];
   }
+  if (!PLAIN && epi_needs(a.epi) == 2 && act) {  // accumulator rows of the AOS / MAOS epilogue: on their
+                                       // way to L1 while the line is solved
+    const double* yp = a.acc + gl + (long long)(i0 + 1) * st;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      if (i0 + 1 + j <= m) asm volatile("prefetch.global.L1 [%0];" ::"l"(yp));
+      if (j + 1 < S) yp = next_row(yp, st);
+    }
+  }
   // The uniform-segment tables stay in global memory (7.7 KB, L1-resident): only warps
   // with a non-solvent or general segment read them, the dominant kind comes from the
   // kernel parameters, and staging them per block cost 7% of the kernel's instructions.
@@ -1074,12 +1110,12 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
   double* FP = X + 4 * NT;
   if (a.static_ok)
     for (int c = tid; c < kSegS * (kSegS + 2) / 2; c += NT) cp_async16(Mi + 2 * c, a.minv + 2 * c);
-  if (uses_flow(a.pro, a.epi))
+  if (!PLAIN && uses_flow(a.pro, a.epi))
     for (int c = tid; c < a.fpoly_n / 2; c += NT) cp_async16(FP + kFlowHdr + 2 * c, a.fpoly + 2 * c);
   cp_async_wait_all();
   __syncthreads();
   if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
-  col_body<S, kSegS, CN, LB>(a, g, r, wl, wr, amask, w1, bfold, a.tab, Mi, X, FP);
+  col_body<S, kSegS, CN, LB, MODE>(a, g, r, wl, wr, amask, w1, bfold, a.tab, Mi, X, FP);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -2162,7 +2198,7 @@ __global__ void __launch_bounds__(LB * P, 3)
         if (threadIdx.y == 0) bfold = a1.bnd[gl];
         else if ((int)threadIdx.y == (m - 1) / S) bfold = a1.bnd[gl + a1.hi_off];
       }
-      col_body<S, P, false, LB>(a1, g, r, 0.0, 0.0, amask, 0ull, bfold, T, Mi, U, FP);
+      col_body<S, P, false, LB, 1>(a1, g, r, 0.0, 0.0, amask, 0ull, bfold, T, Mi, U, FP);
       if (tid == 0) s_item = nxt;
       __syncthreads();  // every store of the tile is issued; the scratch is free again
       if (tid == 0) {
@@ -2566,7 +2602,11 @@ static void launch_col(const SweepArgs& a, int axis, cudaStream_t st) {
   const int nouter = a.on ? a.on : (axis == 0 ? a.L.n1 : a.L.n0) - 2;
   const int ntx = (a.L.n2 - 2 + LB - 1) / LB;
   const size_t smem = sizeof(double) * (P * (P + 2) + 4 * LB * P + kFlowHdr + flow_stage_n(a));
-  auto kern = k_sweep_col<S, P, CN, LB>;
+  const bool plain = !CN && (a.pro == PRO_NONE || a.pro == PRO_SRC) && !a.check &&
+                     (a.epi == EPI_STORE || a.epi == EPI_SRC || a.epi == EPI_MAOS0);
+  const bool aos0 = !CN && S % 4 == 0 && a.epi == EPI_AOS0 && a.pro == PRO_NONE;
+  auto kern = plain ? k_sweep_col<S, P, false, LB, 1>
+                    : (aos0 ? k_sweep_col<S, P, false, LB, 2> : k_sweep_col<S, P, CN, LB, 0>);
   resident_blocks((const void*)kern, LB * P, smem);  // shared-memory limit, once
   kern<<<dim3(ntx, nouter, a.L.nb), dim3(LB, P), smem, st>>>(a, axis);
 }
