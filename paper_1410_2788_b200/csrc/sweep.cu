@@ -1567,6 +1567,9 @@ __global__ void __launch_bounds__(kRWarps * 32, 3)
       cmask = (uint32_t)(dd.y >> 32);
       if (seg == 0) bfold = a.bnd[base];
       else if (seg == (m - 1) / S) bfold = a.bnd[base + a.hi_off];
+      if (a.epi == EPI_AOS2)  // the accumulated branches of this line, read by the store pass
+        for (int c = seg; c < G * S / 16; c += G)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.acc + base + 1 + 16 * c));
     }
     asm volatile("cp.async.commit_group;\n" ::);
     {  // the warp's next lines towards L2 while this one is solved (LODIE1 c4: 533 -> 498 us)
