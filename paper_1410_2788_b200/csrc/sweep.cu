@@ -1837,9 +1837,11 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int G, int NW, int NB_>
+template <int S_, int G, int NW, int NB_>
 struct RowLean {
-  static constexpr int S = 16, NL = 32 / G, LD = G * S, WB = NL * LD, NB = NB_;
+  static constexpr int S = S_, NL = 32 / G, LD = G * S, NB = NB_;
+  static constexpr int LDP = (LD + 127) & ~127;  // line buffers 1024-byte aligned (swizzle)
+  static constexpr int WB = NL * LDP;
   static constexpr size_t lines_bytes = (size_t)NW * NB * WB * sizeof(double);
   static constexpr size_t smem(int fpoly_n) {
     return 1024 + lines_bytes +
@@ -1848,18 +1850,30 @@ struct RowLean {
   }
 };
 
-template <int G, int NW, int NB_, int FLOWK>
+// Offset (doubles) of 16-byte unit u of a line inside its swizzled buffer: chunk u / 8, unit
+// (u % 8) ^ (chunk % 8).
+__device__ __forceinline__ int lean_unit(int u) {
+  const int c = u >> 3;
+  return (c << 4) | (((u & 7) ^ (c & 7)) << 1);
+}
+
+// BATCH: nb stacked grids (config 5): a line belongs to grid b = line / (lines per grid),
+// divergence flags per grid, a stopped grid's lines are skipped.  AOS epilogue
+// (a.epi == EPI_AOS2, FLOWK == 0): 0.25 * (accumulated branches + this branch), the
+// accumulator rows read from global memory (prefetched to L1 an iteration ahead).
+template <int S_, int G, int NW, int NB_, int FLOWK, bool BATCH>
 __global__ void __launch_bounds__(NW * 32, 1)
     k_sweep_rowlean(const SweepArgs a, const int nlines, const __grid_constant__ CUtensorMap tms,
                     const __grid_constant__ CUtensorMap tmd) {
   extern __shared__ unsigned char smraw[];
-  using RL = RowLean<G, NW, NB_>;
-  constexpr int S = RL::S, NL = RL::NL, LD = RL::LD, WB = RL::WB, NB = RL::NB;
+  using RL = RowLean<S_, G, NW, NB_>;
+  constexpr int S = RL::S, NL = RL::NL, LD = RL::LD, LDP = RL::LDP, WB = RL::WB, NB = RL::NB;
+  constexpr int HG = S % 8 == 0 ? 8 : 4;  // rows per interleaved flow group
   static_assert(NB == 2 || NB == 3, "two or three line buffers per warp");
+  static_assert(S % 4 == 0 && LD % 16 == 0, "whole 128-byte chunks per line");
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int NT = NW * 32;
-  constexpr bool FLOW = FLOWK != 0, FSM = FLOWK == 2;  // flow epilogue and its form (launch)
-  const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
+  constexpr bool FLOW = FLOWK != 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int sub = lane / G, seg = lane % G;
   double* Lb = reinterpret_cast<double*>(
@@ -1880,134 +1894,169 @@ __global__ void __launch_bounds__(NW * 32, 1)
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   cp_async_wait_all();
   __syncthreads();
-  if (dstep < a.step) return;  // an earlier step diverged: nothing more to compute
+  if (!BATCH) {  // an earlier step diverged: nothing more to compute
+    const int dstep = a.div_step ? *((volatile int*)a.div_step) : INT_MAX;
+    if (dstep < a.step) return;
+  }
 
   const Layout& L = a.L;
-  const int m = a.m, K = L.n1 - 2;
+  const int K = L.n1 - 2;
+  const int npl = a.on ? a.on : L.n0 - 2;          // planes per grid
   const int itop = a.on ? a.o0 + a.on : L.n0 - 2;  // planes itop, itop-1, ... (reverse)
+  const int nlp = npl * K;                         // lines per grid
+  const int glines = BATCH ? (int)(L.bs / L.pitch) : 0;  // field lines between grids
+  const bool aos = FLOWK == 0 && a.epi == EPI_AOS2;
   double* sR = sRb + (warp * NL + sub) * (G + 2);
   unsigned long long* bar = bars + warp * NB;
-  double* Wq = Lb + warp * NB * WB + sub * LD;  // buffer b of this lane's line: Wq + b * WB
-  // Line cursor of this lane: line = (warp-iteration) * NL + sub walks by `dl` lines per
-  // iteration; (i, j) follow without divisions.
-  const int dl = gridDim.x * NW * NL, dq = dl / K, dr = dl - dq * K;
-  int line = (blockIdx.x * NW + warp) * NL + sub;
-  int ci = itop - line / K, cj = 1 + line % K;
-  auto advance = [&](int& ln, int& i, int& j) {
-    ln += dl;
-    i -= dq;
-    j += dr;
-    if (j > K) {
-      j -= K;
-      i -= 1;
+  double* Wq = Lb + warp * NB * WB + sub * LDP;  // buffer b of this lane's line: Wq + b * WB
+  // Line cursor of a lane: line = (warp-iteration) * NL + sub walks by `dl` lines per
+  // iteration; grid, plane and row follow without divisions.
+  struct Cur {
+    int ln, b, i, j;
+  };
+  const int dl = gridDim.x * NW * NL;
+  const int db = BATCH ? dl / nlp : 0, dlr = dl - db * nlp, dq = dlr / K, dr = dlr - dq * K;
+  Cur c0;
+  c0.ln = (blockIdx.x * NW + warp) * NL + sub;
+  c0.b = BATCH ? c0.ln / nlp : 0;
+  {
+    const int l = c0.ln - c0.b * nlp;
+    c0.i = itop - l / K;
+    c0.j = 1 + l % K;
+  }
+  auto advance = [&](Cur& c) {
+    c.ln += dl;
+    c.b += db;
+    c.i -= dq;
+    c.j += dr;
+    if (c.j > K) {
+      c.j -= K;
+      c.i -= 1;
+    }
+    if (BATCH && c.i <= itop - npl) {
+      c.i += npl;
+      c.b += 1;
     }
   };
-  // seg == 0 lanes: tensor copy of line (i, j) into buffer b (every sub-line arrives once per
+  auto fline = [&](const Cur& c) { return c.b * glines + c.i * L.n1 + c.j; };  // field line
+  // seg == 0 lanes: tensor copy of the line into buffer b (every sub-line arrives once per
   // phase, a line past the end with no bytes)
-  auto issue = [&](int ln, int i, int j, int b) {
-    if (ln < nlines) {
+  auto issue = [&](const Cur& c, int b) {
+    if (c.ln < nlines) {
       mbar_expect_tx(bar + b, (unsigned)(LD * sizeof(double)));
-      tma_load_3d(Wq + b * WB, &tms, 0, 0, i * L.n1 + j, bar + b);
+      tma_load_3d(Wq + b * WB, &tms, 0, 0, fline(c), bar + b);
     } else {
       mbar_arrive(bar + b);
     }
   };
-  // descriptor words and low-face fold value of a line, fetched one iteration ahead
-  auto fetch = [&](int ln, int i, int j, ulonglong2& dd, double& bf) {
+  // descriptor words, fold value and (batch) the grid's flag of a line, fetched one
+  // iteration ahead; the AOS accumulator rows start towards L1
+  auto fetch = [&](const Cur& c, ulonglong2& dd, double& bf, int& ds) {
     dd = make_ulonglong2(0ull, 0ull);
     bf = 0.0;
-    if (ln < nlines) {
-      // 32-bit line arithmetic: (i, j) is line i*n1 + j of the field, pitch doubles each
+    ds = INT_MAX;
+    if (c.ln < nlines) {
+      // 32-bit line arithmetic: a line is `pitch` doubles
       dd = *reinterpret_cast<const ulonglong2*>(
-          a.desc + 2 * (long long)(((i - 1) * K + (j - 1)) * G + seg));
-      const double* bp = a.bnd + (long long)(i * L.n1 + j) * L.pitch + kOff;
-      if (seg == 0) bf = bp[0];
-      else if (seg == G - 1) bf = bp[a.hi_off];
+          a.desc + (BATCH ? c.b * a.dstride : 0ll) +
+          2 * (long long)(((c.i - 1) * K + (c.j - 1)) * G + seg));
+      const long long off = (long long)fline(c) * L.pitch + kOff;
+      if (seg == 0) bf = a.bnd[off];
+      else if (seg == G - 1) bf = a.bnd[off + a.hi_off];
+      if (BATCH && a.div_step) ds = a.div_step[c.b];
+      if (aos) {
+        const double* ap = a.acc + off + seg * S + 1;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(ap));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(ap + S - 1));
+      }
     }
   };
-  int l1 = line, i1 = ci, j1 = cj;  // one iteration ahead
-  advance(l1, i1, j1);
-  int l2 = l1, i2 = i1, j2 = j1;    // two iterations ahead
-  advance(l2, i2, j2);
+  Cur c1 = c0;  // one iteration ahead
+  advance(c1);
+  Cur c2 = c1;  // two iterations ahead
+  advance(c2);
   if (seg == 0) {
-    issue(line, ci, cj, 0);
-    issue(l1, i1, j1, 1);
+    issue(c0, 0);
+    issue(c1, 1);
   }
   ulonglong2 ddn;
   double bfn;
-  fetch(line, ci, cj, ddn, bfn);
+  int dsn;
+  fetch(c0, ddn, bfn, dsn);
   const double thrc = fmin(a.thr, 1.7976931348623157e308);
   const int thrH = thrc >= 0.0 ? __double2hiint(thrc) : -1;
   bool bad = false;
-  // swizzled offsets of the lane's eight 16-byte units inside its 128-byte chunk
-  const int x7 = seg & 7;
+  // offsets of the lane's S / 2 16-byte units in its line buffer (S = 16: one chunk per lane)
+  const int u0 = seg * (S / 2);
+  auto uoff = [&](int k) {
+    return S == 16 ? (seg << 4) | ((k ^ (seg & 7)) << 1) : lean_unit(u0 + k);
+  };
   int it = 0;
   for (int w0 = blockIdx.x * NW + warp; w0 * NL < nlines; w0 += gridDim.x * NW, ++it) {
     const int b = it % NB;
-    const bool valid = line < nlines;
-    const long long base = (long long)(valid ? ci * L.n1 + cj : 0) * L.pitch + kOff;
+    const bool valid = c0.ln < nlines && (!BATCH || dsn >= a.step);
+    const long long base = (valid ? (long long)fline(c0) * L.pitch : 0ll) + kOff;
     const unsigned long long amask = ddn.x;
     const uint32_t sbits = (uint32_t)ddn.y, cmask = (uint32_t)(ddn.y >> 32);
     const double bfold = bfn;
-    fetch(l1, i1, j1, ddn, bfn);
-    double* W = Wq + b * WB + seg * 16;  // this lane's chunk
+    fetch(c1, ddn, bfn, dsn);
+    double* W = Wq + b * WB;  // this lane's line
     mbar_wait(bar + b, (unsigned)(it / NB) & 1u);
 
     double r[S];
 #pragma unroll
     for (int q = 0; q < S; q += 2) {
-      // (an idle sub-line of the last iteration solves whatever its buffer holds; nothing
-      // of it is stored or tested)
-      const double2 v = *reinterpret_cast<const double2*>(W + (((q >> 1) ^ x7) << 1));
+      // (an idle sub-line solves whatever its buffer holds; nothing of it is stored or tested)
+      const double2 v = *reinterpret_cast<const double2*>(W + uoff(q >> 1));
       r[q] = v.x;
       r[q + 1] = v.y;
     }
-    const double face = r[S - 1];  // last lane: row m + 1, written back unchanged
     rw_solve<S, G>(a, r, amask, cmask, bfold, valid, seg, T, Mi, sR, base);
     unsigned need = 0u;  // FLOWK == 3: rows whose flow is evaluated from the buffer below
     int mx = 0;  // divergence test: largest high word of |x| over the lane's final rows
     if (FLOWK == 3) {
-      // Flow on the lane's 16 rows, eight interleaved Horner chains at a time, the tier chosen
-      // per warp and half (no divergence): the tiny-argument polynomial when every row of the
-      // warp's half is solvent with |w| <= 0.5 (the far field, most of the grid), else the
+      // Flow on the lane's rows, HG interleaved Horner chains at a time, the tier chosen per
+      // warp and group (no divergence): the tiny-argument polynomial when every row of the
+      // warp's group is solvent with |w| <= 0.5 (the far field, most of the grid), else the
       // small-argument polynomial (|w| <= 2) with the solute rows keeping w.  Rows outside
       // both (|w| > 2, NaN, a solute palette with ions, no small form) are redone from the
       // buffer below (need).
       const unsigned force = a.fsmall_on ? sbits : 0xffffu;
       const unsigned ident = a.decay1 >= 1.0 ? sbits : 0u;  // ion-free solute: w is final
 #pragma unroll
-      for (int h = 0; h < S; h += 8) {
-        bool tiny = ((force >> h) & 0xffu) == 0u;
+      for (int h = 0; h < S; h += HG) {
+        bool tiny = ((force >> h) & ((1u << HG) - 1u)) == 0u;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) tiny = tiny && fabs(r[h + u]) <= kFTinyX;
-        double t[8], p[8];
-        if (__all_sync(FULL, tiny)) {
+        for (int u = 0; u < HG; ++u) tiny = tiny && fabs(r[h + u]) <= kFTinyX;
+        double t[HG], p[HG];
+        // (an idle sub-line holds stale data: it must not decide the tier of the others)
+        if (__all_sync(FULL, tiny || !valid)) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < HG; ++u) {
             t[u] = fma(r[h + u], r[h + u], -0.5 * kFTinyX * kFTinyX);
             p[u] = a.ftiny[kFTinyN - 1];
           }
 #pragma unroll
           for (int c = kFTinyN - 2; c >= 0; --c)
 #pragma unroll
-            for (int u = 0; u < 8; ++u) p[u] = fma(p[u], t[u], a.ftiny[c]);
+            for (int u = 0; u < HG; ++u) p[u] = fma(p[u], t[u], a.ftiny[c]);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < HG; ++u) {
             r[h + u] *= p[u];
             mx = max(mx, __double2hiint(r[h + u]) & 0x7fffffff);
           }
         } else {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < HG; ++u) {
             t[u] = fma(r[h + u], r[h + u], -0.5 * kFSmallX * kFSmallX);
             p[u] = a.fsmall[kFSmallN - 1];
           }
 #pragma unroll
           for (int c = kFSmallN - 2; c >= 0; --c)
 #pragma unroll
-            for (int u = 0; u < 8; ++u) p[u] = fma(p[u], t[u], a.fsmall[c]);
+            for (int u = 0; u < HG; ++u) p[u] = fma(p[u], t[u], a.fsmall[c]);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < HG; ++u) {
             const bool keep = !(fabs(r[h + u]) <= kFSmallX) || ((force >> (h + u)) & 1u);
             need |= keep ? (1u << (h + u)) : 0u;
             r[h + u] = keep ? r[h + u] : r[h + u] * p[u];
@@ -2018,69 +2067,77 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
       }
       need &= ~ident;
-      if (seg == G - 1) need &= 0x7fffu;  // the face row
+      if (seg == G - 1) need &= (1u << (S - 1)) - 1u;  // the face row
     } else if (FLOW) {
 #pragma unroll
       for (int q = 0; q < S; q += 4)
-        if (FSM)
-          flow_group_small(a, FP, r[q], r[q + 1], r[q + 2], r[q + 3], (sbits >> q) & 1u,
-                           (sbits >> (q + 1)) & 1u, (sbits >> (q + 2)) & 1u,
-                           (sbits >> (q + 3)) & 1u, 1.0);
-        else
-          flow_group(a, FP, r[q], r[q + 1], r[q + 2], r[q + 3], (sbits >> q) & 1u,
-                     (sbits >> (q + 1)) & 1u, (sbits >> (q + 2)) & 1u, (sbits >> (q + 3)) & 1u,
-                     1.0);
+        flow_group(a, FP, r[q], r[q + 1], r[q + 2], r[q + 3], (sbits >> q) & 1u,
+                   (sbits >> (q + 1)) & 1u, (sbits >> (q + 2)) & 1u, (sbits >> (q + 3)) & 1u,
+                   1.0);
+    } else if (aos) {  // 0.25 * (accumulated branches + this branch), rounding as the tiles
+      const double2* ap = reinterpret_cast<const double2*>(a.acc + base + seg * S + 1);
+#pragma unroll
+      for (int q = 0; q < S; q += 2) {
+        const double2 y = valid ? ap[q >> 1] : make_double2(0.0, 0.0);
+        r[q] = __dmul_rn(0.25, __dadd_rn(y.x, r[q]));
+        r[q + 1] = __dmul_rn(0.25, __dadd_rn(y.y, r[q + 1]));
+      }
     }
     if (seg == G - 1) r[S - 1] = 0.0;
     // divergence test (schemes.py:417-421) on the high words: |x| > thr for sure when the
     // high word is above the threshold's, undecided only when equal (exact compare then)
     if (FLOWK != 3) {  // (FLOWK == 3 tests its rows where the flow leaves them)
 #pragma unroll
-      for (int q = 0; q < S; ++q)
-        if (!((need >> q) & 1u)) mx = max(mx, __double2hiint(r[q]) & 0x7fffffff);
+      for (int q = 0; q < S; ++q) mx = max(mx, __double2hiint(r[q]) & 0x7fffffff);
     }
+    bool lbad = false;
     if (mx >= thrH && valid) {
       if (mx > thrH) {
-        bad = true;
+        lbad = true;
       } else {
 #pragma unroll
-        for (int q = 0; q < S; ++q) bad |= !((need >> q) & 1u) && !(fabs(r[q]) <= thrc);
+        for (int q = 0; q < S; ++q) lbad |= !((need >> q) & 1u) && !(fabs(r[q]) <= thrc);
       }
     }
-    if (seg == G - 1) r[S - 1] = face;
+    if (seg == G - 1) r[S - 1] = bfold;  // row m + 1: the far face keeps its Dirichlet value
     if (valid) {
 #pragma unroll
       for (int q = 0; q < S; q += 2)
-        *reinterpret_cast<double2*>(W + (((q >> 1) ^ x7) << 1)) = make_double2(r[q], r[q + 1]);
+        *reinterpret_cast<double2*>(W + uoff(q >> 1)) = make_double2(r[q], r[q + 1]);
     }
     if (FLOWK == 3 && valid) {  // the other rows, one at a time, in the buffer
 #pragma unroll 1
       for (unsigned nm = need; nm; nm &= nm - 1) {
         const int u = __ffs(nm) - 1;
-        double* slot = W + ((((u >> 1) ^ x7) << 1) | (u & 1));
+        double* slot = W + (uoff(u >> 1) | (u & 1));
         const double x = flow_sm(a, FP, *slot, (sbits >> u) & 1u, 1.0);
         *slot = x;
-        bad |= !(fabs(x) <= thrc);
+        lbad |= !(fabs(x) <= thrc);
       }
+    }
+    if (BATCH) {  // the line's own grid (the lines of a warp may belong to different grids)
+      if (a.check && lbad) atomicMin(a.div_step + c0.b, a.step);
+    } else {
+      bad |= lbad;
     }
     // the lanes' writes are ordered before the tensor store reads the buffer
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (seg == 0) {
-      if (valid) tma_store_3d(&tmd, 0, 0, ci * L.n1 + cj, Wq + b * WB);
+      if (valid) tma_store_3d(&tmd, 0, 0, fline(c0), Wq + b * WB);
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       // the buffer refilled next was stored one iteration ago (three buffers: all but the
       // newest group done) or just now (two buffers)
       if (NB == 3) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      if ((w0 + 2 * gridDim.x * NW) * NL < nlines) issue(l2, i2, j2, (it + 2) % NB);
+      if ((w0 + 2 * gridDim.x * NW) * NL < nlines) issue(c2, (it + 2) % NB);
     }
-    line = l1; ci = i1; cj = j1;
-    l1 = l2; i1 = i2; j1 = j2;
-    advance(l2, i2, j2);
+    c0 = c1;
+    c1 = c2;
+    advance(c2);
   }
   if (seg == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  if (a.check && __any_sync(FULL, bad) && lane == 0) atomicMin(a.div_step, a.step);
+  if (!BATCH && a.check && __any_sync(FULL, bad) && lane == 0) atomicMin(a.div_step, a.step);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -2755,28 +2812,30 @@ static bool rowlean_enabled() {
   return on;
 }
 static bool rowlean_ok(const SweepArgs& a) {
-  return rowlean_enabled() && a.L.nb == 1 && rowwarp_S(a.m) == 16 &&
-         (a.epi == EPI_STORE || a.epi == EPI_FLOW || a.epi == EPI_SRC);
+  if (!rowlean_enabled()) return false;
+  const int S = rowwarp_S(a.m), G = rowwarp_G(a.m);
+  if (S == 16 && a.L.nb == 1)  // 256- and 512-row lines of a single grid, LOD epilogues
+    return a.epi == EPI_STORE || a.epi == EPI_FLOW || a.epi == EPI_SRC;
+  if (S == 12 && G == 8)  // 96-row lines (config 5), single or batched, LOD and AOS epilogues
+    return a.epi == EPI_STORE || a.epi == EPI_FLOW || a.epi == EPI_SRC || a.epi == EPI_AOS2;
+  return false;
 }
 
-template <int G, int NW, int NB>
-static bool launch_rowlean_GN(const SweepArgs& a, cudaStream_t st) {
+template <int S, int G, int NW, int NB>
+static bool launch_rowlean_T(const SweepArgs& a, cudaStream_t st) {
   CUtensorMap tms, tmd;
-  if (!line_tensor_map(a, G, &tms, a.src) || !line_tensor_map(a, G, &tmd, a.dst)) return false;
-  const int nlines = (a.on ? a.on : a.L.n0 - 2) * (a.L.n1 - 2);
+  if (!line_tensor_map(a, G * S / 16, &tms, a.src) || !line_tensor_map(a, G * S / 16, &tmd, a.dst))
+    return false;
+  const int nlines = (a.on ? a.on : a.L.n0 - 2) * (a.L.n1 - 2) * a.L.nb;
   const bool flow = a.epi == EPI_FLOW;
-  const size_t smem = RowLean<G, NW, NB>::smem(flow ? a.fpoly_n : 0);
-  // PBG_FLOWK: 3 = per-warp tier choice on all 16 rows (default); 2 = small form for all
-  // rows; 1 = flow_group (tiny tier + per-node fallback), as the other kernels
-  static const int fsm = [] {
-    const char* e = getenv("PBG_FLOWK");
-    const int v = e && *e ? atoi(e) : 3;
-    return v == 1 ? 0 : v;
-  }();
-  auto kern = !flow ? k_sweep_rowlean<G, NW, NB, 0>
-                    : (fsm == 3 ? k_sweep_rowlean<G, NW, NB, 3>
-                                : (fsm ? k_sweep_rowlean<G, NW, NB, 2>
-                                       : k_sweep_rowlean<G, NW, NB, 1>));
+  const size_t smem = RowLean<S, G, NW, NB>::smem(flow ? a.fpoly_n : 0);
+  // PBG_FLOWK=1: flow_group (tiny tier + per-node fallback) instead of the per-warp tier
+  // choice on all rows, for comparison
+  static const int fk = env_int("PBG_FLOWK", 3) == 1 ? 1 : 3;
+  constexpr bool BATCH = S == 12;  // the batched form also serves a single 97^3 grid
+  auto kern = !flow ? k_sweep_rowlean<S, G, NW, NB, 0, BATCH>
+                    : (fk == 3 ? k_sweep_rowlean<S, G, NW, NB, 3, BATCH>
+                               : k_sweep_rowlean<S, G, NW, NB, 1, BATCH>);
   const int per_block = NW * (32 / G);
   const int grid = std::min((nlines + per_block - 1) / per_block,
                             resident_blocks((const void*)kern, NW * 32, smem));
@@ -2784,25 +2843,22 @@ static bool launch_rowlean_GN(const SweepArgs& a, cudaStream_t st) {
   return true;
 }
 
-template <int G>
-static bool launch_rowlean_G(const SweepArgs& a, cudaStream_t st) {
-  static const int nw = [] {
-    const char* e = getenv("PBG_ROWLEAN_NW");
-    return e && *e ? atoi(e) : 16;
-  }();
-  if (nw == 12) return launch_rowlean_GN<G, 12, 3>(a, st);
-  if (nw == 20) return launch_rowlean_GN<G, 20, 2>(a, st);
-  if (nw == 24) return launch_rowlean_GN<G, 24, 2>(a, st);
-  if (nw == 162) return launch_rowlean_GN<G, 16, 2>(a, st);
-  return launch_rowlean_GN<G, 16, 3>(a, st);
+static bool launch_rowlean(const SweepArgs& a, cudaStream_t st) {
+  // 16 warps x 3 buffers measured best or equal (20 x 2: c4 -2%, c3 equal; 12 and 24 slower:
+  // profiles/rowlean_ab_r02.txt); PBG_ROWLEAN_NW=20 selects 20 x 2
+  static const int nw = env_int("PBG_ROWLEAN_NW", 16);
+  const int S = rowwarp_S(a.m), G = rowwarp_G(a.m);
+  if (S == 12) return launch_rowlean_T<12, 8, 16, 3>(a, st);
+  if (G == 32) return nw == 20 ? launch_rowlean_T<16, 32, 20, 2>(a, st)
+                               : launch_rowlean_T<16, 32, 16, 3>(a, st);
+  return nw == 20 ? launch_rowlean_T<16, 16, 20, 2>(a, st) : launch_rowlean_T<16, 16, 16, 3>(a, st);
 }
 
 static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
   if (a.rw == 2) {
     if (!a.faces_ok && a.src != a.dst)
       return fail(PBG_E_INVALID, "row sweep: source and destination faces must agree");
-    const bool ok = rowwarp_G(a.m) == 32 ? launch_rowlean_G<32>(a, st) : launch_rowlean_G<16>(a, st);
-    if (!ok) return fail(PBG_E_CUDA, "tensor map encoding failed");
+    if (!launch_rowlean(a, st)) return fail(PBG_E_CUDA, "tensor map encoding failed");
     PBG_LAUNCH_CHECK("k_sweep_rowlean");
     return PBG_OK;
   }
