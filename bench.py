@@ -687,7 +687,9 @@ def slab_main(args, c, p, t_asm, world, rank, local, dist):
     import torch
 
     import paper_1410_2788_b200 as pb
-    from paper_1410_2788_b200.slab import GroupExchange, make_slabs, run_slabs, slab_ranges
+    from paper_1410_2788_b200.schemes import device_problem
+    from paper_1410_2788_b200.slab import (GroupExchange, make_slabs, plane_costs, run_slabs,
+                                           slab_ranges)
 
     nint = (c.n - 2) ** 3
     cfg = pb.MarchConfig(dt=c.dt, T=c.dt * args.steps, variant=c.variant)
@@ -742,7 +744,7 @@ def slab_main(args, c, p, t_asm, world, rank, local, dist):
                        "owned planes back to the host; max over ranks"}
     clocks = clk.summary()
     if rank == 0:
-        rng = slab_ranges(c.n, world)
+        rng = slab_ranges(c.n, world, plane_costs(device_problem(p)))
         line = {
             "metric": "LOD grid-point updates/s (fp64)",
             "value": value,

@@ -85,55 +85,142 @@ static int slab_chunks_env() {
   return std::max(1, std::min(v, 64));
 }
 
+// Static half of the interface elimination for one line's responses: per rank
+//   inv = 1 / (1 - pf d),  hh = qf inv,  d' = pl d hh + ql
+// (d = 0 before rank 0).  st[r] = {pf, pl, inv, hh, pl d, d'}.
+struct SlabStatic {
+  double pf, pl, inv, hh, pld, dd;
+};
+__device__ __forceinline__ SlabStatic slab_static(int r, int nranks, const double* Q,
+                                                  long long C, long long t, double d) {
+  SlabStatic s;
+  s.pf = r > 0 ? Q[t] : 0.0;
+  s.pl = r > 0 ? Q[C + t] : 0.0;
+  const double qf = r + 1 < nranks ? Q[2 * C + t] : 0.0;
+  const double ql = r + 1 < nranks ? Q[3 * C + t] : 0.0;
+  s.inv = 1.0 / (1.0 - s.pf * d);
+  s.hh = qf * s.inv;
+  s.pld = s.pl * d;
+  s.dd = s.pld * s.hh + ql;
+  return s;
+}
+
+// Lines whose responses equal line 0's on every rank (uni[t] = 1): in a protein problem
+// most axis-0 lines are solvent end to end, so their p, q are the same few constants and
+// the interface solve reads them from shared memory instead of 4 * nranks doubles per line.
+// (Whatever line 0 is, the flag only says "same coefficients as line 0".)
+__global__ void k_slab_classify(long long C, int nranks, const double* coef, long long Es,
+                                unsigned char* uni, SlabStatic* s0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // line 0's static elimination, once
+    double d = 0.0;
+    for (int r = 0; r < nranks; ++r) {
+      s0[r] = slab_static(r, nranks, coef + r * Es, C, 0, d);
+      d = s0[r].dd;
+    }
+  }
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < C;
+       t += (long long)gridDim.x * blockDim.x) {
+    bool same = true;
+    for (int r = 0; r < nranks; ++r) {
+      const double* Q = coef + r * Es;
+      for (int q = 0; q < 4; ++q) same = same && Q[q * C + t] == Q[q * C];
+    }
+    uni[t] = same ? 1 : 0;
+  }
+}
+
 // Per line (j, k): block Thomas over the ranks' chunk end values.  recv holds the step
 // exchange (chunk blocks, rank-major inside each chunk), coef the gathered setup blocks.
-__global__ void k_slab_interface(const Layout L, int rank, int nranks, const double* recv,
-                                 const double* coef, long long Es, int J, double* gb,
-                                 int* dflag) {
+// NR = nranks (compile time: the recurrence lives in registers).  Only the rank's two
+// neighbour values leave the kernel: L_{rank-1} and F_{rank+1}.
+template <int NR>
+__global__ void __launch_bounds__(128, 4)
+    k_slab_interface(const Layout L, int rank, const double* recv, const double* coef,
+                     long long Es, int J, const unsigned char* uni, const SlabStatic* g0,
+                     double* gb, int* dflag) {
   const long long plane = L.s0, C = compact_plane(L);
   const long long B0 = chunk_block(L, J, 0);
-  if (blockIdx.x == 0 && (int)threadIdx.x < nranks) {
+  __shared__ SlabStatic s0[NR];
+  if ((int)threadIdx.x < NR) s0[threadIdx.x] = g0[threadIdx.x];  // line 0's (k_slab_classify)
+  if (blockIdx.x == 0 && blockIdx.y == 0 && (int)threadIdx.x < NR) {
     const int f = *reinterpret_cast<const int*>(recv + threadIdx.x * B0);
     if (f != INT_MAX) atomicMin(dflag, f);
   }
+  __syncthreads();
+  // grid (k groups, interior rows j): the chunk and its block are uniform per block
   const int nj = L.n1 - 2, nk = L.n2 - 2;
-  const long long nl = (long long)nj * nk;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nl;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int j = 1 + (int)(t / nk), k = 1 + (int)(t % nk);
+  const int j = 1 + blockIdx.y;
+  const int c = (j - 1) / J;
+  const long long Bc = chunk_block(L, J, c);
+  const long long len = (long long)min(J, nj - c * J) * nk;
+  const double* chunk = recv + (long long)NR * c * B0;  // all earlier chunks are full
+  for (int k = 1 + blockIdx.x * blockDim.x + threadIdx.x; k <= nk; k += gridDim.x * blockDim.x) {
+    const long long t = (long long)(j - 1) * nk + (k - 1);
     const long long o = L.at(0, j, k);
-    const int c = (j - 1) / J;
-    const long long Bc = chunk_block(L, J, c), len = (Bc == B0 ? (long long)J * nk
-                                                                : (long long)(nj - c * J) * nk);
     const long long local = t - (long long)c * J * nk;
-    const double* chunk = recv + (long long)nranks * c * B0;  // all earlier chunks are full
-    double e[kMaxRanks], hh[kMaxRanks], cc[kMaxRanks], dd[kMaxRanks];
-    double cv = 0.0, d = 0.0;
-    for (int r = 0; r < nranks; ++r) {
+    const bool same = uni[t] != 0;
+    double gf[NR], gl[NR];  // all loads in flight before the recurrence starts
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
       const double* G = chunk + r * Bc + kExchTail;
-      const double* Q = coef + r * Es;
-      const double gf = G[local], gl = G[len + local];
-      const double pf = r > 0 ? Q[t] : 0.0, pl = r > 0 ? Q[C + t] : 0.0;
-      const double qf = r + 1 < nranks ? Q[2 * C + t] : 0.0;
-      const double ql = r + 1 < nranks ? Q[3 * C + t] : 0.0;
-      const double inv = 1.0 / (1.0 - pf * d);
-      e[r] = (gf + pf * cv) * inv;
-      hh[r] = qf * inv;
-      const double cn = gl + pl * cv + pl * d * e[r];
-      const double dn = pl * d * hh[r] + ql;
-      cc[r] = cv = cn;
-      dd[r] = d = dn;
+      gf[r] = G[local];
+      gl[r] = G[len + local];
     }
-    double F = 0.0, Lprev = 0.0, Fnext = 0.0;
-    for (int r = nranks - 1; r >= 0; --r) {
-      const double Fr = e[r] + hh[r] * F;
-      if (r == rank + 1) Fnext = Fr;
-      if (r == rank - 1) Lprev = cc[r] + dd[r] * F;
-      F = Fr;
+    double e[NR], hh[NR];
+    double cv = 0.0, cprev = 0.0, dprev = 0.0;  // (c, d) of rank - 1
+    auto fwd = [&](int r, const SlabStatic& s) {
+      e[r] = (gf[r] + s.pf * cv) * s.inv;
+      hh[r] = s.hh;
+      cv = gl[r] + s.pl * cv + s.pld * e[r];
+      if (r == rank - 1) {
+        cprev = cv;
+        dprev = s.dd;
+      }
+    };
+    if (same) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r) fwd(r, s0[r]);
+    } else {
+      double d = 0.0;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const SlabStatic s = slab_static(r, NR, coef + r * Es, C, t, d);
+        d = s.dd;
+        fwd(r, s);
+      }
     }
-    if (rank > 0) gb[o] = Lprev;
-    if (rank + 1 < nranks) gb[plane + o] = Fnext;
+    double F = 0.0, Frank = 0.0, Fnext = 0.0;
+#pragma unroll
+    for (int r = NR - 1; r >= 0; --r) {
+      F = e[r] + hh[r] * F;
+      if (r == rank + 1) Fnext = F;
+      if (r == rank) Frank = F;
+    }
+    if (rank > 0) gb[o] = cprev + dprev * Frank;
+    if (rank + 1 < NR) gb[plane + o] = Fnext;
   }
+}
+
+template <int NR>
+static void launch_interface_N(const Layout& L, int rank, const double* recv,
+                               const double* coef, long long Es, int J,
+                               const unsigned char* uni, const SlabStatic* g0, double* gb,
+                               int* dflag, cudaStream_t st) {
+  const dim3 grid((L.n2 - 2 + 127) / 128, L.n1 - 2);  // 128 registers: four blocks per SM
+  k_slab_interface<NR><<<grid, 128, 0, st>>>(L, rank, recv, coef, Es, J, uni, g0, gb, dflag);
+}
+
+static void launch_interface(int nranks, const Layout& L, int rank, const double* recv,
+                             const double* coef, long long Es, int J, const unsigned char* uni,
+                             const SlabStatic* g0, double* gb, int* dflag, cudaStream_t st) {
+#define PBG_IFACE(N) \
+  case N: launch_interface_N<N>(L, rank, recv, coef, Es, J, uni, g0, gb, dflag, st); break;
+  switch (nranks) {
+    PBG_IFACE(1) PBG_IFACE(2) PBG_IFACE(3) PBG_IFACE(4) PBG_IFACE(5) PBG_IFACE(6) PBG_IFACE(7)
+    PBG_IFACE(8) PBG_IFACE(9) PBG_IFACE(10) PBG_IFACE(11) PBG_IFACE(12) PBG_IFACE(13)
+    PBG_IFACE(14) PBG_IFACE(15) PBG_IFACE(16)
+  }
+#undef PBG_IFACE
 }
 
 }  // namespace pbg
@@ -149,6 +236,8 @@ struct pbg_slab {
   double* coef = nullptr;  // nranks exchange blocks: the gathered responses
   double* gbA = nullptr;   // ghost values of phase A: zeros (faces on the outer ranks)
   double* gbB = nullptr;   // ghost values of phase B: the neighbours' chunk end values
+  unsigned char* uni = nullptr;  // per interior line: responses equal line 0's on every rank
+  SlabStatic* s0 = nullptr;      // line 0's static interface elimination, per rank
   int* dflag = nullptr;
   int st_idx, st0, step;
   long long plane, C, Es, Eh;
@@ -198,6 +287,8 @@ extern "C" PBG_API int pbg_slab_destroy(pbg_slab* h, void* stream) {
   if (h->coef) cudaFreeAsync(h->coef, st);
   if (h->gbA) cudaFreeAsync(h->gbA, st);
   if (h->gbB) cudaFreeAsync(h->gbB, st);
+  if (h->uni) cudaFreeAsync(h->uni, st);
+  if (h->s0) cudaFreeAsync(h->s0, st);
   if (h->dflag) cudaFreeAsync(h->dflag, st);
   cudaStreamSynchronize(st);
   delete h;
@@ -263,6 +354,8 @@ extern "C" PBG_API int pbg_slab_create(const pbg_march_desc* d, int32_t rank, in
   bool ok = cu(cudaMallocAsync(&h->coef, nranks * h->Es * sizeof(double), st)) &&
             cu(cudaMallocAsync(&h->gbA, 2 * pb, st)) && cu(cudaMallocAsync(&h->gbB, 2 * pb, st)) &&
             cu(cudaMallocAsync(&h->dflag, sizeof(int), st)) &&
+            cu(cudaMallocAsync(&h->uni, (size_t)h->C, st)) &&
+            cu(cudaMallocAsync(&h->s0, kMaxRanks * sizeof(SlabStatic), st)) &&
             cu(cudaMallocAsync(&zeros, nelem * sizeof(double), st)) &&
             cu(cudaMallocAsync(&unit, 2 * pb, st)) &&
             cu(cudaMemsetAsync(zeros, 0, nelem * sizeof(double), st)) &&
@@ -330,6 +423,8 @@ extern "C" PBG_API int pbg_slab_setup(pbg_slab* h, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   PBG_CUDA(cudaMemcpyAsync(h->coef, h->recv, h->nranks * h->Es * sizeof(double),
                            cudaMemcpyDeviceToDevice, st));
+  k_slab_classify<<<148 * 4, 256, 0, st>>>(h->C, h->nranks, h->coef, h->Es, h->uni, h->s0);
+  PBG_LAUNCH_CHECK("k_slab_classify");
   return PBG_OK;
 }
 
@@ -419,8 +514,8 @@ extern "C" PBG_API int pbg_slab_step_b(pbg_slab* h, void* stream) {
   double *A, *Bf;
   const int other = slab_state(h, &X, &A, &Bf);
   const Layout L = make_layout(&h->d.grid);
-  k_slab_interface<<<148 * 4, 256, 0, st>>>(L, h->rank, h->nranks, h->recv, h->coef, h->Es,
-                                            h->J, h->gbB, h->dflag);
+  launch_interface(h->nranks, L, h->rank, h->recv, h->coef, h->Es, h->J, h->uni, h->s0,
+                   h->gbB, h->dflag, st);
   PBG_LAUNCH_CHECK("k_slab_interface");
   const int s = h->step + 1;
   for (int axis = 0; axis < 3; ++axis) {

@@ -2549,7 +2549,12 @@ static int env_int(const char* name, int dflt) {
   return e && *e ? atoi(e) : dflt;
 }
 
-static int seg_S(int m, int P) {
+static bool col_enabled();
+static int seg_S(int m, int P, int axis) {
+  if (P == 4) return m > 48 ? 16 : 12;
+  // 65..80-row lines of the strided axes (cost-weighted slab chunks): eight segments of 10
+  // rows instead of 12 (two idle segments per line); column sweeps only
+  if (P == 8 && axis < 2 && m > 64 && m <= 80 && col_enabled()) return 10;
   if (P == 16) return m <= 256 ? 16 : 0;  // instantiated: P = 8 with any S, 16/32 with 16/32
   if (P == 32) return m <= 512 ? 16 : (m <= 1024 ? 32 : 0);
   const int opts[] = {2, 3, 4, 6, 8, 12, 16, 24, 32};
@@ -2560,6 +2565,12 @@ static int seg_S(int m, int P) {
 // Strided axes: segments of ~16 rows (registers and occupancy balance, measured); the
 // contiguous axis always uses the 32 lanes of a warp.
 static int seg_P(int axis, int m) {
+  // 33..64-row lines of the strided axes (the axis-0 chunks of an 8-rank slab march at 513
+  // planes): four segments of 12 or 16 rows, sixteen 64-thread blocks per SM, instead of
+  // eight segments of 6 or 8 rows -- twice the rows in flight per thread and half the
+  // separators per line (PBG_P4=0 keeps the old shape, for comparison).
+  static const bool p4 = env_int("PBG_P4", 1) != 0;
+  if (p4 && axis < 2 && m > 32 && m <= 64 && col_enabled()) return 4;
   return m <= 128 ? 8 : (m <= 256 ? 16 : 32);
 }
 
@@ -2885,7 +2896,24 @@ static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
     PBG_LAUNCH_CHECK("k_sweep_rowwarp");
     return PBG_OK;
   }
-  const int P = seg_P(axis, a.m), S = seg_S(a.m, P);
+  const int P = seg_P(axis, a.m), S = seg_S(a.m, P, axis);
+  if (P == 4) {  // column sweeps only (seg_P)
+    if (S == 16) {
+      if (a.cn) launch_col<16, 4, true>(a, axis, st);
+      else launch_col<16, 4, false>(a, axis, st);
+    } else {
+      if (a.cn) launch_col<12, 4, true>(a, axis, st);
+      else launch_col<12, 4, false>(a, axis, st);
+    }
+    PBG_LAUNCH_CHECK("k_sweep_col");
+    return PBG_OK;
+  }
+  if (P == 8 && S == 10) {  // column sweeps only (seg_S)
+    if (a.cn) launch_col<10, 8, true>(a, axis, st);
+    else launch_col<10, 8, false>(a, axis, st);
+    PBG_LAUNCH_CHECK("k_sweep_col");
+    return PBG_OK;
+  }
   if (P == 8) {
 #define PBG_STRIDED8(S) launch_strided_SP<S, 8>(a, axis, st)
     PBG_DISPATCH_S(S, PBG_STRIDED8)
@@ -2917,7 +2945,7 @@ static int fused12_shape(const SweepArgs& a1, const SweepArgs& a2) {
   if (memcmp(&a1.co, &a2.co, sizeof(AxisCoef)) || memcmp(a1.tmid, a2.tmid, sizeof(a1.tmid)) ||
       a1.static_ok != a2.static_ok)
     return 0;
-  const int P = seg_P(1, a1.m), S = seg_S(a1.m, P);
+  const int P = seg_P(1, a1.m), S = seg_S(a1.m, P, 1);
   if (P != rowwarp_G(a2.m) || S != rowwarp_S(a2.m) || S != 16) return 0;
   return P == 16 || P == 32 ? P : 0;
 }
@@ -2969,7 +2997,7 @@ static bool fused01_ok(const SweepArgs& a0, const SweepArgs& a1) {
   if (a0.epi != EPI_STORE || a0.has_extra || a0.check) return false;
   if (a1.pro != PRO_NONE || a1.epi != EPI_STORE || a1.has_extra || a1.check) return false;
   const int P0 = seg_P(0, a0.m), P1 = seg_P(1, a1.m);
-  if (P0 != P1 || seg_S(a0.m, P0) != 16 || seg_S(a1.m, P1) != 16) return false;
+  if (P0 != P1 || seg_S(a0.m, P0, 0) != 16 || seg_S(a1.m, P1, 1) != 16) return false;
   return P0 == 16 || P0 == 32;
 }
 
@@ -3264,7 +3292,7 @@ int prepare_axis(SweepArgs& a, int axis, const uint8_t* codes, AxisAux& aux,
   a.rw = rowwarp_ok(a, axis) ? 1 : 0;
   if (a.rw && a.faces_ok && rowlean_ok(a) && !fused12_enabled()) a.rw = 2;
   const int P = a.rw ? rowwarp_G(a.m) : seg_P(axis, a.m);
-  const int S = a.rw ? rowwarp_S(a.m) : seg_S(a.m, P);
+  const int S = a.rw ? rowwarp_S(a.m) : seg_S(a.m, P, axis);
   const int lm = a.rw;
   if (S < 2) return fail(PBG_E_UNSUPPORTED, "line too long for the device sweep (m > 768)");
   std::vector<double> host(kTabDoubles + kSeg * (kSeg + 2), 0.0);

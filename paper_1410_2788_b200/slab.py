@@ -31,20 +31,80 @@ SLAB_SCHEMES = ("LODIE1", "LODIE2", "LODCN2")
 MAX_RANKS = 16
 
 
-def slab_ranges(n0: int, nranks: int):
-    """Owned global interior planes [first, stop) per rank: contiguous, sizes differ by <= 1."""
+def slab_ranges(n0: int, nranks: int, cost=None):
+    """Owned global interior planes [first, stop) per rank, contiguous.  Without `cost` the
+    sizes differ by <= 1.  With `cost` (one positive weight per interior plane, e.g.
+    `plane_costs`) the split minimises the largest per-rank cost sum: planes through the
+    molecule sweep slower (general segments, cyclic-reduction tiles, the wider flow tiers),
+    so the ranks holding it take fewer planes."""
     m = int(n0) - 2
     if not (1 <= nranks <= MAX_RANKS):
         raise ValueError(f"nranks must be in 1..{MAX_RANKS}")
     if m < nranks:
         raise ValueError(f"{m} interior planes cannot be split over {nranks} ranks")
-    base, extra = divmod(m, nranks)
+    if cost is None:
+        base, extra = divmod(m, nranks)
+        counts = [base + (1 if r < extra else 0) for r in range(nranks)]
+    else:
+        c = np.asarray(cost, dtype=np.float64)
+        if c.shape != (m,) or not np.all(c > 0) or not np.all(np.isfinite(c)):
+            raise ValueError("cost must hold one positive finite weight per interior plane")
+        counts = _balanced_counts(c, nranks)
     out, first = [], 1
-    for r in range(nranks):
-        cnt = base + (1 if r < extra else 0)
+    for cnt in counts:
         out.append((first, first + cnt))
         first += cnt
     return out
+
+
+def _balanced_counts(c, nranks):
+    """Contiguous split of the weights c into nranks non-empty parts with the smallest
+    possible largest part sum (bisection on the capacity, greedy fill)."""
+    m = len(c)
+
+    def fill(cap):
+        counts, i = [], 0
+        for r in range(nranks):
+            left = nranks - r - 1  # parts that still need a plane each
+            acc, n = 0.0, 0
+            while i < m - left and (n == 0 or acc + c[i] <= cap):
+                acc += c[i]
+                i += 1
+                n += 1
+            counts.append(n)
+        return counts if i == m else None
+
+    lo, hi = float(c.max()), float(c.sum())
+    for _ in range(60):
+        mid = 0.5 * (lo + hi)
+        if fill(mid) is None:
+            lo = mid
+        else:
+            hi = mid
+    return fill(hi)
+
+
+def slab_beta():
+    """Relative extra cost of a plane that is all solute, for `plane_costs` (measured on
+    config 4: planes with a ~10% solute cross-section run ~1.6x slower; PBG_SLAB_BETA
+    overrides, 0 = equal plane counts)."""
+    import os
+
+    return float(os.environ.get("PBG_SLAB_BETA", "6.0"))
+
+
+def plane_costs(dp, beta=None):
+    """Per interior plane weight 1 + beta * (solute fraction of the plane), from the device
+    region codes (bit 0 = solute).  None when beta == 0."""
+    beta = slab_beta() if beta is None else float(beta)
+    if beta == 0.0:
+        return None
+    n0, n1, n2 = dp.grid.shape
+    pitch, _ = nat.layout(dp.grid.shape)
+    plane = n1 * pitch
+    sol = (dp.codes[:n0 * plane].view(n0, plane) & 1).sum(dim=1, dtype=nat.torch_cuda().int64)
+    frac = sol[1:n0 - 1].double().cpu().numpy() / float((n1 - 2) * (n2 - 2))
+    return 1.0 + beta * frac
 
 
 SETUP, HALO, STEP = 0, 1, 2  # exchange phases (include/pbg.h PBG_SLAB_*)
@@ -247,27 +307,31 @@ def _check_variant(config: MarchConfig):
 
 
 def make_slabs(problem, config: MarchConfig, ranks, nranks: int, recv=None,
-               initial_dev=None):
-    """DeviceSlab objects for the given ranks of an `nranks`-way split of `problem`."""
+               initial_dev=None, beta=None):
+    """DeviceSlab objects for the given ranks of an `nranks`-way split of `problem`; the
+    split is cost weighted (`plane_costs`; every rank derives the same ranges from the same
+    region codes)."""
     v = _check_variant(config)
     dp = device_problem(problem)
     nsteps = max(1, int(round(config.T / config.dt)))
     init = initial_dev if initial_dev is not None else problem.initial._device()
-    rng = slab_ranges(problem.grid.shape[0], nranks)
+    rng = slab_ranges(problem.grid.shape[0], nranks, plane_costs(dp, beta))
     return [DeviceSlab(dp, v, config.dt, _resolve_alpha(config.alpha, problem), nsteps,
                        config.divergence_threshold, r, nranks, rng[r][0], rng[r][1], init,
                        recv=recv) for r in ranks], nsteps, v.startswith("LODCN")
 
 
-def march_partitioned(problem, config: MarchConfig, nparts: int) -> MarchReport:
+def march_partitioned(problem, config: MarchConfig, nparts: int, beta=None) -> MarchReport:
     """march() with the grid split into `nparts` slabs inside this process (one GPU,
-    exchange by device copy).  Same result as march() up to reassociation."""
+    exchange by device copy).  Same result as march() up to reassociation.  `beta`: weight
+    of the cost-balanced split (`plane_costs`; 0 = equal plane counts)."""
     torch = nat.torch_cuda()
     _check_variant(config)
     g = problem.grid
     E = int(nat.lib().pbg_slab_exchange_elems(ctypes.byref(_local_gs(g, 1))))
     recv = torch.empty(nparts * E, dtype=torch.float64, device="cuda")
-    parts, nsteps, cn = make_slabs(problem, config, range(nparts), nparts, recv=recv)
+    parts, nsteps, cn = make_slabs(problem, config, range(nparts), nparts, recv=recv,
+                                   beta=beta)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     res = run_slabs(parts, LocalExchange(), nsteps, cn)
@@ -303,5 +367,5 @@ def march_distributed(problem, config: MarchConfig, group=None):
     return taken, dstep, part, final
 
 
-__all__ = ["SLAB_SCHEMES", "slab_ranges", "run_slabs", "LocalExchange", "GroupExchange",
+__all__ = ["SLAB_SCHEMES", "slab_ranges", "plane_costs", "run_slabs", "LocalExchange", "GroupExchange",
            "DeviceSlab", "make_slabs", "march_partitioned", "march_distributed"]

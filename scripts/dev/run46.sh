@@ -1,0 +1,10 @@
+python -m pytest tests/test_gpu_slab.py -m gpu -x -q > gpurun_out/t46.log 2>&1; tail -3 gpurun_out/t46.log
+python scripts/dev/slab_model.py 8 queued > gpurun_out/slab46.jsonl 2>gpurun_out/slab46.err; cat gpurun_out/slab46.jsonl
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_slab" -c 100 --csv --log-file gpurun_out/slab_launches46.csv python scripts/dev/slab_model.py 8 > gpurun_out/ncu46.log 2>&1
+grep k_slab_interface gpurun_out/slab_launches46.csv | tail -3
+for R in 0 3; do
+ncu --set full --clock-control none --import-source on -k regex:k_sweep_rowlean -s $((64+R)) -c 1 -o gpurun_out/rowlean_rank$R python scripts/dev/slab_model.py 8 > gpurun_out/ncu46_$R.log 2>&1
+ncu -i gpurun_out/rowlean_rank$R.ncu-rep --page raw --csv > gpurun_out/rowlean_rank${R}_raw.csv 2>/dev/null
+ncu -i gpurun_out/rowlean_rank$R.ncu-rep --page source --csv --print-source cuda > gpurun_out/rowlean_rank${R}_src.csv 2>/dev/null
+done
+ls -la gpurun_out/rowlean_rank*

@@ -12,6 +12,10 @@ from paper_1410_2788_b200.configs import CONFIGS, cubic_box, kappa_bar, syntheti
 from paper_1410_2788_b200.problem import assemble_on_grid
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+# "queued": a ~150 us spin kernel runs ahead of every timed region, so the region's launches
+# are already queued when it starts (what a rank sees in steady state: the host runs ahead of
+# the device); without it every region starts on an idle stream and pays its launch latency.
+QUEUED = len(sys.argv) > 2 and sys.argv[2] == "queued"
 steps = 10
 c = CONFIGS["c4"]
 atoms = synthetic_atoms(c.n_atoms, c.ball_radius, c.seed)
@@ -36,6 +40,8 @@ tB = [0.0] * N
 for s in range(steps):
     for r, q in enumerate(parts):
         e0, e1 = ev(), ev()
+        if QUEUED:
+            torch.cuda._sleep(300000)
         e0.record()
         for ch in range(nc):
             q.step_a_chunk(ch)
@@ -47,6 +53,8 @@ for s in range(steps):
         ex.gather(parts, *parts[0].phase(S.STEP, ch))
     for r, q in enumerate(parts):
         e0, e1 = ev(), ev()
+        if QUEUED:
+            torch.cuda._sleep(300000)
         e0.record()
         q.step_b()
         e1.record()
@@ -55,7 +63,7 @@ for s in range(steps):
             tB[r] += e0.elapsed_time(e1)
 k = steps - 2
 step_bytes = sum(parts[0].phase(S.STEP, ch)[1] for ch in range(nc)) * 8
-out = {"ranks": N, "chunks": nc, "planes_per_rank": [q.stop - q.first for q in parts],
+out = {"ranks": N, "chunks": nc, "queued": QUEUED, "p4": os.environ.get("PBG_P4", "1"), "planes_per_rank": [q.stop - q.first for q in parts],
        "phaseA_ms": [round(t / k, 4) for t in tA], "phaseB_ms": [round(t / k, 4) for t in tB],
        "exchange_bytes_per_rank_per_step": step_bytes,
        "allgather_bytes_received_per_rank": step_bytes * (N - 1)}

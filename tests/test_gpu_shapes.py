@@ -1,4 +1,4 @@
-"""Ragged and extreme line lengths: every tile geometry (P = 8/16/32 segments, S from 2 to
+"""Ragged and extreme line lengths: every tile geometry (P = 4/8/16/32 segments, S from 2 to
 32, padding segments, row tiles, the longest supported line m = 1024, the single-node grid)
 against the CPU oracle on an off-centre dielectric sphere with a random sparse source and
 random Dirichlet faces; lines longer than 1024 interior nodes are refused loudly."""
@@ -13,7 +13,7 @@ from tests.helpers import rel_err
 pytestmark = pytest.mark.gpu
 
 SHAPES = [(3, 3, 3), (4, 5, 6), (18, 19, 20), (131, 10, 9), (9, 260, 11), (7, 8, 600),
-          (6, 390, 5), (1026, 5, 5)]
+          (6, 390, 5), (1026, 5, 5), (66, 9, 20), (8, 59, 21), (50, 7, 36), (77, 8, 30), (9, 70, 19)]
 VARIANTS = ["LODIE1", "LODCN2", "AOSCN1", "MAOSIE", "ADI2"]
 
 

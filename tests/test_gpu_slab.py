@@ -48,9 +48,11 @@ def test_partitioned_unsupported_variant(case):
         march_partitioned(p, pb.MarchConfig(dt=0.3, T=0.3, variant="AOSIE1"), 2)
 
 
-@pytest.mark.parametrize("variant,nparts", [("LODIE2", 8), ("LODCN2", 4)])
+@pytest.mark.parametrize("variant,nparts", [("LODIE2", 8), ("LODCN2", 4), ("LODIE2", 2),
+                                            ("LODCN2", 2)])
 def test_partitioned_config2_vs_single(variant, nparts):
-    """129^3, 500 atoms (config 2 grid): 8 slabs of 15-16 planes, 4 steps."""
+    """129^3, 500 atoms (config 2 grid): 8 slabs of 15-16 planes, 4 steps (2 slabs:
+    64- and 63-row axis-0 chunks, the four-segment column shape)."""
     from paper_1410_2788_b200.configs import CONFIGS, cubic_box, kappa_bar, synthetic_atoms
     from paper_1410_2788_b200.problem import assemble_on_grid
     from tests.helpers import system_of
@@ -66,3 +68,28 @@ def test_partitioned_config2_vs_single(variant, nparts):
     assert rep.steps_taken == 4
     assert rel_err(rep.final.data, single) <= 1e-12
     assert np.isfinite(rep.final.data).all()
+    # equal plane counts and a strongly cost-weighted split give the same field
+    for beta in (0.0, 40.0):
+        rep = march_partitioned(p, cfg, nparts, beta=beta)
+        assert rel_err(rep.final.data, single) <= 1e-12, beta
+
+
+def test_cost_weighted_ranges_follow_the_molecule():
+    """The ranks holding the molecule get fewer planes; beta = 0 keeps equal counts."""
+    from paper_1410_2788_b200.configs import CONFIGS, cubic_box, kappa_bar, synthetic_atoms
+    from paper_1410_2788_b200.problem import assemble_on_grid
+    from paper_1410_2788_b200.schemes import device_problem
+    from paper_1410_2788_b200.slab import plane_costs, slab_ranges
+    from tests.helpers import system_of
+
+    c = CONFIGS["c2"]
+    atoms = synthetic_atoms(c.n_atoms, c.ball_radius, c.seed)
+    lo, hi = cubic_box(atoms, c.n, c.h)
+    p = assemble_on_grid(system_of(atoms), pb.make_grid(lo, hi, c.h),
+                         kappa_bar(c.ionic_strength), c.eps_m, c.eps_s)
+    dp = device_problem(p)
+    assert plane_costs(dp, 0.0) is None
+    cost = plane_costs(dp, 6.0)
+    assert cost.shape == (c.n - 2,) and cost.min() >= 1.0 and cost.max() > 1.2
+    sizes = [b - a for a, b in slab_ranges(c.n, 4, cost)]
+    assert sum(sizes) == c.n - 2 and sizes[1] < sizes[0] and sizes[2] < sizes[3]

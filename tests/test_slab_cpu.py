@@ -33,6 +33,20 @@ def test_slab_ranges_cover_interior_contiguously():
             sizes = [b - a for a, b in rng]
             assert min(sizes) >= 1 and max(sizes) - min(sizes) <= 1
     assert [b - a for a, b in slab_ranges(513, 8)] == [64] * 7 + [63]
+    # cost-weighted split: contiguous cover, the expensive planes end up in smaller slabs,
+    # the largest per-rank cost is optimal for this small case, uniform weights = equal counts
+    cost = np.ones(30)
+    cost[12:18] = 5.0
+    rng = slab_ranges(32, 4, cost)
+    assert rng[0][0] == 1 and rng[-1][1] == 31
+    assert all(rng[r][1] == rng[r + 1][0] for r in range(3))
+    sums = [cost[a - 1:b - 1].sum() for a, b in rng]
+    assert max(sums) <= 15.0 + 1e-9  # total 54 over 4 ranks: 13.5 is a lower bound, 15 reachable
+    assert [b - a for a, b in slab_ranges(32, 4, np.ones(30))] in ([8, 8, 7, 7], [8, 7, 8, 7],
+                                                                  [8, 8, 8, 6], [7, 8, 8, 7])
+    assert all(b > a for a, b in slab_ranges(7, 5, np.array([9.0, 1, 1, 1, 1])))
+    with pytest.raises(ValueError):
+        slab_ranges(32, 4, np.ones(29))
     with pytest.raises(ValueError):
         slab_ranges(5, 4)
     with pytest.raises(ValueError):
