@@ -2555,6 +2555,10 @@ static int seg_S(int m, int P, int axis) {
   // 65..80-row lines of the strided axes (cost-weighted slab chunks): eight segments of 10
   // rows instead of 12 (two idle segments per line); column sweeps only
   if (P == 8 && axis < 2 && m > 64 && m <= 80 && col_enabled()) return 10;
+  // 129..192-row lines of the strided axes (cost-weighted slab chunks at four ranks): sixteen
+  // segments of 10 or 12 rows instead of 16 (up to seven idle segments per line); column
+  // sweeps only
+  if (P == 16 && axis < 2 && m > 128 && m <= 192 && col_enabled()) return m <= 160 ? 10 : 12;
   if (P == 16) return m <= 256 ? 16 : 0;  // instantiated: P = 8 with any S, 16/32 with 16/32
   if (P == 32) return m <= 512 ? 16 : (m <= 1024 ? 32 : 0);
   const int opts[] = {2, 3, 4, 6, 8, 12, 16, 24, 32};
@@ -2918,6 +2922,16 @@ static int launch_strided(const SweepArgs& a, int axis, cudaStream_t st) {
 #define PBG_STRIDED8(S) launch_strided_SP<S, 8>(a, axis, st)
     PBG_DISPATCH_S(S, PBG_STRIDED8)
 #undef PBG_STRIDED8
+  } else if (P == 16 && S == 10) {  // column sweeps only (seg_S)
+    if (a.cn) launch_col<10, 16, true>(a, axis, st);
+    else launch_col<10, 16, false>(a, axis, st);
+    PBG_LAUNCH_CHECK("k_sweep_col");
+    return PBG_OK;
+  } else if (P == 16 && S == 12) {
+    if (a.cn) launch_col<12, 16, true>(a, axis, st);
+    else launch_col<12, 16, false>(a, axis, st);
+    PBG_LAUNCH_CHECK("k_sweep_col");
+    return PBG_OK;
   } else if (P == 16 && S == 16) {
     launch_strided_SP<16, 16>(a, axis, st);
   } else if (P == 32 && S == 16) {

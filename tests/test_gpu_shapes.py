@@ -13,7 +13,7 @@ from tests.helpers import rel_err
 pytestmark = pytest.mark.gpu
 
 SHAPES = [(3, 3, 3), (4, 5, 6), (18, 19, 20), (131, 10, 9), (9, 260, 11), (7, 8, 600),
-          (6, 390, 5), (1026, 5, 5), (66, 9, 20), (8, 59, 21), (50, 7, 36), (77, 8, 30), (9, 70, 19)]
+          (6, 390, 5), (1026, 5, 5), (66, 9, 20), (8, 59, 21), (50, 7, 36), (77, 8, 30), (9, 70, 19), (152, 6, 20), (7, 180, 18)]
 VARIANTS = ["LODIE1", "LODCN2", "AOSCN1", "MAOSIE", "ADI2"]
 
 
