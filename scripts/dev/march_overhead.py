@@ -1,6 +1,6 @@
 """Dev tool: host overhead of one march() call at config-5 size."""
 import sys, os, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_1410_2788_b200 as pb
 from paper_1410_2788_b200.batch import config5_problem

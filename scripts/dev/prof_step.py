@@ -1,6 +1,6 @@
 """Minimal profiling driver: assemble a config, march a few steps (dev tool for ncu)."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_1410_2788_b200 as pb
 from paper_1410_2788_b200.configs import CONFIGS, synthetic_atoms, cubic_box, kappa_bar
 from paper_1410_2788_b200.problem import assemble_on_grid

@@ -1,6 +1,6 @@
 """Quick device timing of the step and of each sweep kernel at config sizes (dev tool)."""
 import ctypes, sys, time, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_1410_2788_b200 as pb
 from paper_1410_2788_b200 import _native as nat
 from paper_1410_2788_b200.configs import CONFIGS, synthetic_atoms, cubic_box, kappa_bar

@@ -1,7 +1,7 @@
 """Dev tool: per-kernel timing on the vacuum (uniform dielectric) version of a config, to
 separate the cost of general (dielectric-crossing) segments from the uniform path."""
 import ctypes, sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_1410_2788_b200 as pb
 from paper_1410_2788_b200 import _native as nat
 from paper_1410_2788_b200.configs import CONFIGS, synthetic_atoms, cubic_box, kappa_bar
