@@ -2105,14 +2105,48 @@ __global__ void __launch_bounds__(NW * 32, 1)
       for (int q = 0; q < S; q += 2)
         *reinterpret_cast<double2*>(W + uoff(q >> 1)) = make_double2(r[q], r[q + 1]);
     }
-    if (FLOWK == 3 && valid) {  // the other rows, one at a time, in the buffer
+    if (FLOWK == 3) {
+      // The other rows, from the buffer, spread over the whole warp: they cluster in the few
+      // lanes whose segment lies in a pocket of the molecule (|w| > 2 next to the charges), and
+      // a lane-private loop ran as long as the fullest lane while the others idled.  Lane
+      // counts are prefix-summed, item i belongs to the lane whose running count first
+      // exceeds i (binary search in the warp's scratch) and is that lane's (i - before)-th
+      // needed row; any lane can reach it because the rows sit in shared memory.
+      const unsigned nd = valid ? need : 0u;
+      if (__any_sync(FULL, nd != 0u)) {
+        unsigned short* sc = reinterpret_cast<unsigned short*>(sRb + warp * NL * (G + 2));
+        int incl = __popc(nd);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int v = __shfl_up_sync(FULL, incl, d);
+          if (lane >= d) incl += v;
+        }
+        const int total = __shfl_sync(FULL, incl, 31);
+        sc[lane] = (unsigned short)incl;
+        sc[32 + lane] = (unsigned short)nd;
+        sc[64 + lane] = (unsigned short)sbits;
+        if (BATCH) sc[96 + lane] = (unsigned short)c0.b;  // the owner's grid (divergence flag)
+        __syncwarp();
 #pragma unroll 1
-      for (unsigned nm = need; nm; nm &= nm - 1) {
-        const int u = __ffs(nm) - 1;
-        double* slot = W + (uoff(u >> 1) | (u & 1));
-        const double x = flow_sm(a, FP, *slot, (sbits >> u) & 1u, 1.0);
-        *slot = x;
-        lbad |= !(fabs(x) <= thrc);
+        for (int i = lane; i < total; i += 32) {
+          int o = 0;
+#pragma unroll
+          for (int step = 16; step; step >>= 1)
+            if ((int)sc[o + step - 1] <= i) o += step;
+          const int before = o ? (int)sc[o - 1] : 0;
+          const int u = __fns((unsigned)sc[32 + o], 0, i - before + 1);
+          const int oseg = o % G;
+          const int uo = S == 16 ? (oseg << 4) | (((u >> 1) ^ (oseg & 7)) << 1)
+                                 : lean_unit(oseg * (S / 2) + (u >> 1));
+          double* slot = Lb + warp * NB * WB + (o / G) * LDP + b * WB + (uo | (u & 1));
+          const double x = flow_sm(a, FP, *slot, ((unsigned)sc[64 + o] >> u) & 1u, 1.0);
+          *slot = x;
+          if (BATCH) {
+            if (a.check && !(fabs(x) <= thrc)) atomicMin(a.div_step + sc[96 + o], a.step);
+          } else {
+            lbad |= !(fabs(x) <= thrc);
+          }
+        }
       }
     }
     if (BATCH) {  // the line's own grid (the lines of a warp may belong to different grids)
