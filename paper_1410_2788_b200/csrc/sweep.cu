@@ -1069,6 +1069,13 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
     } else {
       amask = *dp;
     }
+    if (const unsigned long long slot = amask >> kSlotShift) {
+      // a general segment's factor tables (five 120-byte rows, L2 resident) start towards L1
+      // while the rows load: the elimination reads them on its dependent chain
+      const double* tp = a.gfac + (long long)(slot - 1ull) * 5 * kTabRows;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + q * kTabRows));
+    }
   }
   double r[S];
   const double* srow = a.src + gl + (long long)(i0 + 1) * st;
