@@ -1069,13 +1069,6 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
     } else {
       amask = *dp;
     }
-    if (const unsigned long long slot = amask >> kSlotShift) {
-      // a general segment's factor tables (five 120-byte rows, L2 resident) start towards L1
-      // while the rows load: the elimination reads them on its dependent chain
-      const double* tp = a.gfac + (long long)(slot - 1ull) * 5 * kTabRows;
-#pragma unroll
-      for (int q = 0; q < 5; ++q) asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + q * kTabRows));
-    }
   }
   double r[S];
   const double* srow = a.src + gl + (long long)(i0 + 1) * st;
@@ -1099,6 +1092,17 @@ __global__ void __launch_bounds__(LB * kSegS, S >= 32 ? 1 : 1024 / (LB * kSegS))
   if (act) {
     if (threadIdx.y == 0) bfold = a.bnd[gl];
     else if ((int)threadIdx.y == (m - 1) / S) bfold = a.bnd[gl + a.hi_off];
+  }
+  if (act) {
+    // A general segment's factor tables (five 120-byte rows, L2 resident) start towards L1
+    // while the rows load: the elimination reads them on its dependent chain.  After the other
+    // loads in program order: the test waits for the descriptor, and ahead of them it held
+    // the row loads back by that latency (slab phase A +10%, config 5 +3%).
+    if (const unsigned long long slot = amask >> kSlotShift) {
+      const double* tp = a.gfac + (long long)(slot - 1ull) * 5 * kTabRows;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + q * kTabRows));
+    }
   }
   if (!PLAIN && epi_needs(a.epi) == 2 && act) {  // accumulator rows of the AOS / MAOS epilogue: on their
                                        // way to L1 while the line is solved
