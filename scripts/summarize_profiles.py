@@ -109,3 +109,16 @@ open(os.path.join(out, f"ncu_{tag}_summary.md"), "w").write("\n".join(md) + "\n"
 tr["_note"] = f"dram read+write bytes per launch by sweep axis, ncu --set full captures {tag}"
 json.dump(tr, open(os.path.join(out, "ncu_traffic.json"), "w"), indent=1)
 print("\n".join(md))
+
+# slab model lines (scripts/dev/collect_final.sh): add the split's beta and the per-rank totals
+sm = os.path.join(go, f"slab_model_{tag}.jsonl")
+if os.path.exists(sm):
+    with open(os.path.join(out, f"slab_model_{tag}.jsonl"), "w") as f:
+        for ln in open(sm):
+            r = json.loads(ln)
+            sizes = r["planes_per_rank"]
+            r["beta"] = 0 if max(sizes) - min(sizes) <= 1 else 6
+            r["total_ms"] = [round(a + b, 4) for a, b in zip(r["phaseA_ms"], r["phaseB_ms"])]
+            f.write(json.dumps(r) + "\n")
+            print(r["ranks"], r["beta"], sizes, "A", min(r["phaseA_ms"]), max(r["phaseA_ms"]), "B",
+                  min(r["phaseB_ms"]), max(r["phaseB_ms"]), "slowest", max(r["total_ms"]))
